@@ -1,0 +1,215 @@
+/*
+ * rank1_b200.h — C-ABI of the B200-native HOSCF / iHOSCF hot path.
+ *
+ * This is the drop-in boundary between a host driver (the C++ `rank1::` API in
+ * include/rank1/, a Python ctypes mirror, or a foreign FFI) and the sm_100a
+ * kernels.  Every entry point is `extern "C"`, takes plain pointers and sizes,
+ * returns an `int` status and never lets a C++ exception cross.  No torch or
+ * CUDA types appear in the signatures; device pointers are `double*` that live
+ * on the context's device and streams are passed as `void*` (a cudaStream_t).
+ *
+ * Layout conventions follow the reference (proj/include/rank1/tensor.hpp:11-14,
+ * matrix.hpp:10): tensors are column-major with the FIRST index fastest; a
+ * factor set is passed "flat" as u(0) ++ u(1) ++ ... ++ u(d-1) (length sum I_k,
+ * the StackedVector block order of stacked.hpp:11-12); the symmetric block
+ * matrix J is passed as its strictly-upper blocks B(m,n), m<n, concatenated in
+ * the reference's pair order (nepv.cpp:98-102: (0,1),(0,2),...,(0,d-1),(1,2),...),
+ * each block column-major I_m x I_n (mode m = rows).  J = (1/(d-1)) [B] as in
+ * nepv.cpp:91.
+ *
+ * Status codes map 1:1 onto the reference's exception types:
+ *   R1_ERR_INVALID_ARGUMENT  <-> std::invalid_argument
+ *   R1_ERR_RUNTIME           <-> std::runtime_error (zero factor, failure after
+ *                                restart, eigen non-convergence)
+ *   R1_ERR_CUDA / R1_ERR_NO_DEVICE  new: device failures; there is NO CPU fallback.
+ * r1_last_error() returns the (thread-local) message of the last failure, with
+ * the reference's wording where one exists.
+ */
+#ifndef RANK1_B200_H
+#define RANK1_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define R1_ABI_VERSION 1
+
+#define R1_OK 0
+#define R1_ERR_INVALID_ARGUMENT 1
+#define R1_ERR_RUNTIME 2
+#define R1_ERR_CUDA 3
+#define R1_ERR_NO_DEVICE 4
+#define R1_ERR_INTERNAL 5
+
+/* enum values mirror proj/include/rank1/solvers.hpp:13-15 */
+#define R1_INIT_UNIFORM01 0
+#define R1_INIT_PROVIDED 1
+#define R1_RQI_MAGNITUDE 0
+#define R1_RQI_SIGNED_INCREASE 1
+#define R1_STOP_KKT 0
+#define R1_STOP_EQ11 1
+#define R1_STOP_LAMBDA_DELTA 2
+
+typedef struct r1_context r1_context; /* device, stream, events, workspaces   */
+typedef struct r1_tensor r1_tensor;   /* a dense order-d tensor resident in HBM */
+
+/* Mirrors rank1::SolveOptions (solvers.hpp:17-31), same defaults via
+ * r1_solve_options_default().  `init_factors` is flat (sum I_k) or NULL. */
+typedef struct r1_solve_options {
+    double tol;
+    int32_t max_iters;
+    int32_t init;
+    uint64_t seed;
+    const double* init_factors;
+    int32_t determinism;
+    int32_t rqi_accept_rule;
+    int32_t stop_rule;
+    int32_t threads;
+    int32_t record_kkt;
+    int32_t asvd_disjoint_pairs;
+    int32_t reuse_intermediates;
+    /* Extension (not in the reference): when nonzero the SCF solvers also stop
+     * once |lambda_k - lambda_{k-1}| <= scf_lambda_rtol * |lambda_k|
+     * (BASELINE config 1's "relative sigma change" rule).  0 = reference
+     * behaviour (Eq. 11 residual only, solvers.cpp:175-178). */
+    double scf_lambda_rtol;
+} r1_solve_options;
+
+/* Mirrors rank1::IterationRecord (solvers.hpp:33-43). */
+typedef struct r1_iteration_record {
+    double lambda;
+    double stop_value;
+    double eq11_value;
+    double kkt_max_residual;
+    int32_t rqi_accepted;
+    int32_t n_sweeps;      /* extension: build_j sweeps charged to this iteration */
+    double lambda_pre_rqi;
+    double t_build_j;      /* seconds, CUDA events on the solver stream          */
+    double t_eig;
+    double t_other;
+} r1_iteration_record;
+
+/* Mirrors rank1::SolveReport (solvers.hpp:45-58).  The caller owns every
+ * array: `factors` and `final_x` hold sum I_k doubles, `trace` holds
+ * max_iters records. */
+typedef struct r1_solve_report {
+    double lambda;
+    double* factors;
+    int32_t converged;
+    int32_t iterations;
+    double lambda0;
+    int32_t restarted;
+    double* final_x;
+    r1_iteration_record* trace;
+    /* extension: device-measured totals */
+    int32_t total_sweeps;
+    double t_total;        /* seconds around the whole solve (events)           */
+} r1_solve_report;
+
+/* ---- library / context ------------------------------------------------ */
+int r1_abi_version(void);
+const char* r1_last_error(void);
+int r1_device_count(int* n);
+void r1_solve_options_default(r1_solve_options* o);
+
+int r1_context_create(int device, r1_context** out);
+int r1_context_destroy(r1_context* ctx);
+/* Use a caller-owned cudaStream_t (e.g. torch's current stream) for every
+ * subsequent launch on this context; NULL restores the context's own stream. */
+int r1_context_set_stream(r1_context* ctx, void* cuda_stream);
+int r1_context_synchronize(r1_context* ctx);
+/* Kernel launches issued on this context since creation (evidence counter). */
+int r1_context_launch_count(const r1_context* ctx, uint64_t* count);
+
+/* ---- tensors ------------------------------------------------------------- */
+/* Allocate a device tensor (16-byte aligned, padded) and copy `host` into it. */
+int r1_tensor_from_host(r1_context* ctx, const double* host, const uint64_t* dims, int order,
+                        r1_tensor** out);
+/* Allocate without copying (values undefined). */
+int r1_tensor_create(r1_context* ctx, const uint64_t* dims, int order, r1_tensor** out);
+/* Wrap caller-owned device memory (no copy, not freed).  `dev` must be 16-byte
+ * aligned and readable up to 16*ceil(8N/16) bytes. */
+int r1_tensor_wrap_device(r1_context* ctx, const double* dev, const uint64_t* dims, int order,
+                          r1_tensor** out);
+/* Asynchronous H2D of the full tensor on the context stream. */
+int r1_tensor_copy_from_host(r1_context* ctx, r1_tensor* t, const double* host);
+int r1_tensor_destroy(r1_tensor* t);
+double* r1_tensor_device_ptr(const r1_tensor* t);
+
+/* ---- sizes ----------------------------------------------------------------- */
+/* Number of doubles of the concatenated upper blocks: sum_{m<n} I_m I_n. */
+uint64_t r1_blocks_numel(const uint64_t* dims, int order);
+
+/* ---- the TTVc sweep (replaces rank1::build_j, nepv.hpp:58 / nepv.cpp:199-231)
+ * Device-pointer form, asynchronous on the context stream.  `factors_dev` is
+ * flat (sum I_k), `blocks_dev` receives all P = d(d-1)/2 blocks (pair order),
+ * `fro2_dev` (nullable) receives sum over blocks of sum of squared entries
+ * (||J||_F = sqrt(2*fro2)/(d-1), nepv.cpp:152-157).  Factors are NOT validated
+ * here (use r1_build_j for the reference's checks).  Deterministic: fixed
+ * reduction order, no atomics; identical inputs give identical bits. */
+int r1_build_j_device(r1_context* ctx, const r1_tensor* a, const double* factors_dev,
+                      double* blocks_dev, double* fro2_dev);
+
+/* Host form with the reference's argument checks (nepv.cpp:24-41, 199-207):
+ * order>=2 (invalid_argument), factor lengths (invalid_argument), for d>2 every
+ * factor nonzero (runtime_error "degenerate factor set: zero factor for mode k")
+ * and unit to 1e-8 (invalid_argument).  `a_host` is copied to the device on
+ * every call unless `a_dev` (nullable) is given.  Blocks are returned to host. */
+int r1_build_j(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
+               const uint64_t* dims, int order, const double* factors_host, double* blocks_host);
+
+/* One block B(m,n) (replaces rank1::build_block, nepv.hpp:54 / nepv.cpp:159-170);
+ * m>n is swapped as in the reference; only the contracted factors are checked. */
+int r1_build_block(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
+                   const uint64_t* dims, int order, const double* factors_host, int m, int n,
+                   double* block_host);
+
+/* ---- block-matrix operations (nepv.cpp:110-157, 249-282) ------------------ */
+/* y = J x (scale included), device pointers, async. */
+int r1_block_matvec_device(r1_context* ctx, const uint64_t* dims, int order,
+                           const double* blocks_dev, const double* x_dev, double* y_dev);
+/* Eq. 11: ||Jx - rho x|| / (||J||_F + |lambda|), rho = x'Jx (nepv.cpp:271-282).
+ * Host form: blocks/x on host, result to *out. */
+int r1_scf_stopping_value(r1_context* ctx, const uint64_t* dims, int order,
+                          const double* blocks_host, const double* x_host, double lambda,
+                          double* out);
+/* KKT report derived from the blocks of J(u) (no tensor pass):
+ * w_n = B(n,m) u_m, lambda = u_0' B(0,1) u_1, residual_n = ||w_n - lambda u_n||.
+ * out: [lambda, max_residual, residual_0..residual_{d-1}] (d+2 doubles). */
+int r1_kkt_from_blocks(r1_context* ctx, const uint64_t* dims, int order,
+                       const double* blocks_host, const double* factors_host, double* out);
+/* kkt_report(A,f) (nepv.hpp:72): one sweep + the block identities above. */
+int r1_kkt_report(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
+                  const uint64_t* dims, int order, const double* factors_host, double* out);
+
+/* ---- eigen steps (sym_eig.hpp:30, 37-38) ------------------------------------ */
+/* Largest-magnitude eigenpair of the block matrix J (Lanczos on device, both
+ * spectral ends converged; reference pick rule sym_eig.cpp:214-216 and sign
+ * canonicalisation :223-227).  x0_dev (nullable) warm-starts. */
+int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order,
+                         const double* blocks_dev, const double* x0_dev, double* value_dev,
+                         double* vec_dev);
+/* Same for a dense symmetric n x n matrix given on the host (column-major). */
+int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_host,
+                                   double* value, double* vec);
+/* One Rayleigh-quotient step (sym_eig.cpp:411-438) on device: Bunch-Kaufman
+ * LDL^T of S - rho I, diag-condition rejection (>1e14), one shift bump.
+ * *accepted = 0 reproduces std::nullopt. */
+int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host,
+                              const double* x_host, double* y_host, int* accepted);
+
+/* ---- solvers (solvers.hpp:63-88) -------------------------------------------- */
+/* algorithm: "hoscf" | "ihoscf".  Other reference names are rejected with
+ * R1_ERR_INVALID_ARGUMENT ("unknown solver" for unknown names, "not on the
+ * device path" for the CPU baselines): there is no CPU fallback. */
+int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
+             const r1_solve_options* opts, r1_solve_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANK1_B200_H */

@@ -1,0 +1,179 @@
+// Shared host/device plumbing for the B200 HOSCF path: error handling across
+// the C-ABI, the device context (stream, events, workspace arena, launch
+// counter) and small PTX helpers.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rank1_b200.h"
+
+namespace r1 {
+
+// ------------------------------------------------------------------ errors --
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        char buf[512];
+        snprintf(buf, sizeof(buf), "CUDA error %s (%d) in %s at %s:%d", cudaGetErrorString(e),
+                 static_cast<int>(e), what, file, line);
+        fail(R1_ERR_CUDA, buf);
+    }
+}
+#define R1_CUDA(x) ::r1::cuda_check((x), #x, __FILE__, __LINE__)
+
+void set_last_error(const std::string& msg);
+
+// Runs f, mapping exceptions onto the ABI status codes (never throws).
+template <typename F>
+int abi_guard(F&& f) {
+    try {
+        f();
+        return R1_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        set_last_error(e.what());
+        return R1_ERR_INVALID_ARGUMENT;
+    } catch (const std::bad_alloc& e) {
+        set_last_error("out of memory");
+        return R1_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return R1_ERR_RUNTIME;
+    } catch (...) {
+        set_last_error("unknown error");
+        return R1_ERR_INTERNAL;
+    }
+}
+
+// ---------------------------------------------------------- device buffers --
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    DeviceBuffer() = default;
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    ~DeviceBuffer() {
+        if (ptr) cudaFree(ptr);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (ptr) R1_CUDA(cudaFree(ptr));
+        ptr = nullptr;
+        bytes = 0;
+        R1_CUDA(cudaMalloc(&ptr, b));
+        bytes = b;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
+struct PinnedBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ~PinnedBuffer() {
+        if (ptr) cudaFreeHost(ptr);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (ptr) R1_CUDA(cudaFreeHost(ptr));
+        ptr = nullptr;
+        bytes = 0;
+        R1_CUDA(cudaMallocHost(&ptr, b));
+        bytes = b;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
+struct SweepPlan;  // sweep.cu
+
+}  // namespace r1
+
+struct r1_tensor {
+    r1_context* ctx = nullptr;
+    std::vector<uint64_t> dims;
+    uint64_t numel = 0;
+    double* dev = nullptr;
+    bool owned = false;
+};
+
+struct r1_context {
+    int device = 0;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    // Workspace arena, grow-only: sweeps, eigen solver, RQI.
+    r1::DeviceBuffer ws_sweep;
+    r1::DeviceBuffer ws_eig;
+    r1::DeviceBuffer ws_rqi;
+    r1::DeviceBuffer ws_small;   // factors, scalars, flags
+    r1::PinnedBuffer pinned;     // small host staging
+    std::map<std::vector<uint64_t>, std::shared_ptr<r1::SweepPlan>> plans;
+};
+
+namespace r1 {
+
+inline void count_launch(r1_context* ctx, uint64_t n = 1) { ctx->launches += n; }
+
+inline void check_launch(r1_context* ctx, const char* what) {
+    count_launch(ctx);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) cuda_check(e, what, __FILE__, __LINE__);
+}
+
+inline uint64_t numel_of(const uint64_t* dims, int order) {
+    uint64_t n = 1;
+    for (int k = 0; k < order; ++k) n *= dims[k];
+    return n;
+}
+
+inline uint64_t blocks_numel(const uint64_t* dims, int order) {
+    uint64_t s = 0;
+    for (int m = 0; m < order; ++m)
+        for (int n = m + 1; n < order; ++n) s += dims[m] * dims[n];
+    return s;
+}
+
+// Offset of block (m,n), m<n, in the concatenated pair order (nepv.cpp:98-102).
+inline uint64_t block_offset(const uint64_t* dims, int order, int m, int n) {
+    uint64_t s = 0;
+    for (int a = 0; a < order; ++a)
+        for (int b = a + 1; b < order; ++b) {
+            if (a == m && b == n) return s;
+            s += dims[a] * dims[b];
+        }
+    return s;
+}
+
+// --------------------------------------------------------- component APIs --
+// sweep.cu
+void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int order,
+                  const double* factors_dev, double* blocks_dev);
+// blockops.cu
+void sumsq_device(r1_context* ctx, const double* x, uint64_t n, double* out_dev);
+void block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
+                  const double* x, double* y);
+
+}  // namespace r1

@@ -1,0 +1,694 @@
+// The fused TTVc sweep: every NEPv block B(m,n) = A x_{k not in {m,n}} u_k of
+// J(u) from ONE streaming pass over the tensor per recursion level.
+//
+// Replaces rank1::build_j (reference proj/src/nepv.cpp:199-231), which builds
+// each of the P = d(d-1)/2 blocks by its own TTV chain over the whole tensor
+// (contract_to_block, nepv.cpp:46-77; ttv, tensor.cpp:100-138), i.e. P full
+// passes over A.
+//
+// Design:
+//   View A (column-major, first index fastest) as A[i0, i1, o] with o the
+//   linear index of modes 2..d-1 and outer weight W[o] = prod_{k>=2} u_k[i_k].
+//   One pass over A produces
+//     B01[i0,i1] = sum_o A[i0,i1,o] W[o]          (= block (0,1))
+//     C0[i0,o]   = sum_i1 A[i0,i1,o] u1[i1]       (= A x_1 u1, order d-1)
+//     C1[i1,o]   = sum_i0 A[i0,i1,o] u0[i0]       (= A x_0 u0, order d-1)
+//   For d = 3 these ARE blocks (0,1), (0,2), (1,2).  For d >= 4 the remaining
+//   blocks are the blocks of C0 (modes 0,2,..) and the (0,k) blocks of C1
+//   (modes 1,2,..) — the same problem one order lower on tensors I1x (resp.
+//   I0x) smaller, handled by recursion (the reference's reuse_intermediates
+//   idea, nepv.cpp:174-195, applied to the fused pass).
+//
+// Kernel: persistent, one CTA per SM; the CTA owns a face tile (r0 x t1 of
+// (i0,i1)) and a contiguous run of o.  A producer warp streams the tile's
+// column runs HBM -> shared memory with cp.async.bulk (TMA bulk copies,
+// L2 evict_first) into a STAGES-deep ring guarded by mbarriers; 8 consumer
+// warps keep the B01 face tile in registers, reduce C1 with a transposing warp
+// butterfly and C0 through shared memory.  C0/C1 partials over face tiles go
+// to a workspace and are summed in a fixed order by a second kernel: no
+// atomics anywhere, so results are bit-reproducible run to run.
+#include "common.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace r1 {
+
+namespace {
+
+constexpr int kNWC = 8;                    // consumer warps
+constexpr int kThreads = (kNWC + 1) * 32;  // + one producer warp
+constexpr int kMaxOrder = 16;
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+struct Seg {
+    int tile;
+    int o0;
+    int o1;
+    int pad;
+};
+
+struct SweepArgs {
+    const double* A;
+    int64_t I0, I1, O;
+    const double* u0;
+    const double* u1;
+    const double* W;
+    int r0, t1, G0;
+    const Seg* segs;
+    const int* cta_seg;
+    double* P01;            // [nseg][t1][r0]
+    double* P0;             // [G1] copies of I0 x O, stride P0_stride
+    int64_t P0_stride;
+    double* P1;             // [G0] copies of I1 x O, stride P1_stride (nullptr: skip)
+    int64_t P1_stride;
+};
+
+// ------------------------------------------------------------- PTX helpers --
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void consumer_bar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kNWC * 32) : "memory");
+}
+
+// After the call lane L holds the 32-lane sum of v[col], col = *col_out, for
+// NV = 2^L values per lane: L halving levels (offsets 16, 8, ...) exchange
+// half the values each, the remaining offsets reduce the single survivor.
+template <int NV>
+__device__ __forceinline__ double warp_transpose_sum(double (&v)[NV], int lane, int* col_out) {
+    int col = 0;
+    int off = 16;
+#pragma unroll
+    for (int half = NV / 2; half >= 1; half >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int q = 0; q < half; ++q) {
+            const double send = upper ? v[q] : v[q + half];
+            const double keep = upper ? v[q + half] : v[q];
+            v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+        if (upper) col += half;
+        off >>= 1;
+    }
+    double r = v[0];
+#pragma unroll
+    for (; off >= 1; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+    *col_out = col;
+    return r;
+}
+
+// --------------------------------------------------------------- the sweep --
+template <int NRA, int NCB, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1) sweep3_kernel(const SweepArgs p) {
+    constexpr int RMAX = 32 * NRA;
+    constexpr int CS = RMAX + 2;  // doubles per smem column (even: 16-B aligned)
+    constexpr int STAGE_DBL = kNWC * NCB * CS;
+    extern __shared__ __align__(128) double smem[];
+    double* ring = smem;
+    double* red = smem + STAGES * STAGE_DBL;  // [2][kNWC][RMAX]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kNWC * RMAX);
+    uint64_t* empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kNWC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int seg_begin = p.cta_seg[blockIdx.x];
+    const int seg_end = p.cta_seg[blockIdx.x + 1];
+    const int64_t I0 = p.I0, I1 = p.I1;
+
+    if (warp == kNWC) {
+        // ---------------- producer: column runs HBM -> smem ring ----------
+        const uint64_t pol = policy_evict_first();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int s = seg_begin; s < seg_end; ++s) {
+            const Seg sg = p.segs[s];
+            const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
+            const int64_t R0s = static_cast<int64_t>(g0) * p.r0;
+            const int64_t R1s = static_cast<int64_t>(g1) * p.t1;
+            const int r0e = static_cast<int>(min64(p.r0, I0 - R0s));
+            const int t1e = static_cast<int>(min64(p.t1, I1 - R1s));
+            for (int o = sg.o0; o < sg.o1; ++o) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                double* dst = ring + stage * STAGE_DBL;
+                uint32_t bytes = 0;
+                for (int j = lane; j < t1e; j += 32) {
+                    const int64_t st = R0s + I0 * (R1s + j + I1 * static_cast<int64_t>(o));
+                    const int64_t as = st & ~int64_t(1), ae = (st + r0e + 1) & ~int64_t(1);
+                    bytes += static_cast<uint32_t>((ae - as) * 8);
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1)
+                    bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
+                if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+                __syncwarp();
+                for (int j = lane; j < t1e; j += 32) {
+                    const int64_t st = R0s + I0 * (R1s + j + I1 * static_cast<int64_t>(o));
+                    const int64_t as = st & ~int64_t(1), ae = (st + r0e + 1) & ~int64_t(1);
+                    bulk_g2s(dst + j * CS, p.A + as, static_cast<uint32_t>((ae - as) * 8),
+                             &full[stage], pol);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // -------------------- consumers: 8 warps, lanes along i0 -------------
+    int stage = 0;
+    uint32_t phase = 0;
+    int rbuf = 0;
+    for (int s = seg_begin; s < seg_end; ++s) {
+        const Seg sg = p.segs[s];
+        const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
+        const int64_t R0s = static_cast<int64_t>(g0) * p.r0;
+        const int64_t R1s = static_cast<int64_t>(g1) * p.t1;
+        const int r0e = static_cast<int>(min64(p.r0, I0 - R0s));
+        const int t1e = static_cast<int>(min64(p.t1, I1 - R1s));
+
+        double u0r[NRA], u1c[NCB];
+        double acc[NRA][NCB];
+#pragma unroll
+        for (int a = 0; a < NRA; ++a) {
+            const int i = lane + 32 * a;
+            u0r[a] = i < r0e ? __ldg(p.u0 + R0s + i) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < NCB; ++b) {
+            const int j = warp + kNWC * b;
+            u1c[b] = j < t1e ? __ldg(p.u1 + R1s + j) : 0.0;
+#pragma unroll
+            for (int a = 0; a < NRA; ++a) acc[a][b] = 0.0;
+        }
+        double* P0row = p.P0 + static_cast<int64_t>(g1) * p.P0_stride + R0s;
+        double* P1row = p.P1 ? p.P1 + static_cast<int64_t>(g0) * p.P1_stride + R1s : nullptr;
+
+        for (int o = sg.o0; o < sg.o1; ++o) {
+            const double wo = __ldg(p.W + o);
+            mbar_wait(&full[stage], phase);
+            const double* st = ring + stage * STAGE_DBL;
+            const int64_t colbase = R0s + I0 * (R1s + I1 * static_cast<int64_t>(o));
+            double c0p[NRA];
+            double c1v[NCB];
+#pragma unroll
+            for (int a = 0; a < NRA; ++a) c0p[a] = 0.0;
+#pragma unroll
+            for (int b = 0; b < NCB; ++b) {
+                const int j = warp + kNWC * b;
+                double c1p = 0.0;
+                if (j < t1e) {
+                    const double* col = st + j * CS + ((colbase + I0 * j) & 1);
+#pragma unroll
+                    for (int a = 0; a < NRA; ++a) {
+                        const int i = lane + 32 * a;
+                        if (i < r0e) {
+                            const double v = col[i];
+                            acc[a][b] = fma(v, wo, acc[a][b]);
+                            c1p = fma(v, u0r[a], c1p);
+                            c0p[a] = fma(v, u1c[b], c0p[a]);
+                        }
+                    }
+                }
+                c1v[b] = c1p;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+
+            // C1 partial: full column dots over this tile's rows.
+            int col;
+            const double c1 = warp_transpose_sum<NCB>(c1v, lane, &col);
+            if (P1row && (lane & (32 / NCB - 1)) == 0) {
+                const int j = warp + kNWC * col;
+                if (j < t1e) P1row[static_cast<int64_t>(o) * I1 + j] = c1;
+            }
+
+            // C0 partial: row sums over this tile's columns, across warps.
+            double* rb = red + rbuf * kNWC * RMAX;
+#pragma unroll
+            for (int a = 0; a < NRA; ++a) rb[warp * RMAX + lane + 32 * a] = c0p[a];
+            consumer_bar();
+            for (int i = threadIdx.x; i < r0e; i += kNWC * 32) {
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < kNWC; ++w) sum += rb[w * RMAX + i];
+                P0row[static_cast<int64_t>(o) * I0 + i] = sum;
+            }
+            rbuf ^= 1;
+        }
+
+        // Flush the B01 face partial of this segment.
+        double* dst = p.P01 + static_cast<int64_t>(s) * p.r0 * p.t1;
+#pragma unroll
+        for (int b = 0; b < NCB; ++b) {
+            const int j = warp + kNWC * b;
+            if (j >= t1e) continue;
+#pragma unroll
+            for (int a = 0; a < NRA; ++a) {
+                const int i = lane + 32 * a;
+                if (i < r0e) dst[j * p.r0 + i] = acc[a][b];
+            }
+        }
+    }
+}
+
+// out[i] = sum_{c<K} in[c*stride + i], fixed order.
+__global__ void reduce_copies_kernel(const double* __restrict__ in, int64_t stride, int K,
+                                     int64_t n, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = in[i];
+        for (int c = 1; c < K; ++c) s += in[c * stride + i];
+        out[i] = s;
+    }
+}
+
+// B01[i0 + I0*i1] = sum over the tile's segments (in o order) of P01 partials.
+__global__ void reduce_b01_kernel(const double* __restrict__ P01, const int* __restrict__ tile_seg,
+                                  int64_t I0, int64_t I1, int r0, int t1, int G0,
+                                  double* __restrict__ out) {
+    const int64_t n = I0 * I1;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i0 = e % I0, i1 = e / I0;
+        const int g0 = static_cast<int>(i0 / r0), g1 = static_cast<int>(i1 / t1);
+        const int tile = g0 + G0 * g1;
+        const int64_t local = (i1 - static_cast<int64_t>(g1) * t1) * r0 + (i0 - int64_t(g0) * r0);
+        const int sb = tile_seg[tile], se = tile_seg[tile + 1];
+        double s = 0.0;
+        for (int k = sb; k < se; ++k) s += P01[static_cast<int64_t>(k) * r0 * t1 + local];
+        out[e] = s;
+    }
+}
+
+struct OuterArgs {
+    int nout;
+    int64_t dims[kMaxOrder];
+    const double* u[kMaxOrder];
+    int64_t O;
+    double* W;
+};
+
+// W[o] = u_2[i_2] * u_3[i_3] * ... (first outer mode fastest).
+__global__ void outer_weights_kernel(const OuterArgs a) {
+    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.O;
+         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t q = o;
+        double w = 1.0;
+        for (int k = 0; k < a.nout; ++k) {
+            w *= a.u[k][q % a.dims[k]];
+            q /= a.dims[k];
+        }
+        a.W[o] = w;
+    }
+}
+
+// ------------------------------------------------------------ the planner --
+enum class Where { Tensor, Final, Work, None };
+
+struct Ref {
+    Where where = Where::None;
+    uint64_t off = 0;  // element offset into the final blocks or the work arena
+};
+
+struct Level {
+    // sub-problem
+    int order = 0;
+    int64_t dims[kMaxOrder] = {};
+    int modes[kMaxOrder] = {};  // original mode ids (ascending)
+    Ref input;
+    // view & tiling
+    int64_t I0 = 0, I1 = 0, O = 0;
+    int nra = 4, ncb = 8, stages = 3;
+    int r0 = 0, t1 = 0, G0 = 0, G1 = 0, ncta = 0, nseg = 0, ntiles = 0;
+    size_t smem = 0;
+    // plan metadata (device offsets into SweepPlan::meta, in ints)
+    uint64_t seg_off = 0, cta_off = 0, tile_off = 0;
+    // outputs
+    Ref out_b01, out_c0, out_c1;
+    Ref w, p01, p0, p1;
+};
+
+}  // namespace
+
+struct SweepPlan {
+    std::vector<uint64_t> dims;
+    std::vector<Level> levels;
+    std::vector<int> host_meta;
+    DeviceBuffer meta;
+    uint64_t work_elems = 0;
+    uint64_t nblocks = 0;
+};
+
+namespace {
+
+size_t smem_bytes(int nra, int ncb, int stages) {
+    const int rmax = 32 * nra;
+    return static_cast<size_t>(stages) * kNWC * ncb * (rmax + 2) * 8 +
+           static_cast<size_t>(2) * kNWC * rmax * 8 + 2 * stages * 8;
+}
+
+void tile_level(Level& L, int num_sms) {
+    L.nra = L.I0 > 64 ? 4 : (L.I0 > 32 ? 2 : 1);
+    L.ncb = 8;
+    L.stages = L.nra == 4 ? 3 : (L.nra == 2 ? 5 : 8);
+    L.smem = smem_bytes(L.nra, L.ncb, L.stages);
+    const int rmax = 32 * L.nra, cmax = kNWC * L.ncb;
+    // Balance row tiles: G0 = ceil(I0/rmax), r0 = ceil(I0/G0) (same for cols).
+    L.G0 = static_cast<int>((L.I0 + rmax - 1) / rmax);
+    L.r0 = static_cast<int>((L.I0 + L.G0 - 1) / L.G0);
+    L.G1 = static_cast<int>((L.I1 + cmax - 1) / cmax);
+    L.t1 = static_cast<int>((L.I1 + L.G1 - 1) / L.G1);
+    L.ntiles = L.G0 * L.G1;
+    (void)num_sms;
+}
+
+// Partition (tile, o) panels into ncta contiguous chunks of equal cost and
+// cut them into segments (maximal runs inside one tile).
+void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
+    const int64_t npanels = static_cast<int64_t>(L.ntiles) * L.O;
+    auto panel_cost = [&](int tile) {
+        const int g0 = tile % L.G0, g1 = tile / L.G0;
+        const int64_t r = std::min<int64_t>(L.r0, L.I0 - int64_t(g0) * L.r0);
+        const int64_t c = std::min<int64_t>(L.t1, L.I1 - int64_t(g1) * L.t1);
+        return static_cast<double>(r * c + 512);
+    };
+    double total = 0.0;
+    for (int t = 0; t < L.ntiles; ++t) total += panel_cost(t) * static_cast<double>(L.O);
+    // Enough CTAs to fill the chip, but at least ~16 panels each.
+    int64_t ncta = std::min<int64_t>(num_sms, std::max<int64_t>(1, npanels / 16));
+    L.ncta = static_cast<int>(ncta);
+    std::vector<Seg> segs;
+    std::vector<int> cta_seg(L.ncta + 1, 0);
+    const double per = total / static_cast<double>(L.ncta);
+    int cur = 0;          // CTA receiving the current panel
+    int seg_cta = -1;     // CTA owning segs.back()
+    double x = 0.0;       // cost of all earlier panels
+    for (int t = 0; t < L.ntiles; ++t) {
+        const double c = panel_cost(t);
+        for (int64_t o = 0; o < L.O; ++o) {
+            const int target = std::min<int>(
+                L.ncta - 1, static_cast<int>((x + 0.5 * c) / per));
+            while (cur < target) cta_seg[++cur] = static_cast<int>(segs.size());
+            if (segs.empty() || segs.back().tile != t || seg_cta != cur ||
+                segs.back().o1 != o)
+                segs.push_back(Seg{t, static_cast<int>(o), static_cast<int>(o + 1), 0});
+            else
+                segs.back().o1 = static_cast<int>(o + 1);
+            seg_cta = cur;
+            x += c;
+        }
+    }
+    while (cur < L.ncta) cta_seg[++cur] = static_cast<int>(segs.size());
+    L.nseg = static_cast<int>(segs.size());
+    std::vector<int> tile_seg(L.ntiles + 1, 0);
+    {
+        int k = 0;
+        for (int t = 0; t < L.ntiles; ++t) {
+            tile_seg[t] = k;
+            while (k < L.nseg && segs[k].tile == t) ++k;
+        }
+        tile_seg[L.ntiles] = L.nseg;
+    }
+    auto align4 = [&]() {
+        while (meta.size() % 4) meta.push_back(0);
+    };
+    align4();
+    L.seg_off = meta.size();
+    for (const Seg& s : segs) {
+        meta.push_back(s.tile);
+        meta.push_back(s.o0);
+        meta.push_back(s.o1);
+        meta.push_back(0);
+    }
+    L.cta_off = meta.size();
+    meta.insert(meta.end(), cta_seg.begin(), cta_seg.end());
+    L.tile_off = meta.size();
+    meta.insert(meta.end(), tile_seg.begin(), tile_seg.end());
+}
+
+// Recursively lay out the levels for a sub-problem of order `order` (>= 3).
+// need_all: also produce the blocks among modes >= 2 of this sub-problem.
+void plan_rec(SweepPlan& P, const uint64_t* full_dims, int full_order, int order,
+              const int64_t* dims, const int* modes, Ref input, bool need_all, int num_sms) {
+    Level L;
+    L.order = order;
+    for (int k = 0; k < order; ++k) {
+        L.dims[k] = dims[k];
+        L.modes[k] = modes[k];
+    }
+    L.input = input;
+    L.I0 = dims[0];
+    L.I1 = dims[1];
+    L.O = 1;
+    for (int k = 2; k < order; ++k) L.O *= dims[k];
+    tile_level(L, num_sms);
+    partition_level(L, num_sms, P.host_meta);
+
+    auto final_ref = [&](int a, int b) {
+        return Ref{Where::Final, block_offset(full_dims, full_order, modes[a], modes[b])};
+    };
+    auto work = [&](uint64_t n) {
+        Ref r{Where::Work, P.work_elems};
+        P.work_elems += (n + 31) & ~uint64_t(31);
+        return r;
+    };
+    L.out_b01 = final_ref(0, 1);
+    const bool need_c1 = need_all;
+    if (order == 3) {
+        L.out_c0 = final_ref(0, 2);
+        L.out_c1 = need_c1 ? final_ref(1, 2) : Ref{};
+    } else {
+        L.out_c0 = work(static_cast<uint64_t>(L.I0 * L.O));
+        L.out_c1 = need_c1 ? work(static_cast<uint64_t>(L.I1 * L.O)) : Ref{};
+    }
+    L.w = work(static_cast<uint64_t>(L.O));
+    L.p01 = work(static_cast<uint64_t>(L.nseg) * L.r0 * L.t1);
+    L.p0 = L.G1 > 1 ? work(static_cast<uint64_t>(L.G1) * L.I0 * L.O) : L.out_c0;
+    if (need_c1) L.p1 = L.G0 > 1 ? work(static_cast<uint64_t>(L.G0) * L.I1 * L.O) : L.out_c1;
+    P.levels.push_back(L);
+
+    if (order >= 4) {
+        // C0: modes (0, 2, 3, ...) — all of its blocks are blocks of A (if need_all),
+        // else only its (0,k) blocks.
+        int64_t d0[kMaxOrder];
+        int m0[kMaxOrder];
+        d0[0] = dims[0];
+        m0[0] = modes[0];
+        for (int k = 2; k < order; ++k) {
+            d0[k - 1] = dims[k];
+            m0[k - 1] = modes[k];
+        }
+        const Ref c0 = L.out_c0, c1 = L.out_c1;
+        plan_rec(P, full_dims, full_order, order - 1, d0, m0, c0, need_all, num_sms);
+        if (need_c1) {
+            d0[0] = dims[1];
+            m0[0] = modes[1];
+            plan_rec(P, full_dims, full_order, order - 1, d0, m0, c1, false, num_sms);
+        }
+    }
+}
+
+std::shared_ptr<SweepPlan> get_plan(r1_context* ctx, const uint64_t* dims, int order) {
+    std::vector<uint64_t> key(dims, dims + order);
+    auto it = ctx->plans.find(key);
+    if (it != ctx->plans.end()) return it->second;
+    auto P = std::make_shared<SweepPlan>();
+    P->dims = key;
+    P->nblocks = blocks_numel(dims, order);
+    int64_t d[kMaxOrder];
+    int m[kMaxOrder];
+    for (int k = 0; k < order; ++k) {
+        d[k] = static_cast<int64_t>(dims[k]);
+        m[k] = k;
+    }
+    plan_rec(*P, dims, order, order, d, m, Ref{Where::Tensor, 0}, true, ctx->num_sms);
+    P->meta.ensure(std::max<size_t>(16, P->host_meta.size() * sizeof(int)));
+    R1_CUDA(cudaMemcpy(P->meta.ptr, P->host_meta.data(), P->host_meta.size() * sizeof(int),
+                       cudaMemcpyHostToDevice));
+    ctx->plans[key] = P;
+    return P;
+}
+
+template <int NRA, int NCB, int STAGES>
+void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
+    static bool configured = false;  // per instantiation; attribute is per-function
+    auto kern = sweep3_kernel<NRA, NCB, STAGES>;
+    if (!configured) {
+        R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(L.smem)));
+        configured = true;
+    }
+    kern<<<L.ncta, kThreads, L.smem, ctx->stream>>>(a);
+    check_launch(ctx, "sweep3_kernel");
+}
+
+int grid_for(int64_t n, int threads, int num_sms) {
+    const int64_t g = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, int64_t(num_sms) * 8)));
+}
+
+}  // namespace
+
+void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int order,
+                  const double* factors_dev, double* blocks_dev) {
+    if (order < 2 || order > kMaxOrder) fail(R1_ERR_INVALID_ARGUMENT, "sweep: unsupported order");
+    const uint64_t n = numel_of(dims, order);
+    if (order == 2) {
+        // Nothing to contract: the block is the tensor itself (nepv.cpp:49-53).
+        R1_CUDA(cudaMemcpyAsync(blocks_dev, a, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        return;
+    }
+    auto P = get_plan(ctx, dims, order);
+    ctx->ws_sweep.ensure(std::max<uint64_t>(P->work_elems, 32) * sizeof(double));
+    double* work = ctx->ws_sweep.as<double>();
+    const int* meta = P->meta.as<int>();
+    uint64_t foff[kMaxOrder + 1];
+    foff[0] = 0;
+    for (int k = 0; k < order; ++k) foff[k + 1] = foff[k] + dims[k];
+
+    auto resolve = [&](const Ref& r) -> double* {
+        switch (r.where) {
+            case Where::Tensor: return const_cast<double*>(a);
+            case Where::Final: return blocks_dev + r.off;
+            case Where::Work: return work + r.off;
+            default: return nullptr;
+        }
+    };
+
+    for (const Level& L : P->levels) {
+        // outer weights
+        OuterArgs oa{};
+        oa.nout = L.order - 2;
+        for (int k = 2; k < L.order; ++k) {
+            oa.dims[k - 2] = L.dims[k];
+            oa.u[k - 2] = factors_dev + foff[L.modes[k]];
+        }
+        oa.O = L.O;
+        oa.W = resolve(L.w);
+        outer_weights_kernel<<<grid_for(L.O, 256, ctx->num_sms), 256, 0, ctx->stream>>>(oa);
+        check_launch(ctx, "outer_weights_kernel");
+
+        SweepArgs s{};
+        s.A = resolve(L.input);
+        s.I0 = L.I0;
+        s.I1 = L.I1;
+        s.O = L.O;
+        s.u0 = factors_dev + foff[L.modes[0]];
+        s.u1 = factors_dev + foff[L.modes[1]];
+        s.W = oa.W;
+        s.r0 = L.r0;
+        s.t1 = L.t1;
+        s.G0 = L.G0;
+        s.segs = reinterpret_cast<const Seg*>(meta + L.seg_off);
+        s.cta_seg = meta + L.cta_off;
+        s.P01 = resolve(L.p01);
+        s.P0 = resolve(L.p0);
+        s.P0_stride = L.I0 * L.O;
+        s.P1 = L.out_c1.where == Where::None ? nullptr : resolve(L.p1);
+        s.P1_stride = L.I1 * L.O;
+        if (L.nra == 4)
+            launch_sweep<4, 8, 3>(ctx, L, s);
+        else if (L.nra == 2)
+            launch_sweep<2, 8, 5>(ctx, L, s);
+        else
+            launch_sweep<1, 8, 8>(ctx, L, s);
+
+        // second stage: fixed-order partial sums
+        reduce_b01_kernel<<<grid_for(L.I0 * L.I1, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+            s.P01, meta + L.tile_off, L.I0, L.I1, L.r0, L.t1, L.G0, resolve(L.out_b01));
+        check_launch(ctx, "reduce_b01_kernel");
+        if (L.G1 > 1) {
+            const int64_t n0 = L.I0 * L.O;
+            reduce_copies_kernel<<<grid_for(n0, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+                s.P0, s.P0_stride, L.G1, n0, resolve(L.out_c0));
+            check_launch(ctx, "reduce_copies_kernel(C0)");
+        }
+        if (s.P1 && L.G0 > 1) {
+            const int64_t n1 = L.I1 * L.O;
+            reduce_copies_kernel<<<grid_for(n1, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+                s.P1, s.P1_stride, L.G0, n1, resolve(L.out_c1));
+            check_launch(ctx, "reduce_copies_kernel(C1)");
+        }
+    }
+}
+
+// Introspection for tests / DESIGN.md: the plan of the top level.
+void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* info) {
+    auto P = get_plan(ctx, dims, order);
+    const Level& L = P->levels.front();
+    info[0] = L.r0;
+    info[1] = L.t1;
+    info[2] = L.G0;
+    info[3] = L.G1;
+    info[4] = L.ncta;
+    info[5] = L.nseg;
+    info[6] = static_cast<int64_t>(P->levels.size());
+    info[7] = static_cast<int64_t>(P->work_elems);
+    info[8] = static_cast<int64_t>(L.smem);
+    info[9] = L.nra;
+}
+
+}  // namespace r1

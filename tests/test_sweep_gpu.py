@@ -1,0 +1,81 @@
+"""Parity of the fused device sweep (rank1::build_j replacement) with the
+oracle restatement, which is itself pinned bit-exact to the compiled reference
+(tests/test_oracle_pins.py).  Tolerance: blocks agree entrywise within
+1e-12 * (sum_i |A_i| prod |u_k| bound), i.e. a relative accuracy far tighter
+than the north-star's 1e-10 sigma tolerance."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (3, 4), (5, 7), (2, 2, 2), (7, 5, 9), (30, 20, 10), (100, 100, 100), (129, 65, 33),
+    (1, 1, 1), (1, 7, 3), (300, 2, 5), (3, 300, 5), (257, 130, 17), (6, 5, 4, 3),
+    (4, 3, 5, 2, 3), (2, 3, 4, 5, 6, 2), (20, 20, 20, 20), (10, 10, 10, 10, 10), (65, 64, 3, 3),
+]
+
+
+def _bound(o, a, dims, f):
+    """Entrywise error scale: the same contraction on |A| and |u|."""
+    return o.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
+
+
+@pytest.mark.parametrize("dims", SHAPES)
+def test_build_j_matches_oracle(gpu_ctx, oracle, dims):
+    import paper_2403_01778_b200 as r1
+    a = oracle.oracle_random_tensor(dims, 11 + len(dims))
+    f = oracle.oracle_random_unit_factors(dims, 12 + len(dims))
+    want = oracle.build_j(a, dims, f)
+    got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
+    scale = _bound(oracle, a, dims, f)
+    err = np.abs(got - want)
+    assert np.all(err <= 1e-13 * scale + 1e-300), (dims, float(np.max(err / (scale + 1e-300))))
+
+
+def test_build_j_all_ones_kat(gpu_ctx):
+    """test_nepv.cpp:126-137: every block entry of the all-ones 2x2x2 tensor with
+    factors (1/sqrt2, 1/sqrt2) is sqrt(2); scale 0.5."""
+    import paper_2403_01778_b200 as r1
+    s = 1.0 / np.sqrt(2.0)
+    j = r1.build_j(r1.DenseTensor([2, 2, 2], np.ones(8)), r1.FactorSet(0.0, [[s, s]] * 3))
+    assert j.scale() == 0.5
+    np.testing.assert_allclose(j.blocks, np.sqrt(2.0), rtol=1e-12)
+
+
+def test_build_j_rank_one_kat(gpu_ctx, oracle):
+    """test_nepv.cpp:81-89: rank-one tensor with its own factors -> B(0,1) = u0 u1'."""
+    import paper_2403_01778_b200 as r1
+    dims = (3, 4, 5)
+    f = oracle.oracle_random_unit_factors(dims, 6)
+    a = np.einsum("i,j,k->ijk", *f).reshape(-1, order="F")
+    b = r1.build_block(r1.DenseTensor(dims, a), r1.FactorSet(1.0, f), 0, 1)
+    np.testing.assert_allclose(b, np.outer(f[0], f[1]), rtol=1e-12, atol=1e-15)
+
+
+def test_build_j_deterministic(gpu_ctx, oracle):
+    """Fixed-order reductions: identical inputs give identical bits."""
+    import paper_2403_01778_b200 as r1
+    dims = (129, 130, 40)
+    a = oracle.oracle_random_tensor(dims, 5)
+    f = oracle.oracle_random_unit_factors(dims, 6)
+    t = r1.DenseTensor(dims, a)
+    b1 = r1.build_j(t, r1.FactorSet(0.0, f)).blocks
+    b2 = r1.build_j(t, r1.FactorSet(0.0, f)).blocks
+    assert np.array_equal(b1, b2)
+
+
+def test_build_j_errors(gpu_ctx, oracle):
+    """nepv.cpp:24-41 / test_nepv.cpp:104-107, 227-232."""
+    import paper_2403_01778_b200 as r1
+    dims = (3, 3, 3)
+    a = r1.DenseTensor(dims, oracle.oracle_random_tensor(dims, 20))
+    f = oracle.oracle_random_unit_factors(dims, 21)
+    zero = [f[0], f[1], np.zeros(3)]
+    with pytest.raises(RuntimeError, match="zero factor for mode 2"):
+        r1.build_j(a, r1.FactorSet(0.0, zero))
+    with pytest.raises(ValueError, match="not unit length"):
+        r1.build_j(a, r1.FactorSet(0.0, [f[0] * 1.5, f[1], f[2]]))
+    with pytest.raises(ValueError):
+        r1.build_block(a, r1.FactorSet(0.0, f), 1, 1)
+    with pytest.raises(ValueError, match="order mismatch"):
+        r1.build_j(a, r1.FactorSet(0.0, f[:2]))
