@@ -329,6 +329,15 @@ int r1_block_matvec_device(r1_context* ctx, const uint64_t* dims, int order,
     });
 }
 
+// Diagnostics (not in the public header): per-CTA {start,end,smid} of the
+// top-level sweep kernel into a device buffer of 3*ncta uint64 (NULL: off).
+int r1x_set_sweep_trace(r1_context* ctx, void* dev) {
+    return abi_guard([&] {
+        bind(ctx);
+        ctx->dbg_sweep_trace = static_cast<unsigned long long*>(dev);
+    });
+}
+
 // Test/diagnostic hook (not in the public header): the top-level sweep plan.
 int r1x_sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* info) {
     return abi_guard([&] {

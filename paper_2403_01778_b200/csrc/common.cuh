@@ -124,6 +124,7 @@ struct r1_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
+    unsigned long long* dbg_sweep_trace = nullptr;  // diagnostics: per-CTA timing of level 0
     // Workspace arena, grow-only: sweeps, eigen solver, RQI.
     r1::DeviceBuffer ws_sweep;
     r1::DeviceBuffer ws_eig;

@@ -29,7 +29,10 @@
 // atomics anywhere, so results are bit-reproducible run to run.
 #include "common.cuh"
 
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace r1 {
@@ -39,6 +42,10 @@ namespace {
 constexpr int kNWC = 8;                    // consumer warps
 constexpr int kThreads = (kNWC + 1) * 32;  // + one producer warp
 constexpr int kMaxOrder = 16;
+constexpr int kBoxNWC = 15;  // consumer warps of the TMA box kernel (+1 producer = 16 warps)
+constexpr int kBoxNCB = 4;   // columns per consumer warp (box = 32*NRA x 60)
+constexpr int kMaxStages = 16;          // mbarrier slots of the box kernel ring
+constexpr size_t kSmemBudget = 227 * 1024;  // opt-in dynamic shared memory per CTA
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -56,6 +63,7 @@ struct SweepArgs {
     const double* u1;
     const double* W;
     int r0, t1, G0;
+    int rbox;               // TMA path: box rows (= r0, even); smem column stride
     const Seg* segs;
     const int* cta_seg;
     double* P01;            // [nseg][t1][r0]
@@ -63,6 +71,8 @@ struct SweepArgs {
     int64_t P0_stride;
     double* P1;             // [G0] copies of I1 x O, stride P1_stride (nullptr: skip)
     int64_t P1_stride;
+    unsigned long long* trace;  // optional: per CTA {t_start, t_end, smid}
+    int debug_mode;             // diagnostics: 1 = consumers only wait/release
 };
 
 // ------------------------------------------------------------- PTX helpers --
@@ -105,6 +115,7 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return pol;
 }
 
+// 1-D bulk copy (any 16-B aligned run), completion on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar, uint64_t pol) {
     asm volatile(
@@ -112,6 +123,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
+}
+
+// 3-D TMA tile load of box (rbox, t1, 1) at (c0, c1, c2); out-of-range
+// elements are zero-filled by the hardware.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)),
+        "l"(pol)
+        : "memory");
+}
+
+// L2 prefetch of a 3-D box (no smem, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
 
 __device__ __forceinline__ void consumer_bar() {
@@ -145,12 +176,16 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[NV], int lane, 
 }
 
 // --------------------------------------------------------------- the sweep --
-template <int NRA, int NCB, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1) sweep3_kernel(const SweepArgs p) {
+// TMA = true : one cp.async.bulk.tensor.3d per panel (I0 even: 16-B strides).
+// TMA = false: one 1-D bulk copy per column run, 16-B aligned superset, the
+//              consumer skips the (st & 1) leading element (any I0).
+template <int NRA, int NCB, int STAGES, bool TMA>
+__global__ void __launch_bounds__(kThreads, 1)
+    sweep3_kernel(const SweepArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int RMAX = 32 * NRA;
-    constexpr int CS = RMAX + 2;  // doubles per smem column (even: 16-B aligned)
+    constexpr int CS = TMA ? RMAX : RMAX + 2;  // doubles per smem column
     constexpr int STAGE_DBL = kNWC * NCB * CS;
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(1024) double smem[];
     double* ring = smem;
     double* red = smem + STAGES * STAGE_DBL;  // [2][kNWC][RMAX]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kNWC * RMAX);
@@ -170,12 +205,35 @@ __global__ void __launch_bounds__(kThreads, 1) sweep3_kernel(const SweepArgs p) 
     const int seg_begin = p.cta_seg[blockIdx.x];
     const int seg_end = p.cta_seg[blockIdx.x + 1];
     const int64_t I0 = p.I0, I1 = p.I1;
+    const int cstride = TMA ? p.rbox : CS;
 
     if (warp == kNWC) {
-        // ---------------- producer: column runs HBM -> smem ring ----------
+        // ---------------- producer: panels HBM -> smem ring ----------------
         const uint64_t pol = policy_evict_first();
         int stage = 0;
         uint32_t phase = 0;
+        if (TMA) {
+            if (lane == 0) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap))
+                             : "memory");
+                const uint32_t box_bytes = static_cast<uint32_t>(p.rbox) * p.t1 * 8;
+                for (int s = seg_begin; s < seg_end; ++s) {
+                    const Seg sg = p.segs[s];
+                    const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
+                    for (int o = sg.o0; o < sg.o1; ++o) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[stage], box_bytes);
+                        tma_load_3d(ring + stage * STAGE_DBL, &tmap, g0 * p.r0, g1 * p.t1, o,
+                                    &full[stage], pol);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+            return;
+        }
         for (int s = seg_begin; s < seg_end; ++s) {
             const Seg sg = p.segs[s];
             const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
@@ -226,15 +284,18 @@ __global__ void __launch_bounds__(kThreads, 1) sweep3_kernel(const SweepArgs p) 
 
         double u0r[NRA], u1c[NCB];
         double acc[NRA][NCB];
+        bool rv[NRA], cv[NCB];
 #pragma unroll
         for (int a = 0; a < NRA; ++a) {
             const int i = lane + 32 * a;
-            u0r[a] = i < r0e ? __ldg(p.u0 + R0s + i) : 0.0;
+            rv[a] = i < r0e;
+            u0r[a] = rv[a] ? __ldg(p.u0 + R0s + i) : 0.0;
         }
 #pragma unroll
         for (int b = 0; b < NCB; ++b) {
             const int j = warp + kNWC * b;
-            u1c[b] = j < t1e ? __ldg(p.u1 + R1s + j) : 0.0;
+            cv[b] = j < t1e;
+            u1c[b] = cv[b] ? __ldg(p.u1 + R1s + j) : 0.0;
 #pragma unroll
             for (int a = 0; a < NRA; ++a) acc[a][b] = 0.0;
         }
@@ -254,13 +315,13 @@ __global__ void __launch_bounds__(kThreads, 1) sweep3_kernel(const SweepArgs p) 
             for (int b = 0; b < NCB; ++b) {
                 const int j = warp + kNWC * b;
                 double c1p = 0.0;
-                if (j < t1e) {
-                    const double* col = st + j * CS + ((colbase + I0 * j) & 1);
+                if (cv[b]) {
+                    const double* col =
+                        st + j * cstride + (TMA ? 0 : static_cast<int>((colbase + I0 * j) & 1));
 #pragma unroll
                     for (int a = 0; a < NRA; ++a) {
-                        const int i = lane + 32 * a;
-                        if (i < r0e) {
-                            const double v = col[i];
+                        if (rv[a]) {
+                            const double v = col[lane + 32 * a];
                             acc[a][b] = fma(v, wo, acc[a][b]);
                             c1p = fma(v, u0r[a], c1p);
                             c0p[a] = fma(v, u1c[b], c0p[a]);
@@ -303,13 +364,239 @@ __global__ void __launch_bounds__(kThreads, 1) sweep3_kernel(const SweepArgs p) 
 #pragma unroll
         for (int b = 0; b < NCB; ++b) {
             const int j = warp + kNWC * b;
-            if (j >= t1e) continue;
+            if (!cv[b]) continue;
 #pragma unroll
             for (int a = 0; a < NRA; ++a) {
                 const int i = lane + 32 * a;
-                if (i < r0e) dst[j * p.r0 + i] = acc[a][b];
+                if (rv[a]) dst[j * p.r0 + i] = acc[a][b];
             }
         }
+    }
+}
+
+// TMA path with fixed RMAX x CMAX tiles.  Interior tiles load one full box;
+// the ragged last row / column tiles use their own tensor maps whose box is
+// exactly the remainder (boxes straddling the tensor edge take the slow
+// out-of-bounds path in the TMA unit).  The smem column stride is the box's
+// row count; rows beyond it read finite neighbours (the ring is zeroed once)
+// whose contributions carry zero weights and are never stored.  Lane l owns
+// rows 64p + 2l + {0,1} (one 128-bit LDS per pair p), warp w owns columns
+// w + NWC*b: the inner loop is branch-free.
+struct BoxMaps {
+    CUtensorMap m[4];  // [row-edge bit | col-edge bit << 1]: boxes r0|rem0 x t1|rem1
+};
+
+// TMA path.  Tiles are balanced (r0 = ceil(I0/G0) rounded to even, t1 =
+// ceil(I1/G1)), so every box is within a few rows/columns of the others; the
+// ragged last row/column tiles use their own tensor maps (a box straddling the
+// tensor edge takes the slow out-of-bounds path in the TMA unit).  The smem
+// ring is budgeted in BYTES: nst = ring_bytes / box_bytes stages, so every SM
+// keeps the same volume in flight — in a saturated memory system an SM's share
+// of bandwidth follows its bytes in flight.  The consumer thread grid is fixed
+// (RMAX x CMAX); rows/columns beyond the tile read finite neighbours (the ring
+// is zeroed once) and carry zero weights, and are never stored.  Lane l owns
+// rows 64p + 2l + {0,1} (one 128-bit LDS per pair), warp w owns columns
+// w + NWC*b.  Each thread copies its slice to registers and releases the
+// stage before computing.
+template <int NRA, int NCB, int NWC, bool STAGE_REGS>
+__global__ void __launch_bounds__((NWC + 1) * 32, 1)
+    sweep3_box_kernel(const SweepArgs p, const __grid_constant__ BoxMaps maps, int nst,
+                      int stage_dbl) {
+    static_assert(NRA % 2 == 0, "rows are read in pairs");
+    constexpr int RMAX = 32 * NRA;
+    constexpr int CMAX = NWC * NCB;
+    constexpr int NP = NRA / 2;
+    extern __shared__ __align__(1024) double smem[];
+    double* ring = smem;
+    const int ring_dbl = nst * stage_dbl + RMAX;  // + slack for over-reads
+    double* red = smem + ring_dbl;                // [2][NWC][RMAX]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * NWC * RMAX);
+    uint64_t* empty = full + kMaxStages;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < ring_dbl / 2; i += blockDim.x)
+        reinterpret_cast<double2*>(ring)[i] = make_double2(0.0, 0.0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+
+    const int seg_begin = p.cta_seg[blockIdx.x];
+    const int seg_end = p.cta_seg[blockIdx.x + 1];
+    const int64_t I0 = p.I0, I1 = p.I1;
+    const int G1 = static_cast<int>((I1 + p.t1 - 1) / p.t1);
+    const int rem0 = static_cast<int>(I0 - static_cast<int64_t>(p.G0 - 1) * p.r0);
+    const int rem1 = static_cast<int>(I1 - static_cast<int64_t>(G1 - 1) * p.t1);
+
+    if (warp == NWC) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int m = 0; m < 4; ++m)
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[m]))
+                             : "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int s = seg_begin; s < seg_end; ++s) {
+                const Seg sg = p.segs[s];
+                const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
+                const bool er = g0 == p.G0 - 1, ec = g1 == G1 - 1;
+                const uint32_t bytes = static_cast<uint32_t>(er ? rem0 : p.r0) *
+                                       static_cast<uint32_t>(ec ? rem1 : p.t1) * 8u;
+                const CUtensorMap* map = &maps.m[(er ? 1 : 0) | (ec ? 2 : 0)];
+                for (int o = sg.o0; o < sg.o1; ++o) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], bytes);
+                    tma_load_3d(ring + stage * stage_dbl, map, g0 * p.r0, g1 * p.t1, o,
+                                &full[stage], pol);
+                    if (++stage == nst) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    unsigned long long t_start = 0;
+    if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    int stage = 0;
+    uint32_t phase = 0;
+    int rbuf = 0;
+    for (int s = seg_begin; s < seg_end; ++s) {
+        const Seg sg = p.segs[s];
+        const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
+        const int64_t R0s = static_cast<int64_t>(g0) * p.r0;
+        const int64_t R1s = static_cast<int64_t>(g1) * p.t1;
+        const int r0e = static_cast<int>(min64(p.r0, I0 - R0s));
+        const int t1e = static_cast<int>(min64(p.t1, I1 - R1s));
+
+        double u0r[NRA], u1c[NCB];
+        double acc[NRA][NCB];
+        int coff[NCB];  // smem offset (double2 units) of the thread's columns
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 64 * q + 2 * lane + h;
+                u0r[2 * q + h] = i < r0e ? __ldg(p.u0 + R0s + i) : 0.0;
+            }
+#pragma unroll
+        for (int b = 0; b < NCB; ++b) {
+            const int j = warp + NWC * b;
+            u1c[b] = j < t1e ? __ldg(p.u1 + R1s + j) : 0.0;
+            coff[b] = (min(j, t1e - 1) * r0e) / 2 + lane;
+#pragma unroll
+            for (int a = 0; a < NRA; ++a) acc[a][b] = 0.0;
+        }
+        double* P0row = p.P0 + static_cast<int64_t>(g1) * p.P0_stride + R0s;
+        double* P1row = p.P1 ? p.P1 + static_cast<int64_t>(g0) * p.P1_stride + R1s : nullptr;
+
+        for (int o = sg.o0; o < sg.o1; ++o) {
+            const double wo = __ldg(p.W + o);
+            mbar_wait(&full[stage], phase);
+            const double2* st = reinterpret_cast<const double2*>(ring + stage * stage_dbl);
+            if (p.debug_mode == 1) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                if (++stage == nst) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                continue;
+            }
+            double c0p[NRA];
+            double c1v[NCB];
+#pragma unroll
+            for (int a = 0; a < NRA; ++a) c0p[a] = 0.0;
+            auto column = [&](int b, const double2* v) {
+                double c1p = 0.0;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    acc[2 * q][b] = fma(v[q].x, wo, acc[2 * q][b]);
+                    acc[2 * q + 1][b] = fma(v[q].y, wo, acc[2 * q + 1][b]);
+                    c1p = fma(v[q].x, u0r[2 * q], c1p);
+                    c1p = fma(v[q].y, u0r[2 * q + 1], c1p);
+                    c0p[2 * q] = fma(v[q].x, u1c[b], c0p[2 * q]);
+                    c0p[2 * q + 1] = fma(v[q].y, u1c[b], c0p[2 * q + 1]);
+                }
+                c1v[b] = c1p;
+            };
+            if constexpr (STAGE_REGS) {
+                // copy the slice to registers and release the stage before computing
+                double2 v[NCB][NP];
+#pragma unroll
+                for (int b = 0; b < NCB; ++b)
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) v[b][q] = st[coff[b] + 32 * q];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+#pragma unroll
+                for (int b = 0; b < NCB; ++b) column(b, v[b]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < NCB; ++b) {
+                    double2 v[NP];
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) v[q] = st[coff[b] + 32 * q];
+                    column(b, v);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+            }
+            if (++stage == nst) {
+                stage = 0;
+                phase ^= 1;
+            }
+
+            int col;
+            const double c1 = warp_transpose_sum<NCB>(c1v, lane, &col);
+            if (P1row && (lane & (32 / NCB - 1)) == 0) {
+                const int j = warp + NWC * col;
+                if (j < t1e) P1row[static_cast<int64_t>(o) * I1 + j] = c1;
+            }
+
+            double2* rb = reinterpret_cast<double2*>(red + rbuf * NWC * RMAX + warp * RMAX) + lane;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) rb[32 * q] = make_double2(c0p[2 * q], c0p[2 * q + 1]);
+            asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory");
+            const double* rr = red + rbuf * NWC * RMAX;
+            for (int i = threadIdx.x; i < r0e; i += NWC * 32) {
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX + i];
+                P0row[static_cast<int64_t>(o) * I0 + i] = sum;
+            }
+            rbuf ^= 1;
+        }
+
+        double* dst = p.P01 + static_cast<int64_t>(s) * p.r0 * p.t1;
+#pragma unroll
+        for (int b = 0; b < NCB; ++b) {
+            const int j = warp + NWC * b;
+            if (j >= t1e) continue;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const int i = 64 * q + 2 * lane;
+                if (i < r0e) dst[j * p.r0 + i] = acc[2 * q][b];
+                if (i + 1 < r0e) dst[j * p.r0 + i + 1] = acc[2 * q + 1][b];
+            }
+        }
+    }
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long t_end;
+        unsigned int smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[3 * blockIdx.x] = t_start;
+        p.trace[3 * blockIdx.x + 1] = t_end;
+        p.trace[3 * blockIdx.x + 2] = smid;
     }
 }
 
@@ -381,6 +668,8 @@ struct Level {
     // view & tiling
     int64_t I0 = 0, I1 = 0, O = 0;
     int nra = 4, ncb = 8, stages = 3;
+    int stage_dbl = 0;
+    bool tma = false;
     int r0 = 0, t1 = 0, G0 = 0, G1 = 0, ncta = 0, nseg = 0, ntiles = 0;
     size_t smem = 0;
     // plan metadata (device offsets into SweepPlan::meta, in ints)
@@ -403,9 +692,9 @@ struct SweepPlan {
 
 namespace {
 
-size_t smem_bytes(int nra, int ncb, int stages) {
+size_t smem_bytes(int nra, int ncb, int stages, bool tma) {
     const int rmax = 32 * nra;
-    return static_cast<size_t>(stages) * kNWC * ncb * (rmax + 2) * 8 +
+    return static_cast<size_t>(stages) * kNWC * ncb * (rmax + (tma ? 0 : 2)) * 8 +
            static_cast<size_t>(2) * kNWC * rmax * 8 + 2 * stages * 8;
 }
 
@@ -413,11 +702,44 @@ void tile_level(Level& L, int num_sms) {
     L.nra = L.I0 > 64 ? 4 : (L.I0 > 32 ? 2 : 1);
     L.ncb = 8;
     L.stages = L.nra == 4 ? 3 : (L.nra == 2 ? 5 : 8);
-    L.smem = smem_bytes(L.nra, L.ncb, L.stages);
+    // TMA needs 16-B global strides (I0 even) and an int32 outer coordinate.
+    L.tma = (L.I0 % 2 == 0) && L.O < (int64_t(1) << 31) && L.I1 < (int64_t(1) << 31);
+    L.smem = smem_bytes(L.nra, L.ncb, L.stages, L.tma);
     const int rmax = 32 * L.nra, cmax = kNWC * L.ncb;
-    // Balance row tiles: G0 = ceil(I0/rmax), r0 = ceil(I0/G0) (same for cols).
+    // Balance row tiles: G0 = ceil(I0/rmax), r0 = ceil(I0/G0) (same for cols);
+    // on the TMA path r0 is even so interior boxes hold exactly the tile.
+    if (L.tma) {
+        // Balanced tiles on the fixed RMAX x CMAX consumer grid.
+        if (L.nra == 1) L.nra = 2;
+        const int rm = 32 * L.nra, cm = kBoxNWC * kBoxNCB;
+        L.G0 = static_cast<int>((L.I0 + rm - 1) / rm);
+        L.r0 = static_cast<int>((L.I0 + L.G0 - 1) / L.G0);
+        L.r0 += L.r0 & 1;  // 16-B box rows
+        L.G0 = static_cast<int>((L.I0 + L.r0 - 1) / L.r0);
+        L.G1 = static_cast<int>((L.I1 + cm - 1) / cm);
+        L.t1 = static_cast<int>((L.I1 + L.G1 - 1) / L.G1);
+        L.G1 = static_cast<int>((L.I1 + L.t1 - 1) / L.t1);
+        L.ntiles = L.G0 * L.G1;
+        const size_t red = static_cast<size_t>(2) * kBoxNWC * rm * 8;
+        const size_t bars = 2 * kMaxStages * 8;
+        const size_t box = static_cast<size_t>(L.r0) * L.t1 * 8;
+        const size_t ring = kSmemBudget - red - bars - rm * 8 - 1024;
+        L.stages = static_cast<int>(std::min<size_t>(kMaxStages, ring / box));
+        L.stage_dbl = static_cast<int>(((box + 127) & ~size_t(127)) / 8);  // 128-B aligned
+        L.stages = static_cast<int>(std::min<size_t>(L.stages, ring / (L.stage_dbl * 8)));
+        L.smem = (static_cast<size_t>(L.stages) * L.stage_dbl + rm) * 8 + red + bars;
+        return;
+    }
     L.G0 = static_cast<int>((L.I0 + rmax - 1) / rmax);
     L.r0 = static_cast<int>((L.I0 + L.G0 - 1) / L.G0);
+    // Row tiles in whole 32-B sectors when the column stride allows it, so
+    // neighbouring tiles never share a DRAM sector (it would be fetched twice).
+    const int q = (L.I0 % 4 == 0) ? 4 : (L.tma ? 2 : 1);
+    if (L.r0 % q) {
+        L.r0 += q - L.r0 % q;
+        if (L.r0 > rmax) L.r0 = rmax;
+        L.G0 = static_cast<int>((L.I0 + L.r0 - 1) / L.r0);
+    }
     L.G1 = static_cast<int>((L.I1 + cmax - 1) / cmax);
     L.t1 = static_cast<int>((L.I1 + L.G1 - 1) / L.G1);
     L.ntiles = L.G0 * L.G1;
@@ -432,7 +754,8 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
         const int g0 = tile % L.G0, g1 = tile / L.G0;
         const int64_t r = std::min<int64_t>(L.r0, L.I0 - int64_t(g0) * L.r0);
         const int64_t c = std::min<int64_t>(L.t1, L.I1 - int64_t(g1) * L.t1);
-        return static_cast<double>(r * c + 512);
+        // bytes dominate; zero-filled edge boxes still cost consumer issue time
+        return static_cast<double>(r * c) + 512.0;
     };
     double total = 0.0;
     for (int t = 0; t < L.ntiles; ++t) total += panel_cost(t) * static_cast<double>(L.O);
@@ -571,17 +894,93 @@ std::shared_ptr<SweepPlan> get_plan(r1_context* ctx, const uint64_t* dims, int o
     return P;
 }
 
-template <int NRA, int NCB, int STAGES>
-void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
-    static bool configured = false;  // per instantiation; attribute is per-function
-    auto kern = sweep3_kernel<NRA, NCB, STAGES>;
-    if (!configured) {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        R1_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess)
+            fail(R1_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 3-D map over the view A[i0, i1, o] (fp64, no swizzle, zero OOB fill).
+CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t box_cols) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(L.I0), static_cast<cuuint64_t>(L.I1),
+                                static_cast<cuuint64_t>(L.O)};
+    const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(L.I0) * 8,
+                                   static_cast<cuuint64_t>(L.I0) * L.I1 * 8};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols),
+                               1};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), gdim,
+                             gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(R1_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+template <int NRA, int NCB, int STAGES, bool TMA>
+void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const CUtensorMap& m) {
+    static int configured_device = -1;  // attribute is per function (and device)
+    auto kern = sweep3_kernel<NRA, NCB, STAGES, TMA>;
+    if (configured_device != ctx->device) {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(L.smem)));
-        configured = true;
+        configured_device = ctx->device;
     }
-    kern<<<L.ncta, kThreads, L.smem, ctx->stream>>>(a);
+    kern<<<L.ncta, kThreads, L.smem, ctx->stream>>>(a, m);
     check_launch(ctx, "sweep3_kernel");
+}
+
+template <int NRA, bool SR>
+void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
+    static int configured_device = -1;
+    auto kern = sweep3_box_kernel<NRA, kBoxNCB, kBoxNWC, SR>;
+    if (configured_device != ctx->device) {
+        R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSmemBudget)));
+        configured_device = ctx->device;
+    }
+    BoxMaps maps;
+    const int64_t rem0 = L.I0 - static_cast<int64_t>(L.G0 - 1) * L.r0;
+    const int64_t rem1 = L.I1 - static_cast<int64_t>(L.G1 - 1) * L.t1;
+    maps.m[0] = make_map(a.A, L, L.r0, L.t1);
+    maps.m[1] = make_map(a.A, L, rem0, L.t1);
+    maps.m[2] = make_map(a.A, L, L.r0, rem1);
+    maps.m[3] = make_map(a.A, L, rem0, rem1);
+    kern<<<L.ncta, (kBoxNWC + 1) * 32, L.smem, ctx->stream>>>(a, maps, L.stages, L.stage_dbl);
+    check_launch(ctx, "sweep3_box_kernel");
+}
+
+template <int NRA, int NCB, int STAGES>
+void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
+    if (L.tma) {
+        static const char* sr = std::getenv("R1_SWEEP_STAGE_REGS");
+        const bool stage_regs = sr ? std::atoi(sr) != 0 : true;
+        if (L.nra == 4) {
+            if (stage_regs) launch_box<4, true>(ctx, L, a);
+            else launch_box<4, false>(ctx, L, a);
+        } else {
+            if (stage_regs) launch_box<2, true>(ctx, L, a);
+            else launch_box<2, false>(ctx, L, a);
+        }
+    } else {
+        CUtensorMap m;
+        std::memset(&m, 0, sizeof(m));
+        launch_sweep_t<NRA, NCB, STAGES, false>(ctx, L, a, m);
+    }
 }
 
 int grid_for(int64_t n, int threads, int num_sms) {
@@ -642,6 +1041,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.r0 = L.r0;
         s.t1 = L.t1;
         s.G0 = L.G0;
+        s.rbox = L.r0;
         s.segs = reinterpret_cast<const Seg*>(meta + L.seg_off);
         s.cta_seg = meta + L.cta_off;
         s.P01 = resolve(L.p01);
@@ -649,6 +1049,11 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.P0_stride = L.I0 * L.O;
         s.P1 = L.out_c1.where == Where::None ? nullptr : resolve(L.p1);
         s.P1_stride = L.I1 * L.O;
+        s.trace = (&L == &P->levels.front()) ? ctx->dbg_sweep_trace : nullptr;
+        {
+            static const char* dm = std::getenv("R1_DEBUG_SWEEP_MODE");
+            s.debug_mode = dm ? std::atoi(dm) : 0;
+        }
         if (L.nra == 4)
             launch_sweep<4, 8, 3>(ctx, L, s);
         else if (L.nra == 2)
