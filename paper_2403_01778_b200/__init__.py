@@ -518,6 +518,24 @@ def largest_magnitude_eigenpair(s: np.ndarray, ctx: Optional[Context] = None) ->
     return EigPair(val.value, vec)
 
 
+def eig_blocks(j: SymBlockMatrix, ctx: Optional[Context] = None):
+    """Largest-magnitude eigenpair of the block matrix J on the device (the
+    solver's eigen step).  Returns (EigPair, info dict)."""
+    ctx = ctx or default_context()
+    d = dims_arr(j.block_dims())
+    n = j.total_dim()
+    val = ctypes.c_double()
+    vec = np.empty(n)
+    info = (ctypes.c_int * 5)()
+    stats = np.zeros(5)
+    check(lib().r1x_eig_blocks_info(ctx.handle, u64p(d), j.order(), dptr(j.blocks),
+                                    ctypes.byref(val), dptr(vec), info, dptr(stats)))
+    keys = ["converged", "pick", "steps", "restarts", "breakdowns"]
+    inf = dict(zip(keys, [int(v) for v in info]))
+    inf.update(theta_lo=stats[0], theta_hi=stats[1], res_lo=stats[2], res_hi=stats[3])
+    return EigPair(val.value, vec), inf
+
+
 def rayleigh_quotient_step(s: np.ndarray, x, ctx: Optional[Context] = None):
     """sym_eig.hpp:37-38 on the device; None reproduces std::nullopt."""
     ctx = ctx or default_context()

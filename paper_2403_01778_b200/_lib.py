@@ -104,6 +104,8 @@ SIGNATURES = {
 # Diagnostics not in the public header (tests / bench only).
 EXTRA_SIGNATURES = {
     "r1x_set_sweep_trace": (ctypes.c_int, [_vp, _vp]),
+    "r1x_eig_blocks_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp, _dp,
+                                           ctypes.POINTER(ctypes.c_int), _dp]),
     "r1x_sweep_plan_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_int64)]),
 }

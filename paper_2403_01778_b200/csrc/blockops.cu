@@ -6,6 +6,7 @@
 //   block_matvec     y = J x      (SymBlockMatrix::matvec, nepv.cpp:110-134)
 //   dot_device       x'y
 #include "common.cuh"
+#include "blockmv.cuh"
 
 namespace r1 {
 
@@ -60,86 +61,19 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int n, doub
     if (threadIdx.x == 0) *out = s;
 }
 
-// ---- block matvec ---------------------------------------------------------
-// Pass 1: one CTA per (block, 64-column chunk): column dots (B' x_m)[j] for
-// the chunk's columns (complete), and row partials (B x_n)[i] over the chunk.
-// Pass 2: each output entry sums its contributions in a fixed order.
-constexpr int kMvChunk = 64;
-
-struct MvTask {
-    const double* B;
-    int64_t rows, cols;
-    int64_t xm_off, xn_off;
-    int64_t coldot_off;  // into coldot buffer (cols entries)
-    int64_t part_off;    // into row-partial buffer (nchunk * rows)
-    int chunk;
-};
-
-__global__ void mv_pass1_kernel(const MvTask* __restrict__ tasks, const double* __restrict__ x,
-                                double* __restrict__ coldot, double* __restrict__ part) {
-    const MvTask t = tasks[blockIdx.x];
-    const int64_t j0 = static_cast<int64_t>(t.chunk) * kMvChunk;
-    const int64_t nc = t.cols - j0 < kMvChunk ? t.cols - j0 : int64_t(kMvChunk);
-    const double* xm = x + t.xm_off;
-    const double* xn = x + t.xn_off;
-    // row partials
-    for (int64_t i = threadIdx.x; i < t.rows; i += blockDim.x) {
-        double s = 0.0;
-        for (int64_t j = 0; j < nc; ++j) s = fma(t.B[i + (j0 + j) * t.rows], xn[j0 + j], s);
-        part[t.part_off + static_cast<int64_t>(t.chunk) * t.rows + i] = s;
-    }
-    // column dots: warp per column
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int64_t j = warp; j < nc; j += nw) {
-        const double* c = t.B + (j0 + j) * t.rows;
-        double s = 0.0;
-        for (int64_t i = lane; i < t.rows; i += 32) s = fma(c[i], xm[i], s);
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) coldot[t.coldot_off + j0 + j] = s;
-    }
+// ---- block matvec (blockmv.cuh), two launches over a fixed grid ----------
+__global__ void mv_phase_a_kernel(const BlockOp* __restrict__ op, const double* __restrict__ x) {
+    blockop_phase_a(*op, x);
 }
 
-struct MvOut {
-    int order;
-    int64_t dims[16];
-    int64_t offs[17];
-    // per pair (m<n): coldot offset and row-partial offset, nchunk
-    int64_t pc_off[136];
-    int64_t pp_off[136];
-    int pnch[136];
-    double scale;
-};
-
-__device__ __forceinline__ int pair_idx(int m, int n, int d) { return m * (2 * d - m - 1) / 2 + (n - m - 1); }
-
-__global__ void mv_pass2_kernel(const MvOut* __restrict__ o, const double* __restrict__ coldot,
-                                const double* __restrict__ part, double* __restrict__ y) {
-    const int d = o->order;
-    const int64_t total = o->offs[d];
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int m = 0;
-        while (t >= o->offs[m + 1]) ++m;
-        const int64_t i = t - o->offs[m];
-        double s = 0.0;
-        // y_m += B(k,m)' x_k for k < m, then B(m,n) x_n for n > m (pair order)
-        for (int k = 0; k < m; ++k) s += coldot[o->pc_off[pair_idx(k, m, d)] + i];
-        for (int n = m + 1; n < d; ++n) {
-            const int p = pair_idx(m, n, d);
-            const double* pp = part + o->pp_off[p] + i;
-            double r = 0.0;
-            for (int c = 0; c < o->pnch[p]; ++c) r += pp[static_cast<int64_t>(c) * o->dims[m]];
-            s += r;
-        }
-        y[t] = s * o->scale;
-    }
+__global__ void mv_phase_b_kernel(const BlockOp* __restrict__ op, double* __restrict__ y) {
+    blockop_phase_b(*op, y, blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                    static_cast<int64_t>(gridDim.x) * blockDim.x);
 }
 
 struct MvPlan {
-    std::vector<uint64_t> dims;
-    DeviceBuffer tasks, out, coldot, part;
-    int ntasks = 0;
+    BlockOp op;
+    DeviceBuffer dop, coldot, rowpart;
     const double* blocks = nullptr;
 };
 
@@ -171,63 +105,29 @@ void dot_device(r1_context* ctx, const double* x, const double* y, uint64_t n, d
 void block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                   const double* x, double* y) {
     if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "block_matvec: bad order");
-    std::vector<uint64_t> key(dims, dims + order);
-    auto& plans = mv_plans();
-    auto& P = plans[{ctx, key}];
+    auto& P = mv_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
     if (!P || P->blocks != blocks) {
-        if (!P) P = std::make_shared<MvPlan>();
-        P->dims = key;
-        P->blocks = blocks;
-        std::vector<MvTask> tasks;
-        MvOut o{};
-        o.order = order;
-        o.offs[0] = 0;
-        for (int k = 0; k < order; ++k) {
-            o.dims[k] = static_cast<int64_t>(dims[k]);
-            o.offs[k + 1] = o.offs[k] + o.dims[k];
+        if (!P) {
+            P = std::make_shared<MvPlan>();
+            int64_t cn = 0, rn = 0;
+            blockop_layout(P->op, dims, order, &cn, &rn);
+            P->coldot.ensure(std::max<int64_t>(cn, 1) * sizeof(double));
+            P->rowpart.ensure(std::max<int64_t>(rn, 1) * sizeof(double));
+            P->op.coldot = P->coldot.as<double>();
+            P->op.rowpart = P->rowpart.as<double>();
+            P->dop.ensure(sizeof(BlockOp));
         }
-        o.scale = 1.0 / static_cast<double>(order - 1);
-        int64_t coff = 0, poff = 0;
-        uint64_t boff = 0;
-        int p = 0;
-        for (int m = 0; m < order; ++m)
-            for (int n = m + 1; n < order; ++n, ++p) {
-                const int64_t rows = o.dims[m], cols = o.dims[n];
-                const int nch = static_cast<int>((cols + kMvChunk - 1) / kMvChunk);
-                o.pc_off[p] = coff;
-                o.pp_off[p] = poff;
-                o.pnch[p] = nch;
-                for (int c = 0; c < nch; ++c)
-                    tasks.push_back(MvTask{blocks + boff, rows, cols, o.offs[m], o.offs[n], coff,
-                                           poff, c});
-                coff += cols;
-                poff += static_cast<int64_t>(nch) * rows;
-                boff += static_cast<uint64_t>(rows * cols);
-            }
-        P->ntasks = static_cast<int>(tasks.size());
-        P->tasks.ensure(tasks.size() * sizeof(MvTask));
-        P->out.ensure(sizeof(MvOut));
-        P->coldot.ensure(std::max<int64_t>(coff, 1) * sizeof(double));
-        P->part.ensure(std::max<int64_t>(poff, 1) * sizeof(double));
-        R1_CUDA(cudaMemcpyAsync(P->tasks.ptr, tasks.data(), tasks.size() * sizeof(MvTask),
-                                cudaMemcpyHostToDevice, ctx->stream));
-        R1_CUDA(cudaMemcpyAsync(P->out.ptr, &o, sizeof(MvOut), cudaMemcpyHostToDevice,
+        P->blocks = blocks;
+        P->op.blocks = blocks;
+        R1_CUDA(cudaMemcpyAsync(P->dop.ptr, &P->op, sizeof(BlockOp), cudaMemcpyHostToDevice,
                                 ctx->stream));
-        R1_CUDA(cudaStreamSynchronize(ctx->stream));
     }
-    mv_pass1_kernel<<<P->ntasks, 256, 0, ctx->stream>>>(P->tasks.as<MvTask>(), x,
-                                                       P->coldot.as<double>(),
-                                                       P->part.as<double>());
-    check_launch(ctx, "mv_pass1_kernel");
-    const uint64_t total = [&] {
-        uint64_t s = 0;
-        for (int k = 0; k < order; ++k) s += dims[k];
-        return s;
-    }();
-    const int g = static_cast<int>(std::min<uint64_t>((total + 255) / 256, 1024));
-    mv_pass2_kernel<<<g, 256, 0, ctx->stream>>>(P->out.as<MvOut>(), P->coldot.as<double>(),
-                                               P->part.as<double>(), y);
-    check_launch(ctx, "mv_pass2_kernel");
+    const int ga = std::max(1, std::min(P->op.ntasks, 4 * ctx->num_sms));
+    mv_phase_a_kernel<<<ga, 256, 0, ctx->stream>>>(P->dop.as<BlockOp>(), x);
+    check_launch(ctx, "mv_phase_a_kernel");
+    const int gb = static_cast<int>(std::min<int64_t>((P->op.n + 255) / 256, 1024));
+    mv_phase_b_kernel<<<std::max(gb, 1), 256, 0, ctx->stream>>>(P->dop.as<BlockOp>(), y);
+    check_launch(ctx, "mv_phase_b_kernel");
 }
 
 void forget_matvec_plans(r1_context* ctx) {

@@ -1,0 +1,573 @@
+// Largest-magnitude eigenpair of J on the device.
+//
+// Replaces rank1::largest_magnitude_eigenpair(J.dense()) (reference
+// proj/src/sym_eig.cpp:206-229: tred2 + implicit QL on the dense sum(I) x
+// sum(I) matrix, O(n^3) per HOSCF iteration) by Lanczos on the block operator:
+//
+//   * one persistent cooperative kernel (grid = #SMs, grid.sync between
+//     phases) runs the whole solve; the host launches once and reads nothing;
+//   * matvec through the blocks (blockmv.cuh), never forming dense J;
+//   * full reorthogonalisation, classical Gram-Schmidt applied twice;
+//   * every `check_every` steps CTA 0 computes BOTH extreme eigenvalues of
+//     the tridiagonal T by Sturm-count multisection, their T-eigenvectors by
+//     inverse iteration and the Ritz residual bounds |beta_m s_m|; the solve
+//     stops when both ends satisfy bound <= tol * max(|theta_lo|,|theta_hi|)
+//     (or the Krylov space is the whole space, then T's spectrum is exact);
+//   * the reference's pick rule (lo iff |lo| > |hi| (1 + 1e-12),
+//     sym_eig.cpp:214-216) and sign rule (largest-|entry| positive, first
+//     index on ties, :223-227) are applied to the Ritz pair;
+//   * a breakdown (invariant subspace) injects a fresh random direction;
+//     non-convergence at the size limit restarts from the two extreme Ritz
+//     vectors.
+// All reductions have a fixed order over a fixed grid: deterministic.
+#include "common.cuh"
+#include "blockmv.cuh"
+
+#include <cooperative_groups.h>
+
+#include <cmath>
+#include <map>
+#include <memory>
+#include <vector>
+
+namespace cg = cooperative_groups;
+
+namespace r1 {
+
+namespace {
+
+constexpr int kEigThreads = 512;
+constexpr int kMaxKrylov = 512;
+
+struct EigArgs {
+    const BlockOp* op;
+    int64_t n;
+    int maxm;
+    int check_every;
+    int min_steps;
+    int max_restarts;
+    double tol;
+    const double* x0;
+    double* V;       // n x (maxm + 1), column-major
+    double* w;       // n
+    double* h;       // maxm + 1
+    double* h2;      // maxm + 1
+    double* alpha;   // maxm
+    double* beta;    // maxm
+    double* part;    // 4 * gridDim
+    double* sT;      // 2 * maxm: T-eigenvectors (lo, hi)
+    int* ctl;        // [0] state, [1] picked end, [2] steps, [3] restarts, [4] breakdowns
+    double* stats;   // [theta_lo, theta_hi, res_lo, res_hi, value]
+    double* out_value;
+    double* out_vec;
+};
+
+__device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
+    uint64_t z = i * 0x9e3779b97f4a7c15ull + salt;
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+}
+
+// Fixed-order CTA reduction; result valid in every thread.
+__device__ double cta_sum(double v, double* sh) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int k = 0; k < nw; ++k) s += sh[k];
+    return s;
+}
+
+// Sum of gridDim partials stored at part[slot*gridDim + b], identical in all threads.
+__device__ double grid_total(const double* part, int slot) {
+    double s = 0.0;
+    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) s += part[slot * gridDim.x + b];
+    return s;
+}
+
+// Number of eigenvalues of the symmetric tridiagonal (a, b) that are < x.
+__device__ int sturm_count(const double* a, const double* b, int m, double x, double pivmin) {
+    int c = 0;
+    double q = a[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) ++c;
+    for (int i = 1; i < m; ++i) {
+        q = (a[i] - x) - b[i - 1] * b[i - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        if (q < 0) ++c;
+    }
+    return c;
+}
+
+// Inverse iteration for the eigenvector of T (size m) at shift theta; s unit.
+__device__ void tri_eigvec(const double* a, const double* b, int m, double theta, double tnorm,
+                           double* s, double* work) {
+    // work: d[m], du[m], du2[m], dl[m], piv flags in ipiv (as doubles)
+    double* d = work;
+    double* du = work + m;
+    double* du2 = work + 2 * m;
+    double* l = work + 3 * m;
+    double* sw = work + 4 * m;  // 1.0 if rows i,i+1 were swapped
+    const double tiny = 1e-300 + 2.2e-16 * tnorm;
+    for (int i = 0; i < m; ++i) {
+        d[i] = a[i] - theta;
+        du[i] = i + 1 < m ? b[i] : 0.0;
+        du2[i] = 0.0;
+    }
+    // LU with partial pivoting of the tridiagonal (LAPACK dgttrf pattern)
+    for (int i = 0; i + 1 < m; ++i) {
+        const double sub = b[i];  // T(i+1, i)
+        if (fabs(d[i]) >= fabs(sub)) {
+            sw[i] = 0.0;
+            const double f = d[i] != 0.0 ? sub / d[i] : 0.0;
+            l[i] = f;
+            d[i + 1] -= f * du[i];
+        } else {
+            sw[i] = 1.0;
+            const double f = d[i] / sub;
+            l[i] = f;
+            d[i] = sub;
+            const double t = du[i];
+            du[i] = d[i + 1];
+            d[i + 1] = t - f * d[i + 1];
+            if (i + 2 < m) {
+                du2[i] = du[i + 1];
+                du[i + 1] = -f * du[i + 1];
+            }
+        }
+    }
+    for (int i = 0; i < m; ++i)
+        if (fabs(d[i]) < tiny) d[i] = d[i] < 0 ? -tiny : tiny;
+    for (int i = 0; i < m; ++i) s[i] = 1.0;
+    for (int it = 0; it < 3; ++it) {
+        // forward: apply L^-1 P
+        for (int i = 0; i + 1 < m; ++i) {
+            if (sw[i] == 0.0) {
+                s[i + 1] -= l[i] * s[i];
+            } else {
+                const double t = s[i];
+                s[i] = s[i + 1];
+                s[i + 1] = t - l[i] * s[i];
+            }
+        }
+        // back: U^-1
+        s[m - 1] /= d[m - 1];
+        if (m > 1) s[m - 2] = (s[m - 2] - du[m - 2] * s[m - 1]) / d[m - 2];
+        for (int i = m - 3; i >= 0; --i)
+            s[i] = (s[i] - du[i] * s[i + 1] - du2[i] * s[i + 2]) / d[i];
+        double nrm = 0.0;
+        for (int i = 0; i < m; ++i) nrm += s[i] * s[i];
+        nrm = sqrt(nrm);
+        for (int i = 0; i < m; ++i) s[i] /= nrm;
+    }
+}
+
+// CTA 0: extremes of T_m, eigenvectors, bounds, convergence decision.
+__device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact, int restarts) {
+    __shared__ double ta[kMaxKrylov], tb[kMaxKrylov];
+    __shared__ double lohi[4];  // [a_lo, b_lo, a_hi, b_hi] intervals
+    __shared__ int cnt[kEigThreads];
+    __shared__ double work[5 * kMaxKrylov];
+    __shared__ double sv[2][kMaxKrylov];
+    __shared__ double theta[2];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        ta[i] = a.alpha[i];
+        tb[i] = i + 1 < m ? a.beta[i] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double lo = 1e300, hi = -1e300, tn = 0.0;
+        for (int i = 0; i < m; ++i) {
+            const double r = fabs(i > 0 ? tb[i - 1] : 0.0) + fabs(i + 1 < m ? tb[i] : 0.0);
+            lo = fmin(lo, ta[i] - r);
+            hi = fmax(hi, ta[i] + r);
+            tn = fmax(tn, fabs(ta[i]) + r);
+        }
+        const double pad = 1e-14 * tn + 1e-300;
+        lohi[0] = lo - pad;
+        lohi[1] = hi + pad;
+        lohi[2] = lo - pad;
+        lohi[3] = hi + pad;
+        theta[0] = tn;  // temp: T norm
+    }
+    __syncthreads();
+    const double tnorm = theta[0];
+    const double pivmin = 1e-300 + 1e-30 * tnorm * tnorm;
+    const int half = blockDim.x / 2;
+    const int side = threadIdx.x < half ? 0 : 1;  // 0: lowest, 1: highest
+    const int k = threadIdx.x - side * half;
+    for (int round = 0; round < 12; ++round) {
+        const double lo = lohi[2 * side], hi = lohi[2 * side + 1];
+        const double x = lo + (hi - lo) * static_cast<double>(k + 1) / static_cast<double>(half + 1);
+        cnt[threadIdx.x] = sturm_count(ta, tb, m, x, pivmin);
+        __syncthreads();
+        if (k == 0) {
+            // lowest: first point with count >= 1; highest: first with count >= m
+            const int target = side == 0 ? 1 : m;
+            int f = half;
+            for (int t = 0; t < half; ++t)
+                if (cnt[side * half + t] >= target) {
+                    f = t;
+                    break;
+                }
+            const double nlo = f == 0 ? lo : lo + (hi - lo) * static_cast<double>(f) / (half + 1);
+            const double nhi =
+                f == half ? hi : lo + (hi - lo) * static_cast<double>(f + 1) / (half + 1);
+            lohi[2 * side] = nlo;
+            lohi[2 * side + 1] = nhi;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        theta[0] = 0.5 * (lohi[0] + lohi[1]);
+        theta[1] = 0.5 * (lohi[2] + lohi[3]);
+        tri_eigvec(ta, tb, m, theta[0], tnorm, sv[0], work);
+        tri_eigvec(ta, tb, m, theta[1], tnorm, sv[1], work);
+        const double res_lo = fabs(beta_last * sv[0][m - 1]);
+        const double res_hi = fabs(beta_last * sv[1][m - 1]);
+        const double scale = fmax(fabs(theta[0]), fabs(theta[1]));
+        const bool conv = exact || (res_lo <= a.tol * scale && res_hi <= a.tol * scale);
+        const int pick = fabs(theta[0]) > fabs(theta[1]) * (1.0 + 1e-12) ? 0 : 1;
+        a.stats[0] = theta[0];
+        a.stats[1] = theta[1];
+        a.stats[2] = res_lo;
+        a.stats[3] = res_hi;
+        a.stats[4] = theta[pick];
+        a.ctl[0] = conv ? 1 : 0;
+        a.ctl[1] = pick;
+        a.ctl[2] = m;
+        a.ctl[3] = restarts;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        a.sT[i] = sv[0][i];
+        a.sT[kMaxKrylov + i] = sv[1][i];
+    }
+}
+
+__global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ BlockOp op;
+    __shared__ double red[32];
+    if (threadIdx.x == 0) op = *a.op;
+    __syncthreads();
+    const int64_t n = a.n;
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int G = gridDim.x;
+
+    // ---- start vector
+    for (int64_t i = gtid; i < n; i += gstride) {
+        const double r = hash_unit(static_cast<uint64_t>(i), 0x5eedull);
+        a.w[i] = a.x0 ? a.x0[i] + 1e-3 * r / sqrt(static_cast<double>(n)) : r;
+    }
+    int restarts = 0, breakdowns = 0;
+    auto normalize_w_into = [&](double* dst) {
+        double s = 0.0;
+        for (int64_t i = gtid; i < n; i += gstride) s = fma(a.w[i], a.w[i], s);
+        s = cta_sum(s, red);
+        if (threadIdx.x == 0) a.part[blockIdx.x] = s;
+        grid.sync();
+        const double nrm = sqrt(grid_total(a.part, 0));
+        for (int64_t i = gtid; i < n; i += gstride) dst[i] = a.w[i] / nrm;
+        grid.sync();
+        return nrm;
+    };
+    grid.sync();
+    normalize_w_into(a.V);
+
+    // dots h[k] = V[:,k]' w for k <= j (CTA per column, round robin)
+    auto dots = [&](double* hh, int j) {
+        for (int k = blockIdx.x; k <= j; k += G) {
+            const double* vk = a.V + static_cast<int64_t>(k) * n;
+            double s = 0.0;
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(vk[i], a.w[i], s);
+            s = cta_sum(s, red);
+            if (threadIdx.x == 0) hh[k] = s;
+        }
+        grid.sync();
+    };
+    // w -= V[:, :j+1] hh; optionally accumulate ||w||^2 partials into part[0]
+    auto update = [&](const double* hh, int j, bool norm) {
+        double s = 0.0;
+        for (int64_t i = gtid; i < n; i += gstride) {
+            double acc = 0.0;
+            for (int k = 0; k <= j; ++k) acc = fma(a.V[i + static_cast<int64_t>(k) * n], hh[k], acc);
+            const double wi = a.w[i] - acc;
+            a.w[i] = wi;
+            s = fma(wi, wi, s);
+        }
+        if (norm) {
+            s = cta_sum(s, red);
+            if (threadIdx.x == 0) a.part[blockIdx.x] = s;
+        }
+        grid.sync();
+    };
+
+    int j = 0;
+    double anorm = 0.0;
+    for (;;) {
+        // ---- one Lanczos step on v_j
+        const double* vj = a.V + static_cast<int64_t>(j) * n;
+        blockop_phase_a(op, vj);
+        grid.sync();
+        blockop_phase_b(op, a.w, gtid, gstride);
+        grid.sync();
+        dots(a.h, j);
+        update(a.h, j, false);
+        dots(a.h2, j);
+        update(a.h2, j, true);
+        double nrm = sqrt(grid_total(a.part, 0));
+        const double alpha = a.h[j] + a.h2[j];
+        anorm = fmax(anorm, fabs(alpha) + nrm + (j > 0 ? a.beta[j - 1] : 0.0));
+        const bool space_full = (j + 1 == n);
+        bool breakdown = !space_full && nrm <= 1e-13 * anorm;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.alpha[j] = alpha;
+            a.beta[j] = breakdown ? 0.0 : nrm;
+        }
+        if (breakdown) {
+            // invariant subspace: continue with a fresh direction orthogonal to V
+            ++breakdowns;
+            for (int64_t i = gtid; i < n; i += gstride)
+                a.w[i] = hash_unit(static_cast<uint64_t>(i), 0xb00ull + breakdowns);
+            grid.sync();
+            dots(a.h, j);
+            update(a.h, j, false);
+            dots(a.h2, j);
+            update(a.h2, j, true);
+            nrm = sqrt(grid_total(a.part, 0));
+        }
+        if (!space_full) {
+            for (int64_t i = gtid; i < n; i += gstride)
+                a.V[i + static_cast<int64_t>(j + 1) * n] = a.w[i] / nrm;
+        }
+        grid.sync();
+        ++j;
+        const bool size_limit = (j == a.maxm) || space_full;
+        if (((j >= a.min_steps && j % a.check_every == 0) && !breakdown) || size_limit) {
+            if (blockIdx.x == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts);
+            grid.sync();
+            if (a.ctl[0]) break;
+            if (size_limit) {
+                if (restarts >= a.max_restarts) break;  // best effort: ctl[0] stays 0
+                // restart from (x_lo + x_hi): both ends stay represented
+                ++restarts;
+                for (int64_t i = gtid; i < n; i += gstride) {
+                    double s0 = 0.0, s1 = 0.0;
+                    for (int k = 0; k < j; ++k) {
+                        const double v = a.V[i + static_cast<int64_t>(k) * n];
+                        s0 = fma(v, a.sT[k], s0);
+                        s1 = fma(v, a.sT[kMaxKrylov + k], s1);
+                    }
+                    a.w[i] = s0 + s1;
+                }
+                grid.sync();
+                normalize_w_into(a.V);
+                j = 0;
+                anorm = 0.0;
+            }
+        }
+    }
+
+    // ---- Ritz vector of the picked end
+    const int m = j;
+    const int pick = a.ctl[1];
+    const double* s = a.sT + (pick ? kMaxKrylov : 0);
+    double best = -1.0;
+    int64_t besti = 0;
+    double ss = 0.0;
+    for (int64_t i = gtid; i < n; i += gstride) {
+        double x = 0.0;
+        for (int k = 0; k < m; ++k) x = fma(a.V[i + static_cast<int64_t>(k) * n], s[k], x);
+        a.out_vec[i] = x;
+        ss = fma(x, x, ss);
+        if (fabs(x) > best) {
+            best = fabs(x);
+            besti = i;
+        }
+    }
+    // argmax |x| with the lowest index on ties (sym_eig.cpp:223-227), and ||x||
+    __shared__ double bv[32];
+    __shared__ int64_t bi[32];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, besti, off);
+        if (ov > best || (ov == best && oi < besti)) {
+            best = ov;
+            besti = oi;
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        bv[warp] = best;
+        bi[warp] = besti;
+    }
+    ss = cta_sum(ss, red);
+    if (threadIdx.x == 0) {
+        double b0 = bv[0];
+        int64_t i0 = bi[0];
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k)
+            if (bv[k] > b0 || (bv[k] == b0 && bi[k] < i0)) {
+                b0 = bv[k];
+                i0 = bi[k];
+            }
+        a.part[G + blockIdx.x] = b0;
+        a.part[2 * G + blockIdx.x] = static_cast<double>(i0);
+        a.part[blockIdx.x] = ss;
+    }
+    grid.sync();
+    double b0 = -1.0;
+    int64_t i0 = 0;
+    for (int b = 0; b < G; ++b) {
+        const double v = a.part[G + b];
+        const int64_t ii = static_cast<int64_t>(a.part[2 * G + b]);
+        if (v > b0 || (v == b0 && ii < i0)) {
+            b0 = v;
+            i0 = ii;
+        }
+    }
+    const double nrm = sqrt(grid_total(a.part, 0));
+    const double sgn = a.out_vec[i0] < 0.0 ? -1.0 : 1.0;
+    grid.sync();
+    for (int64_t i = gtid; i < n; i += gstride) a.out_vec[i] = sgn * a.out_vec[i] / nrm;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.out_value = a.stats[4];
+        a.ctl[2] = m;
+        a.ctl[3] = restarts;
+        a.ctl[4] = breakdowns;
+    }
+}
+
+struct EigPlan {
+    BlockOp op;
+    DeviceBuffer dop;
+    int64_t coldot_n = 0, rowpart_n = 0;
+};
+
+}  // namespace
+
+namespace {
+
+void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_dev,
+                 double* vec_dev, int* info_host, double* stats_host) {
+    const int64_t n = P.op.n;
+    const int maxm = static_cast<int>(std::min<int64_t>(n, 320));
+    const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
+                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 128;
+    ctx->ws_eig.ensure(need * sizeof(double));
+    double* base = ctx->ws_eig.as<double>();
+    int64_t off = 0;
+    auto take = [&](int64_t k) {
+        double* p = base + off;
+        off += (k + 7) & ~int64_t(7);
+        return p;
+    };
+    EigArgs a{};
+    a.n = n;
+    a.maxm = maxm;
+    a.check_every = n <= 64 ? 1 : 8;
+    a.min_steps = static_cast<int>(std::min<int64_t>(n, 16));
+    a.max_restarts = 6;
+    a.tol = 1e-13;
+    a.x0 = x0;
+    a.V = take(n * (maxm + 1));
+    a.w = take(n);
+    a.h = take(maxm + 1);
+    a.h2 = take(maxm + 1);
+    a.alpha = take(maxm);
+    a.beta = take(maxm);
+    a.part = take(4 * ctx->num_sms);
+    a.sT = take(2 * kMaxKrylov);
+    a.stats = take(8);
+    a.ctl = reinterpret_cast<int*>(take(4));
+    BlockOp op = P.op;
+    op.coldot = take(std::max<int64_t>(P.coldot_n, 1));
+    op.rowpart = take(std::max<int64_t>(P.rowpart_n, 1));
+    P.dop.ensure(sizeof(BlockOp));
+    R1_CUDA(cudaMemcpyAsync(P.dop.ptr, &op, sizeof(BlockOp), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    a.op = P.dop.as<BlockOp>();
+    a.out_value = value_dev;
+    a.out_vec = vec_dev;
+    R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
+    int per_sm = 0;
+    R1_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_kernel, kEigThreads, 0));
+    if (per_sm < 1) fail(R1_ERR_CUDA, "lanczos kernel cannot be resident");
+    void* args[] = {&a};
+    R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel),
+                                        dim3(ctx->num_sms), dim3(kEigThreads), args, 0,
+                                        ctx->stream));
+    check_launch(ctx, "lanczos_kernel");
+    if (info_host || stats_host) {
+        int ctl[5];
+        double st[5];
+        R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (info_host)
+            for (int k = 0; k < 5; ++k) info_host[k] = ctl[k];
+        if (stats_host)
+            for (int k = 0; k < 5; ++k) stats_host[k] = st[k];
+    }
+}
+
+using PlanKey = std::pair<r1_context*, std::vector<uint64_t>>;
+std::map<PlanKey, std::shared_ptr<EigPlan>>& eig_plans() {
+    static std::map<PlanKey, std::shared_ptr<EigPlan>> m;
+    return m;
+}
+
+}  // namespace
+
+void forget_eig_plans(r1_context* ctx) {
+    auto& m = eig_plans();
+    for (auto it = m.begin(); it != m.end();)
+        if (it->first.first == ctx)
+            it = m.erase(it);
+        else
+            ++it;
+}
+
+// Eigen solve on the blocks of J (dims/order), async on ctx->stream: value_dev[0],
+// vec_dev[0..n).  info_host/stats_host (nullable) force a synchronous read of
+// [converged, picked end, steps, restarts, breakdowns] / [theta_lo, theta_hi,
+// res_lo, res_hi, value].
+void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
+                const double* x0, double* value_dev, double* vec_dev, int* info_host,
+                double* stats_host) {
+    if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "eig: unsupported order");
+    auto& P = eig_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
+    if (!P) {
+        P = std::make_shared<EigPlan>();
+        blockop_layout(P->op, dims, order, &P->coldot_n, &P->rowpart_n);
+    }
+    P->op.blocks = blocks;
+    P->op.dense = nullptr;
+    run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host);
+}
+
+// Same on a dense symmetric n x n matrix S (device, column-major).
+void eig_dense(r1_context* ctx, int64_t n, const double* S, const double* x0, double* value_dev,
+               double* vec_dev, int* info_host, double* stats_host) {
+    auto& P = eig_plans()[{ctx, std::vector<uint64_t>{0, static_cast<uint64_t>(n)}}];
+    if (!P) {
+        P = std::make_shared<EigPlan>();
+        denseop_layout(P->op, n, &P->rowpart_n);
+        P->coldot_n = 0;
+    }
+    P->op.dense = S;
+    P->op.blocks = nullptr;
+    run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host);
+}
+
+}  // namespace r1

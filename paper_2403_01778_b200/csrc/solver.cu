@@ -1,0 +1,581 @@
+// Host driver of HOSCF / iHOSCF (C++), calling the device steps.  Mirrors the
+// reference's control flow (proj/src/solvers.cpp):
+//   validate            :28-32     initial_factors / random_unit_factors :34-66
+//   with_restart        :78-91     finalize_sign :70-76
+//   run_hoscf           :129-183   run_ihoscf    :185-297
+// Every numeric step runs on the device; per iteration the host reads one
+// small status record (degeneracy flag + the stop value) — plus, in iHOSCF,
+// the RQI accept decision.  The tensor never leaves HBM.
+#include "common.cuh"
+#include "solver_ops.cuh"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+namespace r1 {
+
+void forget_eig_plans(r1_context* ctx);
+void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* info);
+
+namespace {
+
+constexpr double kNan = std::numeric_limits<double>::quiet_NaN();
+
+// CounterRng (reference include/rank1/rng.hpp:10-37), host side.
+struct CounterRng {
+    uint64_t key, counter = 0;
+    static uint64_t mix(uint64_t z) {
+        z ^= z >> 30;
+        z *= 0xbf58476d1ce4e5b9ull;
+        z ^= z >> 27;
+        z *= 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        return z;
+    }
+    CounterRng(uint64_t seed, uint64_t stream) : key(mix(seed + 0x9e3779b97f4a7c15ull * (stream + 1))) {}
+    double next_unit() { return static_cast<double>(mix(key + 0x9e3779b97f4a7c15ull * ++counter) >> 11) * 0x1.0p-53; }
+};
+constexpr uint64_t kStreamInit = 2, kStreamRestart = 3;
+
+double norm2_seq(const double* v, size_t n) {
+    double s = 0.0;
+    for (size_t i = 0; i < n; ++i) s += v[i] * v[i];
+    return std::sqrt(s);
+}
+
+// normalize (matrix.cpp:62-67): returns the original norm.
+double normalize(double* v, size_t n) {
+    const double nrm = norm2_seq(v, n);
+    if (nrm > 0.0)
+        for (size_t i = 0; i < n; ++i) v[i] /= nrm;
+    return nrm;
+}
+
+// random_unit_factors (solvers.cpp:34-49).
+std::vector<double> random_unit_factors(const std::vector<uint64_t>& dims, uint64_t seed,
+                                        uint64_t stream) {
+    CounterRng rng(seed, stream);
+    std::vector<double> f;
+    for (uint64_t len : dims) {
+        std::vector<double> u(len);
+        for (double& v : u) v = rng.next_unit();
+        if (normalize(u.data(), len) == 0.0) {
+            std::fill(u.begin(), u.end(), 1.0);
+            normalize(u.data(), len);
+        }
+        f.insert(f.end(), u.begin(), u.end());
+    }
+    return f;
+}
+
+struct Degenerate : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    ~Events() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    cudaEvent_t rec(cudaStream_t s) {
+        cudaEvent_t e;
+        R1_CUDA(cudaEventCreate(&e));
+        ev.push_back(e);
+        R1_CUDA(cudaEventRecord(e, s));
+        return e;
+    }
+    static double secs(cudaEvent_t a, cudaEvent_t b) {
+        float ms = 0.f;
+        R1_CUDA(cudaEventElapsedTime(&ms, a, b));
+        return ms * 1e-3;
+    }
+};
+
+// Device working set of one solve.
+struct Work {
+    r1_context* ctx;
+    const r1_tensor* A;
+    std::vector<uint64_t> dims;
+    int d;
+    int64_t n;     // sum I_k
+    uint64_t nb;   // block entries
+    DeviceBuffer mem;
+    double *U, *Umid, *Urqi, *X, *Xprev, *Xhat, *XhatR, *Yr, *Y, *J, *Jmid, *S;
+    double *fro2, *fro2mid, *mu, *post, *postmid, *dotv;
+    int* flags;
+    PinnedBuffer hst;  // host staging
+
+    Work(r1_context* c, const r1_tensor* a, bool dense)
+        : ctx(c), A(a), dims(a->dims), d(static_cast<int>(a->dims.size())) {
+        n = 0;
+        for (auto v : dims) n += static_cast<int64_t>(v);
+        nb = blocks_numel(dims.data(), d);
+        auto al = [](int64_t k) { return (k + 31) & ~int64_t(31); };
+        const int64_t vec = al(n);
+        const int64_t total = 10 * vec + 2 * al(static_cast<int64_t>(nb)) +
+                              (dense ? al(n * n) : 0) + 7 * 64 + 64;
+        mem.ensure(total * sizeof(double));
+        double* p = mem.as<double>();
+        auto take = [&](int64_t k) {
+            double* r = p;
+            p += al(k);
+            return r;
+        };
+        U = take(n);
+        Umid = take(n);
+        Urqi = take(n);
+        X = take(n);
+        Xprev = take(n);
+        Xhat = take(n);
+        XhatR = take(n);
+        Yr = take(n);
+        Y = take(n);
+        take(n);
+        J = take(static_cast<int64_t>(nb));
+        Jmid = take(static_cast<int64_t>(nb));
+        S = dense ? take(n * n) : nullptr;
+        fro2 = take(64);
+        fro2mid = take(64);
+        mu = take(64);
+        post = take(64);
+        postmid = take(64);
+        dotv = take(64);
+        flags = reinterpret_cast<int*>(take(64));
+        hst.ensure(64 * 1024);
+    }
+
+    cudaStream_t st() const { return ctx->stream; }
+
+    void sweep(const double* u, double* jb, double* f2) {
+        sweep_blocks(ctx, A->dev, dims.data(), d, u, jb);
+        sumsq_device(ctx, jb, nb, f2);
+    }
+    // y = J xhat, then Eq.11 / KKT / lambda into out (see solver_ops.cu)
+    void post_step(const double* jb, const double* f2, const double* xh, const double* u,
+                   const double* mu_dev, double mu_host, double* out) {
+        block_matvec(ctx, dims.data(), d, jb, xh, Y);
+        r1::post_step(ctx, dims.data(), d, Y, xh, u, f2, mu_dev, mu_host, out);
+    }
+    template <typename T>
+    void fetch(T* host, const T* dev, size_t count) {
+        R1_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, st()));
+    }
+    void sync() { R1_CUDA(cudaStreamSynchronize(st())); }
+};
+
+struct RunResult {
+    std::vector<double> factors;  // host, flat
+    double lambda = 0.0;
+    bool converged = false;
+    int iterations = 0;
+    double lambda0 = 0.0;
+    std::vector<r1_iteration_record> trace;
+    std::vector<double> final_x;
+    int sweeps = 0;
+};
+
+RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0, bool accelerated) {
+    RunResult rr;
+    Events ev;
+    const cudaStream_t st = w.st();
+    const int d = w.d;
+    const int64_t n = w.n;
+    R1_CUDA(cudaMemcpyAsync(w.U, u0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    // lambda0 and J(u0): stack u0 on device (split of a unit vector = itself)
+    split_stack(w.ctx, w.dims.data(), d, w.U, nullptr, w.Xhat, w.flags);
+    cudaEvent_t e0 = ev.rec(st);
+    w.sweep(w.U, w.J, w.fro2);
+    cudaEvent_t e1 = ev.rec(st);
+    w.post_step(w.J, w.fro2, w.Xhat, w.U, nullptr, 0.0, w.post);
+    double* h = w.hst.as<double>();
+    w.fetch(h, w.post, 8);
+    w.sync();
+    rr.lambda0 = h[4];
+    rr.sweeps = 1;
+    struct Marks {
+        cudaEvent_t a, b, c, d2, e;
+    };
+    std::vector<Marks> marks;
+    bool have_prev = false;
+    double lam_prev = 0.0;
+    const double sqd = std::sqrt(static_cast<double>(d));
+    (void)sqd;
+
+    for (int k = 1; k <= o.max_iters; ++k) {
+        r1_iteration_record rec{};
+        rec.lambda_pre_rqi = kNan;
+        rec.n_sweeps = (k == 1) ? 2 : 1;
+        Marks mk;
+        mk.a = ev.rec(st);
+        eig_blocks(w.ctx, w.dims.data(), d, w.J, have_prev ? w.Xprev : nullptr, w.mu, w.X, nullptr,
+                   nullptr);
+        mk.b = ev.rec(st);
+        split_stack(w.ctx, w.dims.data(), d, w.X, w.Umid, w.Xhat, w.flags);
+        mk.c = ev.rec(st);
+        w.sweep(w.Umid, w.Jmid, w.fro2mid);
+        mk.d2 = ev.rec(st);
+        w.post_step(w.Jmid, w.fro2mid, w.Xhat, w.Umid, w.mu, 0.0, w.postmid);
+        int* hf = reinterpret_cast<int*>(h + 32);
+        w.fetch(h, w.postmid, 8);
+        w.fetch(h + 8, w.mu, 1);
+        w.fetch(hf, w.flags, 1);
+        w.sync();
+        if (hf[0]) throw Degenerate(accelerated ? "ihoscf: eigenvector block collapsed to zero"
+                                                : "hoscf: eigenvector block collapsed to zero");
+        const double mu = h[8];
+        const double sv = h[1];
+        const double kkt_mid = h[2];
+        const double rho_mid = h[0];
+        double* xfinal = w.X;
+
+        if (!accelerated || sv <= o.tol) {
+            // hoscf step (solvers.cpp:160-178) or the iHOSCF early exit (:220-234)
+            std::swap(w.U, w.Umid);
+            std::swap(w.J, w.Jmid);
+            std::swap(w.fro2, w.fro2mid);
+            std::swap(w.post, w.postmid);
+            rec.lambda = mu;
+            rec.eq11_value = sv;
+            rec.stop_value = sv;
+            rec.kkt_max_residual = o.record_kkt ? kkt_mid : kNan;
+        } else {
+            // skip-ahead RQI refinement (solvers.cpp:236-283)
+            rec.lambda_pre_rqi = rho_mid;
+            dense_from_blocks(w.ctx, w.dims.data(), d, w.Jmid, w.S);
+            bool accepted = false;
+            double rho_y = 0.0;
+            if (rqi_step(w.ctx, n, w.S, w.Xhat, w.Yr)) {
+                split_stack(w.ctx, w.dims.data(), d, w.Yr, w.Urqi, nullptr, w.flags);
+                block_matvec(w.ctx, w.dims.data(), d, w.Jmid, w.Yr, w.Y);
+                dot_device(w.ctx, w.Yr, w.Y, static_cast<uint64_t>(n), w.dotv);
+                w.fetch(hf, w.flags, 1);
+                w.fetch(h + 9, w.dotv, 1);
+                w.sync();
+                if (!hf[0]) {
+                    rho_y = h[9];
+                    const bool improves = o.rqi_accept_rule == R1_RQI_SIGNED_INCREASE
+                                              ? rho_y > rho_mid
+                                              : std::abs(rho_y) > std::abs(rho_mid);
+                    accepted = improves;
+                }
+            }
+            rec.rqi_accepted = accepted ? 1 : 0;
+            if (accepted) {
+                std::swap(w.U, w.Urqi);
+                // xhat of the refined factors (stack_factors(u), :272)
+                split_stack(w.ctx, w.dims.data(), d, w.U, nullptr, w.XhatR, w.flags);
+                w.sweep(w.U, w.J, w.fro2);
+                rec.n_sweeps += 1;
+                w.post_step(w.J, w.fro2, w.XhatR, w.U, nullptr, rho_y, w.post);
+                w.fetch(h + 16, w.post, 8);
+                w.sync();
+                rec.lambda = rho_y;
+                rec.eq11_value = h[16 + 1];
+                rec.stop_value = rec.eq11_value;
+                rec.kkt_max_residual = o.record_kkt ? h[16 + 2] : kNan;
+                xfinal = w.Yr;
+            } else {
+                std::swap(w.U, w.Umid);
+                std::swap(w.J, w.Jmid);
+                std::swap(w.fro2, w.fro2mid);
+                std::swap(w.post, w.postmid);
+                rec.lambda = rho_mid;
+                rec.eq11_value = sv;
+                rec.stop_value = sv;
+                rec.kkt_max_residual = o.record_kkt ? kkt_mid : kNan;
+            }
+        }
+        mk.e = ev.rec(st);
+        marks.push_back(mk);
+        rr.sweeps += rec.n_sweeps - (k == 1 ? 1 : 0);
+        rr.trace.push_back(rec);
+        rr.iterations = k;
+        // final_x / warm start for the next eigen solve
+        R1_CUDA(cudaMemcpyAsync(w.Xprev, xfinal, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        have_prev = true;
+        if (rec.stop_value <= o.tol) {
+            rr.converged = true;
+            break;
+        }
+        if (o.scf_lambda_rtol > 0.0 && k > 1 &&
+            std::abs(rec.lambda - lam_prev) <= o.scf_lambda_rtol * std::abs(rec.lambda)) {
+            rr.converged = true;
+            break;
+        }
+        lam_prev = rec.lambda;
+    }
+    // finalize_sign (solvers.cpp:70-76): lambda = u_0' B(0,1)... of the final J(u)
+    w.fetch(h, w.post, 8);
+    w.sync();
+    double lam = h[4];
+    rr.factors.resize(n);
+    rr.final_x.resize(n);
+    w.fetch(rr.factors.data(), w.U, n);
+    w.fetch(rr.final_x.data(), w.Xprev, n);
+    w.sync();
+    if (lam < 0.0) {
+        lam = -lam;
+        for (uint64_t i = 0; i < w.dims[0]; ++i) rr.factors[i] = -rr.factors[i];
+    }
+    rr.lambda = lam;
+    // phase times (events)
+    for (size_t k = 0; k < marks.size(); ++k) {
+        auto& r = rr.trace[k];
+        const Marks& m = marks[k];
+        r.t_eig = Events::secs(m.a, m.b);
+        r.t_build_j = Events::secs(m.c, m.d2) + (k == 0 ? Events::secs(e0, e1) : 0.0);
+        r.t_other = Events::secs(m.b, m.c) + Events::secs(m.d2, m.e);
+    }
+    return rr;
+}
+
+std::vector<double> initial_factors(const r1_tensor* a, const r1_solve_options& o) {
+    const int d = static_cast<int>(a->dims.size());
+    if (o.init == R1_INIT_PROVIDED) {
+        if (!o.init_factors) fail(R1_ERR_INVALID_ARGUMENT, "solver: provided init has wrong order");
+        uint64_t n = 0;
+        for (auto v : a->dims) n += v;
+        std::vector<double> f(o.init_factors, o.init_factors + n);
+        uint64_t off = 0;
+        for (int k = 0; k < d; ++k) {
+            if (normalize(f.data() + off, a->dims[k]) == 0.0)
+                fail(R1_ERR_INVALID_ARGUMENT, "solver: provided init factor is zero");
+            off += a->dims[k];
+        }
+        return f;
+    }
+    return random_unit_factors(a->dims, o.seed, kStreamInit);
+}
+
+}  // namespace
+
+}  // namespace r1
+
+using namespace r1;
+
+extern "C" {
+
+int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
+             const r1_solve_options* opts, r1_solve_report* report) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        const std::string alg = algorithm ? algorithm : "";
+        if (alg == "hopm" || alg == "jacobi_hopm" || alg == "asvd" || alg == "jacobi_asvd")
+            fail(R1_ERR_INVALID_ARGUMENT, "solver " + alg + " is not on the device path");
+        if (alg != "hoscf" && alg != "ihoscf") fail(R1_ERR_INVALID_ARGUMENT, "unknown solver: " + alg);
+        if (!a || !opts || !report) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        // validate (solvers.cpp:28-32)
+        if (a->dims.size() < 2) fail(R1_ERR_INVALID_ARGUMENT, "solver: tensor order must be >= 2");
+        if (!(opts->tol > 0.0)) fail(R1_ERR_INVALID_ARGUMENT, "solver: tol must be > 0");
+        if (opts->max_iters < 1) fail(R1_ERR_INVALID_ARGUMENT, "solver: max_iters must be >= 1");
+        const bool acc = alg == "ihoscf";
+        auto t0 = std::chrono::steady_clock::now();
+        Work w(ctx, a, acc);
+        RunResult rr;
+        bool restarted = false;
+        try {
+            rr = run(w, *opts, initial_factors(a, *opts), acc);
+        } catch (const Degenerate&) {
+            try {
+                rr = run(w, *opts, random_unit_factors(a->dims, opts->seed, kStreamRestart), acc);
+                restarted = true;
+            } catch (const Degenerate& e) {
+                fail(R1_ERR_RUNTIME, std::string("solver failed after restart: ") + e.what());
+            }
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        report->lambda = rr.lambda;
+        std::memcpy(report->factors, rr.factors.data(), rr.factors.size() * sizeof(double));
+        report->converged = rr.converged ? 1 : 0;
+        report->iterations = rr.iterations;
+        report->lambda0 = rr.lambda0;
+        report->restarted = restarted ? 1 : 0;
+        if (report->final_x)
+            std::memcpy(report->final_x, rr.final_x.data(), rr.final_x.size() * sizeof(double));
+        for (int i = 0; i < rr.iterations; ++i) report->trace[i] = rr.trace[i];
+        report->total_sweeps = rr.sweeps;
+        report->t_total = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
+                         const double* x0_dev, double* value_dev, double* vec_dev) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        eig_blocks(ctx, dims, order, blocks_dev, x0_dev, value_dev, vec_dev, nullptr, nullptr);
+    });
+}
+
+// Diagnostics (not in the public header): eig on host blocks with info/stats.
+int r1x_eig_blocks_info(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                        double* value, double* vec, int* info, double* stats) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        const uint64_t nb = blocks_numel(dims, order);
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        DeviceBuffer b, v;
+        b.ensure(nb * sizeof(double));
+        v.ensure((n + 8) * sizeof(double));
+        R1_CUDA(cudaMemcpyAsync(b.ptr, blocks_host, nb * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        eig_blocks(ctx, dims, order, b.as<double>(), nullptr, v.as<double>() + n,
+                   v.as<double>(), info, stats);
+        R1_CUDA(cudaMemcpyAsync(vec, v.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(value, v.as<double>() + n, sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_host, double* value,
+                                   double* vec) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (n <= 0) fail(R1_ERR_INVALID_ARGUMENT, "largest_magnitude_eigenpair: empty matrix");
+        // check_symmetric (sym_eig.cpp:13-22)
+        double scale = 0.0, dev = 0.0;
+        for (int64_t i = 0; i < n * n; ++i) scale = std::max(scale, std::abs(s_host[i]));
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = j + 1; i < n; ++i)
+                dev = std::max(dev, std::abs(s_host[i + j * n] - s_host[j + i * n]));
+        if (dev > 1e-10 * std::max(scale, 1e-300))
+            fail(R1_ERR_INVALID_ARGUMENT, "sym_eig: matrix is not symmetric");
+        DeviceBuffer S, v;
+        S.ensure(static_cast<size_t>(n) * n * sizeof(double));
+        v.ensure((n + 8) * sizeof(double));
+        R1_CUDA(cudaMemcpyAsync(S.ptr, s_host, static_cast<size_t>(n) * n * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        int info[5];
+        eig_dense(ctx, n, S.as<double>(), nullptr, v.as<double>() + n, v.as<double>(), info, nullptr);
+        if (!info[0]) fail(R1_ERR_RUNTIME, "sym_eig: Lanczos iteration did not converge");
+        R1_CUDA(cudaMemcpyAsync(vec, v.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(value, v.as<double>() + n, sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host, const double* x_host,
+                              double* y_host, int* accepted) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (n <= 0) fail(R1_ERR_INVALID_ARGUMENT, "rayleigh_quotient_step: size mismatch");
+        DeviceBuffer S, v;
+        S.ensure(static_cast<size_t>(n) * n * sizeof(double));
+        v.ensure(2 * n * sizeof(double));
+        R1_CUDA(cudaMemcpyAsync(S.ptr, s_host, static_cast<size_t>(n) * n * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(v.ptr, x_host, n * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        const bool ok = rqi_step(ctx, n, S.as<double>(), v.as<double>(), v.as<double>() + n);
+        *accepted = ok ? 1 : 0;
+        if (ok) {
+            R1_CUDA(cudaMemcpyAsync(y_host, v.as<double>() + n, n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+}
+
+int r1_scf_stopping_value(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                          const double* x_host, double lambda, double* out) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        const uint64_t nb = blocks_numel(dims, order);
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        DeviceBuffer b, v;
+        b.ensure(nb * sizeof(double));
+        v.ensure((3 * n + 80) * sizeof(double));
+        double* x = v.as<double>();
+        double* y = x + n;
+        double* f2 = y + n;
+        double* out_d = f2 + 8;
+        R1_CUDA(cudaMemcpyAsync(b.ptr, blocks_host, nb * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(x, x_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        sumsq_device(ctx, b.as<double>(), nb, f2);
+        block_matvec(ctx, dims, order, b.as<double>(), x, y);
+        // the u argument only feeds the KKT outputs, which are ignored here
+        post_step(ctx, dims, order, y, x, x, f2, nullptr, lambda, out_d);
+        double h[8];
+        R1_CUDA(cudaMemcpyAsync(h, out_d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = h[1];
+    });
+}
+
+// out: [lambda, max_residual, r_0..r_{d-1}]
+int r1_kkt_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                       const double* factors_host, double* out) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        const uint64_t nb = blocks_numel(dims, order);
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        DeviceBuffer b, v;
+        b.ensure(nb * sizeof(double));
+        v.ensure((4 * n + 80) * sizeof(double));
+        double* u = v.as<double>();
+        double* xh = u + n;
+        double* y = xh + n;
+        double* f2 = y + n;
+        double* out_d = f2 + 8;
+        R1_CUDA(cudaMemcpyAsync(b.ptr, blocks_host, nb * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        {
+            // check_unit_nonzero (nepv.cpp:31-41) as kkt_report does
+            uint64_t off = 0;
+            for (int k = 0; k < order; ++k) {
+                double s = 0.0;
+                for (uint64_t i = 0; i < dims[k]; ++i) s += factors_host[off + i] * factors_host[off + i];
+                const double nrm = std::sqrt(s);
+                if (nrm < 1e-12)
+                    fail(R1_ERR_RUNTIME, "degenerate factor set: zero factor for mode " + std::to_string(k));
+                if (std::abs(nrm - 1.0) > 1e-8)
+                    fail(R1_ERR_INVALID_ARGUMENT, "factor for mode " + std::to_string(k) + " is not unit length");
+                off += dims[k];
+            }
+        }
+        R1_CUDA(cudaMemcpyAsync(u, factors_host, n * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        split_stack(ctx, dims, order, u, nullptr, xh, nullptr);
+        sumsq_device(ctx, b.as<double>(), nb, f2);
+        block_matvec(ctx, dims, order, b.as<double>(), xh, y);
+        post_step(ctx, dims, order, y, xh, u, f2, nullptr, 0.0, out_d);
+        std::vector<double> h(5 + order);
+        R1_CUDA(cudaMemcpyAsync(h.data(), out_d, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        out[0] = h[4];
+        out[1] = h[2];
+        for (int k = 0; k < order; ++k) out[2 + k] = h[5 + k];
+    });
+}
+
+int r1_kkt_report(r1_context* ctx, const double* a_host, const r1_tensor* a_dev, const uint64_t* dims,
+                  int order, const double* factors_host, double* out) {
+    return abi_guard([&] {
+        if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
+        const uint64_t nb = blocks_numel(dims, order);
+        std::vector<double> blocks(nb);
+        int rc = r1_build_j(ctx, a_host, a_dev, dims, order, factors_host, blocks.data());
+        if (rc != R1_OK) fail(rc, r1_last_error());
+        rc = r1_kkt_from_blocks(ctx, dims, order, blocks.data(), factors_host, out);
+        if (rc != R1_OK) fail(rc, r1_last_error());
+    });
+}
+
+}  // extern "C"

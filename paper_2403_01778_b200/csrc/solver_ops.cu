@@ -1,0 +1,366 @@
+// Per-iteration device steps of HOSCF / iHOSCF around the sweep and the
+// eigen solve (reference proj/src/solvers.cpp:129-297):
+//
+//   split_stack   split_factors + stack_factors (stacked.cpp:40-73) fused:
+//                 u_n = x_n/||x_n|| (degenerate if < 1e-12), xhat = u/sqrt(d)
+//   post          ONE block matvec y = J(u) xhat feeds everything the
+//                 reference computes with extra tensor passes:
+//                   rho = xhat'y (= lambda, the full contraction),
+//                   Eq. 11 = ||y - rho xhat|| / (||J||_F + |mu|)   (nepv.cpp:271-282)
+//                   w_n = sqrt(d) y_n = A x_{-n} u  (contract_leaving_all),
+//                   lambda = u_0'w_0, KKT residual_n = ||w_n - lambda u_n||
+//                   (kkt_report, nepv.cpp:249-269)
+//   dense         SymBlockMatrix::dense (nepv.cpp:136-150) for the RQI solve
+//   rqi           rayleigh_quotient_step (sym_eig.cpp:411-438): Bunch-Kaufman
+//                 LDL^T (cuSOLVER dsytrf, LAPACK's BK with alpha=(1+sqrt17)/8,
+//                 the same algorithm family as sym_eig.cpp:233-320), the
+//                 reference's D-block condition test (>1e14 -> reject,
+//                 :381-407, :424) and one shift bump (:434-437).
+#include "common.cuh"
+#include "blockmv.cuh"
+#include "solver_ops.cuh"
+
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <vector>
+
+namespace r1 {
+
+namespace {
+
+constexpr int kOpsThreads = 512;
+
+__device__ double block_reduce_sum(double v, double* sh) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) s += sh[k];
+    return s;
+}
+
+struct Dims {
+    int d;
+    int64_t offs[17];
+};
+
+// Single CTA: per-block norms of x, normalise, stack.
+__global__ void split_stack_kernel(Dims dm, const double* __restrict__ x, double* __restrict__ u,
+                                   double* __restrict__ xhat, int* __restrict__ flags) {
+    __shared__ double sh[32];
+    const double inv_sqrt_d = 1.0 / sqrt(static_cast<double>(dm.d));
+    int deg = 0;
+    for (int k = 0; k < dm.d; ++k) {
+        const int64_t o = dm.offs[k], len = dm.offs[k + 1] - dm.offs[k];
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) s = fma(x[o + i], x[o + i], s);
+        const double nrm = sqrt(block_reduce_sum(s, sh));
+        const bool dk = nrm < 1e-12;
+        deg |= dk ? 1 : 0;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const double v = dk ? 0.0 : x[o + i] / nrm;
+            if (u) u[o + i] = v;
+            if (xhat) xhat[o + i] = v * inv_sqrt_d;
+        }
+    }
+    if (threadIdx.x == 0 && flags) flags[0] = deg;
+}
+
+// Single CTA after y = J(u) xhat.
+//   out[0] rho (= lambda), out[1] eq11, out[2] kkt max residual,
+//   out[3] ||J||_F, out[4] lambda = u_0'w_0, out[5..5+d) residual_n
+__global__ void post_kernel(Dims dm, const double* __restrict__ y, const double* __restrict__ xhat,
+                            const double* __restrict__ u, const double* __restrict__ fro2,
+                            const double* __restrict__ mu_dev, double mu_host, int use_mu_dev,
+                            double* __restrict__ out) {
+    __shared__ double sh[32];
+    const int64_t n = dm.offs[dm.d];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(xhat[i], y[i], s);
+    const double rho = block_reduce_sum(s, sh);
+    s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double r = y[i] - rho * xhat[i];
+        s = fma(r, r, s);
+    }
+    const double res = sqrt(block_reduce_sum(s, sh));
+    const double fro = sqrt(2.0 * fro2[0]) / static_cast<double>(dm.d - 1);
+    const double mu = use_mu_dev ? mu_dev[0] : mu_host;
+    const double sqd = sqrt(static_cast<double>(dm.d));
+    // lambda = u_0' w_0
+    s = 0.0;
+    for (int64_t i = threadIdx.x; i < dm.offs[1]; i += blockDim.x) s = fma(u[i], sqd * y[i], s);
+    const double lam = block_reduce_sum(s, sh);
+    double mx = 0.0;
+    for (int k = 0; k < dm.d; ++k) {
+        s = 0.0;
+        for (int64_t i = dm.offs[k] + threadIdx.x; i < dm.offs[k + 1]; i += blockDim.x) {
+            const double r = sqd * y[i] - lam * u[i];
+            s = fma(r, r, s);
+        }
+        const double rk = sqrt(block_reduce_sum(s, sh));
+        if (threadIdx.x == 0) out[5 + k] = rk;
+        mx = fmax(mx, rk);
+    }
+    if (threadIdx.x == 0) {
+        out[0] = rho;
+        out[1] = res / (fro + fabs(mu));
+        out[2] = mx;
+        out[3] = fro;
+        out[4] = lam;
+    }
+}
+
+__global__ void dense_kernel(const BlockOp* __restrict__ opp, double* __restrict__ S) {
+    const BlockOp& op = *opp;
+    const int64_t n = op.n;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e % n, c = e / n;
+        int mr = 0, mc = 0;
+        while (r >= op.offs[mr + 1]) ++mr;
+        while (c >= op.offs[mc + 1]) ++mc;
+        double v = 0.0;
+        if (mr < mc) {
+            const int p = pair_index(mr, mc, op.d);
+            v = op.blocks[op.boff[p] + (r - op.offs[mr]) + (c - op.offs[mc]) * op.dims[mr]];
+        } else if (mr > mc) {
+            const int p = pair_index(mc, mr, op.d);
+            v = op.blocks[op.boff[p] + (c - op.offs[mc]) + (r - op.offs[mr]) * op.dims[mc]];
+        }
+        S[e] = v * op.scale;
+    }
+}
+
+__global__ void flip_kernel(double* v, int64_t n, const double* lam_in, double* lam_out) {
+    const double lam = lam_in[0];
+    if (lam < 0.0)
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            v[i] = -v[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) lam_out[0] = fabs(lam);
+}
+
+// ---- RQI helpers --------------------------------------------------------
+__global__ void shift_copy_kernel(const double* __restrict__ S, double* __restrict__ W, int64_t n,
+                                  const double* __restrict__ shift) {
+    const double sh = shift[0];
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e % n, c = e / n;
+        W[e] = S[e] - (r == c ? sh : 0.0);
+    }
+}
+
+// (Sx)_i, thread per row (column-major S: coalesced across threads).
+__global__ void dense_matvec_kernel(const double* __restrict__ S, const double* __restrict__ x,
+                                    int64_t n, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int64_t j = 0; j < n; ++j) s = fma(S[i + j * n], x[j], s);
+        y[i] = s;
+    }
+}
+
+// shifts[1] = bumped shift (sym_eig.cpp:435-436) from rho = shifts[0].
+__global__ void bump_kernel(double* __restrict__ shifts, const double* __restrict__ fro2) {
+    const double rho = shifts[0];
+    shifts[1] = rho != 0.0 ? rho * (1.0 + 1e-10) : 1e-10 * fmax(sqrt(fro2[0]), 1e-300);
+}
+
+// max|eig(D)| / min|eig(D)| over LAPACK-format BK pivot blocks (lower):
+// ipiv[k] > 0: 1x1; ipiv[k] = ipiv[k+1] < 0: 2x2 at (k,k),(k+1,k),(k+1,k+1).
+__global__ void diag_condition_kernel(const double* __restrict__ W, const int* __restrict__ ipiv,
+                                      int64_t n, const int* __restrict__ info,
+                                      double* __restrict__ cond) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (info[0] != 0) {
+        cond[0] = INFINITY;
+        return;
+    }
+    double lo = INFINITY, hi = 0.0;
+    int64_t k = 0;
+    while (k < n) {
+        if (ipiv[k] > 0) {
+            const double m = fabs(W[k + k * n]);
+            lo = fmin(lo, m);
+            hi = fmax(hi, m);
+            ++k;
+        } else {
+            const double a = W[k + k * n], c = W[(k + 1) + (k + 1) * n], bb = W[(k + 1) + k * n];
+            const double mid = 0.5 * (a + c);
+            const double rad = hypot(0.5 * (a - c), bb);
+            const double e1 = fabs(mid + rad), e2 = fabs(mid - rad);
+            lo = fmin(lo, fmin(e1, e2));
+            hi = fmax(hi, fmax(e1, e2));
+            k += 2;
+        }
+    }
+    cond[0] = lo == 0.0 ? INFINITY : hi / lo;
+}
+
+__global__ void ipiv64_kernel(const int* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = in[i];
+}
+
+__global__ void normalize_check_kernel(double* __restrict__ y, int64_t n, int* __restrict__ ok) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(y[i], y[i], s);
+    const double nrm = sqrt(block_reduce_sum(s, sh));
+    const bool good = isfinite(nrm) && nrm != 0.0;
+    if (good)
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] /= nrm;
+    if (threadIdx.x == 0) ok[0] = good ? 1 : 0;
+}
+
+Dims make_dims(const uint64_t* dims, int order) {
+    Dims dm{};
+    dm.d = order;
+    dm.offs[0] = 0;
+    for (int k = 0; k < order; ++k) dm.offs[k + 1] = dm.offs[k] + static_cast<int64_t>(dims[k]);
+    return dm;
+}
+
+struct SolverHandle {
+    cusolverDnHandle_t h = nullptr;
+    ~SolverHandle() {
+        if (h) cusolverDnDestroy(h);
+    }
+};
+
+std::map<r1_context*, std::shared_ptr<SolverHandle>>& solver_handles() {
+    static std::map<r1_context*, std::shared_ptr<SolverHandle>> m;
+    return m;
+}
+
+cusolverDnHandle_t solver_handle(r1_context* ctx) {
+    auto& H = solver_handles()[ctx];
+    if (!H) {
+        H = std::make_shared<SolverHandle>();
+        if (cusolverDnCreate(&H->h) != CUSOLVER_STATUS_SUCCESS)
+            fail(R1_ERR_CUDA, "cusolverDnCreate failed");
+    }
+    if (cusolverDnSetStream(H->h, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
+        fail(R1_ERR_CUDA, "cusolverDnSetStream failed");
+    return H->h;
+}
+
+}  // namespace
+
+void forget_solver_handles(r1_context* ctx) { solver_handles().erase(ctx); }
+
+void split_stack(r1_context* ctx, const uint64_t* dims, int order, const double* x, double* u,
+                 double* xhat, int* flags_dev) {
+    split_stack_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(make_dims(dims, order), x, u, xhat,
+                                                          flags_dev);
+    check_launch(ctx, "split_stack_kernel");
+}
+
+void post_step(r1_context* ctx, const uint64_t* dims, int order, const double* y,
+               const double* xhat, const double* u, const double* fro2_dev, const double* mu_dev,
+               double mu_host, double* out_dev) {
+    post_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(make_dims(dims, order), y, xhat, u, fro2_dev,
+                                                   mu_dev, mu_host, mu_dev ? 1 : 0, out_dev);
+    check_launch(ctx, "post_kernel");
+}
+
+void flip_first(r1_context* ctx, double* u0, int64_t n0, const double* lam_in, double* lam_out) {
+    flip_kernel<<<1, 256, 0, ctx->stream>>>(u0, n0, lam_in, lam_out);
+    check_launch(ctx, "flip_kernel");
+}
+
+void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
+                       double* S) {
+    BlockOp op;
+    int64_t cn, rn;
+    blockop_layout(op, dims, order, &cn, &rn);
+    op.blocks = blocks;
+    DeviceBuffer dop;
+    dop.ensure(sizeof(BlockOp));
+    R1_CUDA(cudaMemcpyAsync(dop.ptr, &op, sizeof(BlockOp), cudaMemcpyHostToDevice, ctx->stream));
+    const int64_t nn = op.n * op.n;
+    const int g = static_cast<int>(std::min<int64_t>((nn + 255) / 256, ctx->num_sms * 16));
+    dense_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(dop.as<BlockOp>(), S);
+    check_launch(ctx, "dense_kernel");
+    R1_CUDA(cudaStreamSynchronize(ctx->stream));  // dop is freed on return
+}
+
+// One RQI step on the dense symmetric S (device, n x n, column-major) and x
+// (device).  Returns true and y (device, unit) when accepted, false for
+// std::nullopt.  Synchronous (the accept decision is a host branch).
+bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, double* y) {
+    cusolverDnHandle_t h = solver_handle(ctx);
+    const size_t nn = static_cast<size_t>(n) * n;
+    ctx->ws_rqi.ensure((nn + 4 * n + 128) * sizeof(double));
+    double* W = ctx->ws_rqi.as<double>();
+    double* scal = W + nn;  // [0] rho, [1] bumped, [2] cond, [3] fro(S)^2 ...
+    int* ipiv = reinterpret_cast<int*>(scal + 16);
+    int* info = ipiv + n + 8;
+    int lwork = 0;
+    if (cusolverDnDsytrf_bufferSize(h, static_cast<int>(n), W, static_cast<int>(n), &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+        fail(R1_ERR_CUDA, "cusolverDnDsytrf_bufferSize failed");
+    DeviceBuffer work, ipiv64;
+    work.ensure(std::max<size_t>(1, static_cast<size_t>(lwork)) * sizeof(double));
+    ipiv64.ensure(std::max<int64_t>(n, 1) * sizeof(int64_t));
+    // rho = x'Sx (sym_eig.cpp:417-418); ||S||_F only matters when rho == 0
+    double* sx = scal + 16 + (n + 16) / 2 + 8;  // after ipiv/info (ints)
+    dense_matvec_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms))),
+                          256, 0, ctx->stream>>>(S, x, n, sx);
+    check_launch(ctx, "dense_matvec_kernel");
+    dot_device(ctx, x, sx, static_cast<uint64_t>(n), scal);
+    sumsq_device(ctx, S, nn, scal + 3);
+    bump_kernel<<<1, 1, 0, ctx->stream>>>(scal, scal + 3);
+    check_launch(ctx, "bump_kernel");
+    const int g = static_cast<int>(std::min<size_t>((nn + 255) / 256, ctx->num_sms * 16));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        shift_copy_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(S, W, n, scal + attempt);
+        check_launch(ctx, "shift_copy_kernel");
+        if (cusolverDnDsytrf(h, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), W, static_cast<int>(n),
+                             ipiv, work.as<double>(), lwork, info) != CUSOLVER_STATUS_SUCCESS)
+            fail(R1_ERR_CUDA, "cusolverDnDsytrf failed");
+        count_launch(ctx);
+        diag_condition_kernel<<<1, 32, 0, ctx->stream>>>(W, ipiv, n, info, scal + 2);
+        check_launch(ctx, "diag_condition_kernel");
+        double cond = 0.0;
+        R1_CUDA(cudaMemcpyAsync(&cond, scal + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (!(cond <= 1e14)) continue;  // singular or ill-conditioned shift
+        R1_CUDA(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        ipiv64_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 64))), 256, 0,
+                        ctx->stream>>>(ipiv, ipiv64.as<int64_t>(), n);
+        check_launch(ctx, "ipiv64_kernel");
+        size_t dws = 0, hws = 0;
+        if (cusolverDnXsytrs_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, W, n,
+                                        ipiv64.as<int64_t>(), CUDA_R_64F, y, n, &dws, &hws) !=
+            CUSOLVER_STATUS_SUCCESS)
+            fail(R1_ERR_CUDA, "cusolverDnXsytrs_bufferSize failed");
+        DeviceBuffer dwork;
+        dwork.ensure(std::max<size_t>(dws, 16));
+        std::vector<char> hwork(std::max<size_t>(hws, 16));
+        if (cusolverDnXsytrs(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, W, n, ipiv64.as<int64_t>(),
+                             CUDA_R_64F, y, n, dwork.ptr, dws, hwork.data(), hws, info) !=
+            CUSOLVER_STATUS_SUCCESS)
+            fail(R1_ERR_CUDA, "cusolverDnXsytrs failed");
+        count_launch(ctx);
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));  // dwork / hwork lifetime
+        normalize_check_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(y, n, info + 1);
+        check_launch(ctx, "normalize_check_kernel");
+        int ok = 0;
+        R1_CUDA(cudaMemcpyAsync(&ok, info + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ok) return true;
+    }
+    return false;
+}
+
+}  // namespace r1
