@@ -201,6 +201,16 @@ int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_h
 int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host,
                               const double* x_host, double* y_host, int* accepted);
 
+/* ---- synthetic inputs ----------------------------------------------------------- */
+/* Fill `t` with elements [first, first + numel(t)) of BASELINE config `cfg`
+ * (1..5, definitions in DESIGN.md §6) whose global reference dims are
+ * `global_dims`; a contiguous slab along the last (slowest) mode is a tensor of
+ * the global dims with a shorter last extent.  Counter-based: any rank can
+ * generate its own slab.  (Not in the reference API: generators.cpp is out of
+ * scope; this exists so benchmarks never stage 8-32 GB through the host.) */
+int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
+                       const uint64_t* global_dims, int order, uint64_t first);
+
 /* ---- solvers (solvers.hpp:63-88) -------------------------------------------- */
 /* algorithm: "hoscf" | "ihoscf".  Other reference names are rejected with
  * R1_ERR_INVALID_ARGUMENT ("unknown solver" for unknown names, "not on the

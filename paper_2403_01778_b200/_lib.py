@@ -97,6 +97,8 @@ SIGNATURES = {
     "r1_largest_magnitude_eigenpair": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp]),
     "r1_rayleigh_quotient_step": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp,
                                                  ctypes.POINTER(ctypes.c_int)]),
+    "r1_generate_config": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_uint64, _u64p,
+                                          ctypes.c_int, ctypes.c_uint64]),
     "r1_solve": (ctypes.c_int, [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(SolveOptionsC),
                                 ctypes.POINTER(SolveReportC)]),
 }
@@ -104,6 +106,9 @@ SIGNATURES = {
 # Diagnostics not in the public header (tests / bench only).
 EXTRA_SIGNATURES = {
     "r1x_set_sweep_trace": (ctypes.c_int, [_vp, _vp]),
+    "r1x_time_kernels": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "r1x_kernel_time": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_uint64)]),
     "r1x_eig_blocks_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp, _dp,
                                            ctypes.POINTER(ctypes.c_int), _dp]),
     "r1x_sweep_plan_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int,

@@ -342,6 +342,34 @@ int r1x_set_sweep_trace(r1_context* ctx, void* dev) {
     });
 }
 
+// Diagnostics (not in the public header): enable CUDA-event timing of the
+// top-level sweep kernel; r1x_kernel_time syncs and returns the summed
+// milliseconds and the number of timed launches since the last query.
+int r1x_time_kernels(r1_context* ctx, int enable) {
+    return abi_guard([&] {
+        bind(ctx);
+        ctx->time_kernels = enable != 0;
+    });
+}
+
+int r1x_kernel_time(r1_context* ctx, double* ms, uint64_t* launches) {
+    return abi_guard([&] {
+        bind(ctx);
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        double total = 0.0;
+        for (auto& pr : ctx->kernel_events) {
+            float t = 0.f;
+            R1_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+            total += t;
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        *ms = total;
+        *launches = ctx->kernel_events.size();
+        ctx->kernel_events.clear();
+    });
+}
+
 // Test/diagnostic hook (not in the public header): the top-level sweep plan.
 int r1x_sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* info) {
     return abi_guard([&] {

@@ -125,6 +125,9 @@ struct r1_context {
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
     unsigned long long* dbg_sweep_trace = nullptr;  // diagnostics: per-CTA timing of level 0
+    // diagnostics: CUDA events around every top-level sweep kernel launch
+    bool time_kernels = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;
     // Workspace arena, grow-only: sweeps, eigen solver, RQI.
     r1::DeviceBuffer ws_sweep;
     r1::DeviceBuffer ws_eig;

@@ -73,6 +73,7 @@ struct SweepArgs {
     int64_t P1_stride;
     unsigned long long* trace;  // optional: per CTA {t_start, t_end, smid}
     int debug_mode;             // diagnostics: 1 = consumers only wait/release
+    int trace_level0;           // host-side flag: this launch is the top-level sweep
 };
 
 // ------------------------------------------------------------- PTX helpers --
@@ -960,8 +961,19 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
     maps.m[1] = make_map(a.A, L, rem0, L.t1);
     maps.m[2] = make_map(a.A, L, L.r0, rem1);
     maps.m[3] = make_map(a.A, L, rem0, rem1);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const bool timed = ctx->time_kernels && a.trace_level0;
+    if (timed) {
+        R1_CUDA(cudaEventCreate(&e0));
+        R1_CUDA(cudaEventCreate(&e1));
+        R1_CUDA(cudaEventRecord(e0, ctx->stream));
+    }
     kern<<<L.ncta, (kBoxNWC + 1) * 32, L.smem, ctx->stream>>>(a, maps, L.stages, L.stage_dbl);
     check_launch(ctx, "sweep3_box_kernel");
+    if (timed) {
+        R1_CUDA(cudaEventRecord(e1, ctx->stream));
+        ctx->kernel_events.emplace_back(e0, e1);
+    }
 }
 
 template <int NRA, int NCB, int STAGES>
@@ -1050,6 +1062,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.P1 = L.out_c1.where == Where::None ? nullptr : resolve(L.p1);
         s.P1_stride = L.I1 * L.O;
         s.trace = (&L == &P->levels.front()) ? ctx->dbg_sweep_trace : nullptr;
+        s.trace_level0 = (&L == &P->levels.front()) ? 1 : 0;
         {
             static const char* dm = std::getenv("R1_DEBUG_SWEEP_MODE");
             s.debug_mode = dm ? std::atoi(dm) : 0;
