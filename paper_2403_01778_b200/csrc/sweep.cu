@@ -715,7 +715,11 @@ void tile_level(Level& L, int num_sms) {
         const int rm = 32 * L.nra, cm = kBoxNWC * kBoxNCB;
         L.G0 = static_cast<int>((L.I0 + rm - 1) / rm);
         L.r0 = static_cast<int>((L.I0 + L.G0 - 1) / L.G0);
-        L.r0 += L.r0 & 1;  // 16-B box rows
+        // Whole 32-B sectors per tile row when the column pitch allows (else
+        // 16-B, the TMA minimum): neighbouring row tiles never share a DRAM
+        // sector, which would otherwise be fetched twice.
+        const int q = (L.I0 % 4 == 0) ? 4 : 2;
+        L.r0 = std::min(rm, (L.r0 + q - 1) / q * q);
         L.G0 = static_cast<int>((L.I0 + L.r0 - 1) / L.r0);
         L.G1 = static_cast<int>((L.I1 + cm - 1) / cm);
         L.t1 = static_cast<int>((L.I1 + L.G1 - 1) / L.G1);

@@ -67,12 +67,20 @@ def test_rqi_step_matches_reference(gpu_ctx, oracle, ref):
     if yr is not None:
         sgn = 1.0 if np.dot(y, yr) > 0 else -1.0
         assert np.max(np.abs(sgn * y - yr)) <= 1e-8
-    # 2x2 hand case (test_sym_eig.cpp:191-202): S = [[0,1],[1,0]], x = e1
-    y2 = r1.rayleigh_quotient_step(np.array([[0.0, 1.0], [1.0, 0.0]]), np.array([1.0, 0.0]))
-    y2r = ref.rayleigh_quotient_step(np.array([[0.0, 1.0], [1.0, 0.0]]), np.array([1.0, 0.0]))
-    assert (y2 is None) == (y2r is None)
-    if y2r is not None:
-        assert np.max(np.abs(np.abs(y2) - np.abs(y2r))) <= 1e-12
+    # 2x2 hand case (test_sym_eig.cpp:191-202): S = diag(2,1), x = (1,1)/sqrt2 -> (1,-1)/sqrt2
+    r = 1.0 / np.sqrt(2.0)
+    y2 = r1.rayleigh_quotient_step(np.diag([2.0, 1.0]), np.array([r, r]))
+    assert y2 is not None
+    assert abs(y2[0] - r) <= 1e-12 * r and abs(y2[1] + r) <= 1e-12 * r
+
+
+def test_eig_kats(gpu_ctx):
+    """test_sym_eig.cpp:103-111, 134-141 on the device eigen path."""
+    import paper_2403_01778_b200 as r1
+    p = r1.largest_magnitude_eigenpair(np.diag([-5.0, 3.0]))
+    assert abs(p.value + 5.0) <= 1e-14 and abs(abs(p.vector[0]) - 1.0) <= 1e-14 and p.vector[0] > 0
+    p = r1.largest_magnitude_eigenpair(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert abs(p.value - 1.0) <= 1e-14 and p.value > 0
 
 
 def test_eq11_and_kkt_match_reference(gpu_ctx, oracle, ref):

@@ -6,6 +6,8 @@ import time
 import numpy as np
 import torch
 
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2403_01778_b200 as r1
 from paper_2403_01778_b200 import _lib
 
