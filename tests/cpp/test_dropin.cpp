@@ -1,0 +1,155 @@
+// C++ drop-in check: code written against the reference's rank1:: API
+// (proj/include/rank1) compiles unchanged against include/rank1/*.hpp and runs
+// on the B200 library; results are compared with the compiled reference
+// (oracle/_ref/librank1_ref.so, through its C shim) on the same inputs.
+// Modelled on the reference's own tests (test_nepv.cpp, test_solvers.cpp).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <vector>
+
+#include "rank1/nepv.hpp"
+#include "rank1/solvers.hpp"
+#include "rank1/stacked.hpp"
+#include "rank1/sym_eig.hpp"
+#include "rank1_b200.h"
+
+extern "C" {
+int ref_build_j(const double*, const uint64_t*, int, const double*, int, int, int, int, double*, double*);
+int ref_solve(const char*, const double*, const uint64_t*, int, const r1_solve_options*, r1_solve_report*);
+int ref_rng_draws(uint64_t, uint64_t, int, int64_t, double*);
+}
+
+using namespace rank1;
+
+static int failures = 0;
+#define CHECK(c)                                                            \
+    do {                                                                    \
+        if (!(c)) {                                                         \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                     \
+        }                                                                   \
+    } while (0)
+
+static DenseTensor gaussian(const std::vector<std::size_t>& dims, uint64_t seed) {
+    std::size_t n = 1;
+    for (auto d : dims) n *= d;
+    std::vector<double> v(n);
+    ref_rng_draws(seed, 77, 2, static_cast<int64_t>(n), v.data());  // tests/oracles.hpp:114-120
+    return DenseTensor(dims, v);
+}
+
+static FactorSet unit_factors(const std::vector<std::size_t>& dims, uint64_t seed) {
+    FactorSet f;
+    for (std::size_t k = 0; k < dims.size(); ++k) {
+        std::vector<double> u(dims[k]);
+        ref_rng_draws(seed * 131 + k, 78, 2, static_cast<int64_t>(u.size()), u.data());
+        normalize(u);
+        f.factors.push_back(u);
+    }
+    return f;
+}
+
+int main() {
+    // build_j vs the reference, several orders
+    for (auto dims : {std::vector<std::size_t>{7, 5, 9}, std::vector<std::size_t>{6, 5, 4, 3},
+                      std::vector<std::size_t>{4, 3, 5, 2, 3}, std::vector<std::size_t>{3, 4}}) {
+        DenseTensor a = gaussian(dims, 11);
+        FactorSet f = unit_factors(dims, 12);
+        SymBlockMatrix j = build_j(a, f);
+        std::vector<uint64_t> d(dims.begin(), dims.end());
+        std::vector<double> flat;
+        for (auto& u : f.factors) flat.insert(flat.end(), u.begin(), u.end());
+        std::size_t nb = 0;
+        for (std::size_t m = 0; m < dims.size(); ++m)
+            for (std::size_t n = m + 1; n < dims.size(); ++n) nb += dims[m] * dims[n];
+        std::vector<double> want(nb);
+        ref_build_j(a.data(), d.data(), static_cast<int>(d.size()), flat.data(), 1, 0, 1, 0,
+                    want.data(), nullptr);
+        std::size_t off = 0;
+        double worst = 0.0;
+        for (std::size_t m = 0; m < dims.size(); ++m)
+            for (std::size_t n = m + 1; n < dims.size(); ++n)
+                for (double v : j.block(m, n).values()) {
+                    worst = std::max(worst, std::abs(v - want[off]));
+                    ++off;
+                }
+        CHECK(worst <= 1e-12);
+        // Rayleigh identity x'J(x)x = multilinear value (test_nepv.cpp:157-168)
+        StackedVector x = stack_factors(f);
+        double rho = dot(x.flat(), j.matvec(x.flat()));
+        CHECK(std::abs(rho - multilinear_value(a, f)) <= 1e-10 * std::max(1.0, std::abs(rho)));
+        CHECK(std::abs(j.frobenius_norm() - frobenius_norm(j.dense())) <= 1e-12 * j.frobenius_norm());
+    }
+    // all-ones 2x2x2 KAT (test_nepv.cpp:126-137)
+    {
+        DenseTensor a({2, 2, 2}, std::vector<double>(8, 1.0));
+        const double s = 1.0 / std::sqrt(2.0);
+        FactorSet f;
+        f.factors = {{s, s}, {s, s}, {s, s}};
+        SymBlockMatrix j = build_j(a, f);
+        CHECK(j.scale() == 0.5);
+        for (std::size_t m = 0; m < 3; ++m)
+            for (std::size_t n = m + 1; n < 3; ++n)
+                for (double v : j.block(m, n).values()) CHECK(std::abs(v - std::sqrt(2.0)) <= 1e-12);
+    }
+    // error mapping (test_nepv.cpp:104-107, 227-232)
+    {
+        DenseTensor a = gaussian({3, 3, 3}, 20);
+        FactorSet f = unit_factors({3, 3, 3}, 21);
+        bool threw = false;
+        try {
+            build_block(a, f, 1, 1);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        std::fill(f.factors[2].begin(), f.factors[2].end(), 0.0);
+        threw = false;
+        try {
+            build_j(a, f);
+        } catch (const std::runtime_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // hoscf / ihoscf vs the reference (tolerances of the north star)
+    for (const char* alg : {"hoscf", "ihoscf"}) {
+        std::vector<std::size_t> dims{7, 5, 9};
+        DenseTensor a = gaussian(dims, 11);
+        SolveOptions o;
+        o.tol = 1e-10;
+        o.seed = 1;
+        SolveReport rep = solve(alg, a, o);
+        r1_solve_options ro;
+        r1_solve_options_default(&ro);
+        ro.tol = 1e-10;
+        ro.seed = 1;
+        std::vector<double> fac(21), fx(21);
+        std::vector<r1_iteration_record> tr(500);
+        r1_solve_report rr{};
+        rr.factors = fac.data();
+        rr.final_x = fx.data();
+        rr.trace = tr.data();
+        std::vector<uint64_t> d(dims.begin(), dims.end());
+        ref_solve(alg, a.data(), d.data(), 3, &ro, &rr);
+        CHECK(rep.converged == (rr.converged != 0));
+        CHECK(std::abs(rep.iterations - rr.iterations) <= 1);
+        CHECK(std::abs(rep.result.lambda - rr.lambda) <= 1e-10 * rr.lambda);
+        CHECK(rep.result.lambda >= 0.0);
+        CHECK(static_cast<int>(rep.trace.size()) == rep.iterations);
+    }
+    // baselines are not on the device path
+    {
+        bool threw = false;
+        try {
+            solve("hopm", gaussian({3, 3}, 1), SolveOptions{});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    std::printf("test_dropin: %s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
+    return failures ? 1 : 0;
+}
