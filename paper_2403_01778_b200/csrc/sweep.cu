@@ -45,6 +45,8 @@ constexpr int kMaxOrder = 16;
 constexpr int kBoxNWC = 15;  // consumer warps of the TMA box kernel (+1 producer = 16 warps)
 constexpr int kBoxNCB = 4;   // columns per consumer warp (box = 32*NRA x 60)
 constexpr int kMaxStages = 16;          // mbarrier slots of the box kernel ring
+constexpr double kDynFrac = 0.25;       // share of the work scheduled dynamically
+constexpr double kDynMinChunk = 8.0;    // guided chunks: remaining/(2*ncta), >= 8 panels
 constexpr size_t kSmemBudget = 227 * 1024;  // opt-in dynamic shared memory per CTA
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -74,6 +76,8 @@ struct SweepArgs {
     unsigned long long* trace;  // optional: per CTA {t_start, t_end, smid}
     int debug_mode;             // diagnostics: 1 = consumers only wait/release
     int trace_level0;           // host-side flag: this launch is the top-level sweep
+    int dyn_first, ndyn;        // dynamic tail: segments [dyn_first, dyn_first + ndyn)
+    int* dyn_counter;           // work counter of the dynamic tail (zeroed per launch)
 };
 
 // ------------------------------------------------------------- PTX helpers --
@@ -413,6 +417,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     double* red = smem + ring_dbl;                // [2][NWC][RMAX]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * NWC * RMAX);
     uint64_t* empty = full + kMaxStages;
+    int4* meta = reinterpret_cast<int4*>(empty + kMaxStages);  // per stage {seg, tile, o, flags}
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -435,6 +440,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     const int rem0 = static_cast<int>(I0 - static_cast<int64_t>(p.G0 - 1) * p.r0);
     const int rem1 = static_cast<int>(I1 - static_cast<int64_t>(G1 - 1) * p.t1);
 
+    // Schedule (producer-driven): the static segments [seg_begin, seg_end) of
+    // this CTA, then chunks of the dynamic tail taken from a work counter by
+    // whichever CTA is free.  Every segment has its own B01 partial slot, so
+    // the fixed-order reduction stays bit-reproducible for any schedule.
+    // Per stage the producer publishes {segment, tile, o, flags} before its
+    // arrive (release); consumers read it after the full-barrier wait.
+    constexpr int kFirst = 1, kLast = 2, kDone = 4;
     if (warp == NWC) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
@@ -443,7 +455,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                              : "memory");
             int stage = 0;
             uint32_t phase = 0;
-            for (int s = seg_begin; s < seg_end; ++s) {
+            auto run_segment = [&](int s) {
                 const Seg sg = p.segs[s];
                 const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
                 const bool er = g0 == p.G0 - 1, ec = g1 == G1 - 1;
@@ -452,6 +464,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 const CUtensorMap* map = &maps.m[(er ? 1 : 0) | (ec ? 2 : 0)];
                 for (int o = sg.o0; o < sg.o1; ++o) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    meta[stage] = make_int4(s, sg.tile, o,
+                                            (o == sg.o0 ? kFirst : 0) | (o == sg.o1 - 1 ? kLast : 0));
                     mbar_arrive_expect_tx(&full[stage], bytes);
                     tma_load_3d(ring + stage * stage_dbl, map, g0 * p.r0, g1 * p.t1, o,
                                 &full[stage], pol);
@@ -460,7 +474,18 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                         phase ^= 1;
                     }
                 }
+            };
+            for (int s = seg_begin; s < seg_end; ++s) run_segment(s);
+            if (p.ndyn > 0) {
+                for (;;) {
+                    const int c = atomicAdd(p.dyn_counter, 1);
+                    if (c >= p.ndyn) break;
+                    run_segment(p.dyn_first + c);
+                }
             }
+            mbar_wait(&empty[stage], phase ^ 1);
+            meta[stage] = make_int4(-1, 0, 0, kDone);
+            mbar_arrive(&full[stage]);
         }
         return;
     }
@@ -470,38 +495,49 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     int stage = 0;
     uint32_t phase = 0;
     int rbuf = 0;
-    for (int s = seg_begin; s < seg_end; ++s) {
-        const Seg sg = p.segs[s];
-        const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
-        const int64_t R0s = static_cast<int64_t>(g0) * p.r0;
-        const int64_t R1s = static_cast<int64_t>(g1) * p.t1;
-        const int r0e = static_cast<int>(min64(p.r0, I0 - R0s));
-        const int t1e = static_cast<int>(min64(p.t1, I1 - R1s));
-
-        double u0r[NRA], u1c[NCB];
-        double acc[NRA][NCB];
-        int coff[NCB];  // smem offset (double2 units) of the thread's columns
+    int s = -1;
+    int g0 = 0, g1 = 0, r0e = 0, t1e = 0, cst = 0;
+    int64_t R0s = 0, R1s = 0;
+    double u0r[NRA], u1c[NCB];
+    double acc[NRA][NCB];
+    int coff[NCB];  // smem offset (double2 units) of the thread's columns
+    double* P0row = nullptr;
+    double* P1row = nullptr;
+    for (;;) {
+        mbar_wait(&full[stage], phase);
+        const int4 md = meta[stage];
+        if (md.w & kDone) break;
+        const int o = md.z;
+        if (md.w & kFirst) {
+            s = md.x;
+            const int tile = md.y;
+            g0 = tile % p.G0;
+            g1 = tile / p.G0;
+            R0s = static_cast<int64_t>(g0) * p.r0;
+            R1s = static_cast<int64_t>(g1) * p.t1;
+            r0e = static_cast<int>(min64(p.r0, I0 - R0s));
+            t1e = static_cast<int>(min64(p.t1, I1 - R1s));
+            cst = r0e;  // smem column stride (doubles) = box rows
 #pragma unroll
-        for (int q = 0; q < NP; ++q)
+            for (int q = 0; q < NP; ++q)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int i = 64 * q + 2 * lane + h;
-                u0r[2 * q + h] = i < r0e ? __ldg(p.u0 + R0s + i) : 0.0;
+                for (int h = 0; h < 2; ++h) {
+                    const int i = 64 * q + 2 * lane + h;
+                    u0r[2 * q + h] = i < r0e ? __ldg(p.u0 + R0s + i) : 0.0;
+                }
+#pragma unroll
+            for (int b = 0; b < NCB; ++b) {
+                const int j = warp + NWC * b;
+                u1c[b] = j < t1e ? __ldg(p.u1 + R1s + j) : 0.0;
+                coff[b] = (min(j, t1e - 1) * cst) / 2 + lane;
+#pragma unroll
+                for (int a = 0; a < NRA; ++a) acc[a][b] = 0.0;
             }
-#pragma unroll
-        for (int b = 0; b < NCB; ++b) {
-            const int j = warp + NWC * b;
-            u1c[b] = j < t1e ? __ldg(p.u1 + R1s + j) : 0.0;
-            coff[b] = (min(j, t1e - 1) * r0e) / 2 + lane;
-#pragma unroll
-            for (int a = 0; a < NRA; ++a) acc[a][b] = 0.0;
+            P0row = p.P0 + static_cast<int64_t>(g1) * p.P0_stride + R0s;
+            P1row = p.P1 ? p.P1 + static_cast<int64_t>(g0) * p.P1_stride + R1s : nullptr;
         }
-        double* P0row = p.P0 + static_cast<int64_t>(g1) * p.P0_stride + R0s;
-        double* P1row = p.P1 ? p.P1 + static_cast<int64_t>(g0) * p.P1_stride + R1s : nullptr;
-
-        for (int o = sg.o0; o < sg.o1; ++o) {
+        {
             const double wo = __ldg(p.W + o);
-            mbar_wait(&full[stage], phase);
             const double2* st = reinterpret_cast<const double2*>(ring + stage * stage_dbl);
             if (p.debug_mode == 1) {
                 __syncwarp();
@@ -575,18 +611,20 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 P0row[static_cast<int64_t>(o) * I0 + i] = sum;
             }
             rbuf ^= 1;
-        }
-
-        double* dst = p.P01 + static_cast<int64_t>(s) * p.r0 * p.t1;
+            if (md.w & kLast) {
+                // flush the B01 face partial of this segment
+                double* dst = p.P01 + static_cast<int64_t>(s) * p.r0 * p.t1;
 #pragma unroll
-        for (int b = 0; b < NCB; ++b) {
-            const int j = warp + NWC * b;
-            if (j >= t1e) continue;
+                for (int b = 0; b < NCB; ++b) {
+                    const int j = warp + NWC * b;
+                    if (j >= t1e) continue;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
-                const int i = 64 * q + 2 * lane;
-                if (i < r0e) dst[j * p.r0 + i] = acc[2 * q][b];
-                if (i + 1 < r0e) dst[j * p.r0 + i + 1] = acc[2 * q + 1][b];
+                    for (int q = 0; q < NP; ++q) {
+                        const int i = 64 * q + 2 * lane;
+                        if (i < r0e) dst[j * p.r0 + i] = acc[2 * q][b];
+                        if (i + 1 < r0e) dst[j * p.r0 + i + 1] = acc[2 * q + 1][b];
+                    }
+                }
             }
         }
     }
@@ -670,6 +708,7 @@ struct Level {
     int64_t I0 = 0, I1 = 0, O = 0;
     int nra = 4, ncb = 8, stages = 3;
     int stage_dbl = 0;
+    int dyn_first = 0, ndyn = 0;  // dynamic-tail segments (box kernel only)
     bool tma = false;
     int r0 = 0, t1 = 0, G0 = 0, G1 = 0, ncta = 0, nseg = 0, ntiles = 0;
     size_t smem = 0;
@@ -687,6 +726,7 @@ struct SweepPlan {
     std::vector<Level> levels;
     std::vector<int> host_meta;
     DeviceBuffer meta;
+    DeviceBuffer counters;  // one dynamic-tail work counter per level
     uint64_t work_elems = 0;
     uint64_t nblocks = 0;
 };
@@ -726,7 +766,7 @@ void tile_level(Level& L, int num_sms) {
         L.G1 = static_cast<int>((L.I1 + L.t1 - 1) / L.t1);
         L.ntiles = L.G0 * L.G1;
         const size_t red = static_cast<size_t>(2) * kBoxNWC * rm * 8;
-        const size_t bars = 2 * kMaxStages * 8;
+        const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16;
         const size_t box = static_cast<size_t>(L.r0) * L.t1 * 8;
         const size_t ring = kSmemBudget - red - bars - rm * 8 - 1024;
         L.stages = static_cast<int>(std::min<size_t>(kMaxStages, ring / box));
@@ -769,13 +809,42 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     L.ncta = static_cast<int>(ncta);
     std::vector<Seg> segs;
     std::vector<int> cta_seg(L.ncta + 1, 0);
-    const double per = total / static_cast<double>(L.ncta);
+    // The box kernel takes a dynamic tail: the last kDynFrac of the work is cut
+    // into chunks of ~kDynChunk full panels that free CTAs take from a work
+    // counter (SM bandwidth shares vary by ~10%; a static split waits for the
+    // slowest SM).
+    const bool dyn = L.tma && npanels >= static_cast<int64_t>(L.ncta) * 64;
+    const double static_total = dyn ? (1.0 - kDynFrac) * total : total;
+    const double full_cost = static_cast<double>(L.r0) * L.t1 + 512.0;
+    const double per = static_total / static_cast<double>(L.ncta);
     int cur = 0;          // CTA receiving the current panel
-    int seg_cta = -1;     // CTA owning segs.back()
+    int seg_cta = -1;     // CTA owning segs.back() (-1: dynamic chunk)
     double x = 0.0;       // cost of all earlier panels
+    double chunk = 0.0;   // cost of the open dynamic chunk
+    bool in_dyn = false;
     for (int t = 0; t < L.ntiles; ++t) {
         const double c = panel_cost(t);
         for (int64_t o = 0; o < L.O; ++o) {
+            if (!in_dyn && dyn && x + 0.5 * c >= static_total) {
+                in_dyn = true;
+                while (cur < L.ncta) cta_seg[++cur] = static_cast<int>(segs.size());
+                L.dyn_first = static_cast<int>(segs.size());
+            }
+            if (in_dyn) {
+                // guided chunk size: remaining / (2 ncta), at least kDynMinChunk panels
+                const double target = std::max(kDynMinChunk * full_cost,
+                                               (total - x) / (2.0 * L.ncta));
+                if (segs.size() == static_cast<size_t>(L.dyn_first) || segs.back().tile != t ||
+                    segs.back().o1 != o || chunk >= target) {
+                    segs.push_back(Seg{t, static_cast<int>(o), static_cast<int>(o + 1), 0});
+                    chunk = 0.0;
+                } else {
+                    segs.back().o1 = static_cast<int>(o + 1);
+                }
+                chunk += c;
+                x += c;
+                continue;
+            }
             const int target = std::min<int>(
                 L.ncta - 1, static_cast<int>((x + 0.5 * c) / per));
             while (cur < target) cta_seg[++cur] = static_cast<int>(segs.size());
@@ -788,7 +857,11 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
             x += c;
         }
     }
-    while (cur < L.ncta) cta_seg[++cur] = static_cast<int>(segs.size());
+    if (!in_dyn) {
+        while (cur < L.ncta) cta_seg[++cur] = static_cast<int>(segs.size());
+        L.dyn_first = static_cast<int>(segs.size());
+    }
+    L.ndyn = static_cast<int>(segs.size()) - L.dyn_first;
     L.nseg = static_cast<int>(segs.size());
     std::vector<int> tile_seg(L.ntiles + 1, 0);
     {
@@ -893,6 +966,7 @@ std::shared_ptr<SweepPlan> get_plan(r1_context* ctx, const uint64_t* dims, int o
     }
     plan_rec(*P, dims, order, order, d, m, Ref{Where::Tensor, 0}, true, ctx->num_sms);
     P->meta.ensure(std::max<size_t>(16, P->host_meta.size() * sizeof(int)));
+    P->counters.ensure(std::max<size_t>(1, P->levels.size()) * 64);
     R1_CUDA(cudaMemcpy(P->meta.ptr, P->host_meta.data(), P->host_meta.size() * sizeof(int),
                        cudaMemcpyHostToDevice));
     ctx->plans[key] = P;
@@ -1033,6 +1107,8 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         }
     };
 
+    R1_CUDA(cudaMemsetAsync(P->counters.ptr, 0, P->levels.size() * 64, ctx->stream));
+    int level_idx = 0;
     for (const Level& L : P->levels) {
         // outer weights
         OuterArgs oa{};
@@ -1067,6 +1143,10 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.P1_stride = L.I1 * L.O;
         s.trace = (&L == &P->levels.front()) ? ctx->dbg_sweep_trace : nullptr;
         s.trace_level0 = (&L == &P->levels.front()) ? 1 : 0;
+        s.dyn_first = L.dyn_first;
+        s.ndyn = L.ndyn;
+        s.dyn_counter = reinterpret_cast<int*>(P->counters.as<char>() + 64 * level_idx);
+        ++level_idx;
         {
             static const char* dm = std::getenv("R1_DEBUG_SWEEP_MODE");
             s.debug_mode = dm ? std::atoi(dm) : 0;
