@@ -88,8 +88,9 @@ inline void blockop_layout(BlockOp& op, const uint64_t* dims, int d, int64_t* co
 }
 
 #ifdef __CUDACC__
-// Phase A over tasks [blockIdx.x :: gridDim.x].
-__device__ inline void blockop_phase_a(const BlockOp& op, const double* __restrict__ x) {
+// Phase A over tasks [blockIdx.x :: gridDim.x] for the input xscale * x.
+__device__ inline void blockop_phase_a(const BlockOp& op, const double* __restrict__ x,
+                                       double xscale = 1.0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     if (op.dense) {
         const int64_t n = op.n;
@@ -100,8 +101,15 @@ __device__ inline void blockop_phase_a(const BlockOp& op, const double* __restri
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
                 const double* si = op.dense + i + j0 * n;
                 double s = 0.0;
-                for (int j = 0; j < nc; ++j) s = fma(si[j * n], x[j0 + j], s);
-                rp[i] = s;
+#pragma unroll
+                for (int h = 0; h < kMvCols; h += 16) {
+                    double sv[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) sv[j] = h + j < nc ? si[(h + j) * n] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) s = fma(sv[j], h + j < nc ? x[j0 + h + j] : 0.0, s);
+                }
+                rp[i] = s * xscale;
             }
         }
         return;
@@ -118,36 +126,54 @@ __device__ inline void blockop_phase_a(const BlockOp& op, const double* __restri
         const double* xm = x + op.offs[m];
         const double* xn = x + op.offs[n] + j0;
         double* rp = op.rowpart + op.rp_off[p] + static_cast<int64_t>(c) * rows;
+        // row partials: batches of 16 independent loads per row, FMAs in order
         for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
             const double* bi = B + i + j0 * rows;
             double s = 0.0;
-            for (int j = 0; j < nc; ++j) s = fma(bi[j * rows], xn[j], s);
-            rp[i] = s;
+#pragma unroll
+            for (int h = 0; h < kMvCols; h += 16) {
+                double bv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) bv[j] = h + j < nc ? bi[(h + j) * rows] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) s = fma(bv[j], h + j < nc ? xn[h + j] : 0.0, s);
+            }
+            rp[i] = s * xscale;
         }
+        // column dots: warp per column, 4 independent accumulators per lane
         for (int j = warp; j < nc; j += nw) {
             const double* col = B + (j0 + j) * rows;
-            double s = 0.0;
-            for (int64_t i = lane; i < rows; i += 32) s = fma(col[i], xm[i], s);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int64_t i = lane;
+            for (; i + 96 < rows; i += 128) {
+                s0 = fma(col[i], xm[i], s0);
+                s1 = fma(col[i + 32], xm[i + 32], s1);
+                s2 = fma(col[i + 64], xm[i + 64], s2);
+                s3 = fma(col[i + 96], xm[i + 96], s3);
+            }
+            for (; i < rows; i += 32) s0 = fma(col[i], xm[i], s0);
+            double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            if (lane == 0) op.coldot[op.cd_off[p] + j0 + j] = s;
+            if (lane == 0) op.coldot[op.cd_off[p] + j0 + j] = s * xscale;
         }
     }
 }
 
-// Phase B: y[t] for t in [start :: stride].
+// Phase B: y[t] for t in [start, end) step stride (end < 0: n).
 __device__ inline void blockop_phase_b(const BlockOp& op, double* __restrict__ y, int64_t start,
-                                       int64_t stride) {
+                                       int64_t stride, int64_t end = -1) {
     const int d = op.d;
+    const int64_t stop = end < 0 ? op.n : end;
     if (op.dense) {
-        for (int64_t t = start; t < op.n; t += stride) {
+        for (int64_t t = start; t < stop; t += stride) {
             double s = 0.0;
             for (int c = 0; c < op.ntasks; ++c) s += op.rowpart[static_cast<int64_t>(c) * op.n + t];
             y[t] = s;
         }
         return;
     }
-    for (int64_t t = start; t < op.n; t += stride) {
+    for (int64_t t = start; t < stop; t += stride) {
         int m = 0;
         while (t >= op.offs[m + 1]) ++m;
         const int64_t i = t - op.offs[m];
@@ -158,6 +184,7 @@ __device__ inline void blockop_phase_b(const BlockOp& op, double* __restrict__ y
             const int64_t nch = (op.dims[n] + kMvCols - 1) / kMvCols;
             const double* rp = op.rowpart + op.rp_off[p] + i;
             double r = 0.0;
+#pragma unroll 8
             for (int64_t c = 0; c < nch; ++c) r += rp[c * op.dims[m]];
             s += r;
         }

@@ -17,6 +17,7 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 void forget_matvec_plans(r1_context* ctx);
 void forget_eig_plans(r1_context* ctx);
 void forget_solver_handles(r1_context* ctx);
+void forget_solver_work(r1_context* ctx);
 void dot_device(r1_context* ctx, const double* x, const double* y, uint64_t n, double* out_dev);
 void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* info);
 
@@ -150,6 +151,7 @@ int r1_context_destroy(r1_context* ctx) {
         forget_matvec_plans(ctx);
         forget_eig_plans(ctx);
         forget_solver_handles(ctx);
+        forget_solver_work(ctx);
         ctx->plans.clear();
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
         delete ctx;

@@ -26,6 +26,8 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <vector>
@@ -38,6 +40,7 @@ namespace {
 
 constexpr int kEigThreads = 512;
 constexpr int kMaxKrylov = 512;
+constexpr size_t kEigDynSmem = sizeof(double) * 14 * kMaxKrylov;
 
 struct EigArgs {
     const BlockOp* op;
@@ -55,6 +58,8 @@ struct EigArgs {
     double* alpha;   // maxm
     double* beta;    // maxm
     double* part;    // 4 * gridDim
+    double* pdot1;   // gridDim x (kMaxKrylov+1) partial dots (CGS pass 1)
+    double* pdot2;   // same, pass 2
     double* sT;      // 2 * maxm: T-eigenvectors (lo, hi)
     int* ctl;        // [0] state, [1] picked end, [2] steps, [3] restarts, [4] breakdowns
     double* stats;   // [theta_lo, theta_hi, res_lo, res_hi, value]
@@ -172,11 +177,16 @@ __device__ void tri_eigvec(const double* a, const double* b, int m, double theta
 
 // CTA 0: extremes of T_m, eigenvectors, bounds, convergence decision.
 __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact, int restarts) {
-    __shared__ double ta[kMaxKrylov], tb[kMaxKrylov];
+    // tridiagonal, two inverse-iteration workspaces and the two T-eigenvectors
+    // live in dynamic shared memory (kEigDynSmem bytes)
+    extern __shared__ double dsm[];
+    double* ta = dsm;
+    double* tb = ta + kMaxKrylov;
+    double* work = tb + kMaxKrylov;
+    double* work2 = work + 5 * kMaxKrylov;
+    double* sv[2] = {work2 + 5 * kMaxKrylov, work2 + 6 * kMaxKrylov};
     __shared__ double lohi[4];  // [a_lo, b_lo, a_hi, b_hi] intervals
     __shared__ int cnt[kEigThreads];
-    __shared__ double work[5 * kMaxKrylov];
-    __shared__ double sv[2][kMaxKrylov];
     __shared__ double theta[2];
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         ta[i] = a.alpha[i];
@@ -204,20 +214,22 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
     const int half = blockDim.x / 2;
     const int side = threadIdx.x < half ? 0 : 1;  // 0: lowest, 1: highest
     const int k = threadIdx.x - side * half;
-    for (int round = 0; round < 12; ++round) {
+    __shared__ int found[2];
+    for (int round = 0; round < 10; ++round) {
         const double lo = lohi[2 * side], hi = lohi[2 * side + 1];
+        if (hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300) break;  // uniform per CTA
         const double x = lo + (hi - lo) * static_cast<double>(k + 1) / static_cast<double>(half + 1);
         cnt[threadIdx.x] = sturm_count(ta, tb, m, x, pivmin);
+        if (k == 0) found[side] = half;
+        __syncthreads();
+        // lowest: first point with count >= 1; highest: first with count >= m
+        const int target = side == 0 ? 1 : m;
+        const bool hit = cnt[threadIdx.x] >= target;
+        const bool prev = k > 0 && cnt[threadIdx.x - 1] >= target;
+        if (hit && !prev) found[side] = k;  // counts are monotone: one writer
         __syncthreads();
         if (k == 0) {
-            // lowest: first point with count >= 1; highest: first with count >= m
-            const int target = side == 0 ? 1 : m;
-            int f = half;
-            for (int t = 0; t < half; ++t)
-                if (cnt[side * half + t] >= target) {
-                    f = t;
-                    break;
-                }
+            const int f = found[side];
             const double nlo = f == 0 ? lo : lo + (hi - lo) * static_cast<double>(f) / (half + 1);
             const double nhi =
                 f == half ? hi : lo + (hi - lo) * static_cast<double>(f + 1) / (half + 1);
@@ -226,16 +238,24 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
         }
         __syncthreads();
     }
+    if (threadIdx.x == 0 || threadIdx.x == half) {
+        const double th = 0.5 * (lohi[2 * side] + lohi[2 * side + 1]);
+        theta[side] = th;
+        tri_eigvec(ta, tb, m, th, tnorm, sv[side], side == 0 ? work : work2);
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        theta[0] = 0.5 * (lohi[0] + lohi[1]);
-        theta[1] = 0.5 * (lohi[2] + lohi[3]);
-        tri_eigvec(ta, tb, m, theta[0], tnorm, sv[0], work);
-        tri_eigvec(ta, tb, m, theta[1], tnorm, sv[1], work);
         const double res_lo = fabs(beta_last * sv[0][m - 1]);
         const double res_hi = fabs(beta_last * sv[1][m - 1]);
         const double scale = fmax(fabs(theta[0]), fabs(theta[1]));
-        const bool conv = exact || (res_lo <= a.tol * scale && res_hi <= a.tol * scale);
         const int pick = fabs(theta[0]) > fabs(theta[1]) * (1.0 + 1e-12) ? 0 : 1;
+        // The picked end must be converged to tol.  The other end matters only
+        // through the pick rule: it is enough that it is an accurate Ritz value
+        // (<= 1e-6 relative) whose magnitude is clearly on the losing side.
+        const double rp = pick ? res_hi : res_lo, ro = pick ? res_lo : res_hi;
+        const double tp = fabs(theta[pick]), to = fabs(theta[1 - pick]);
+        const bool decided = ro <= 1e-6 * scale && to + 100.0 * ro < tp * (1.0 - 1e-6);
+        const bool conv = exact || (rp <= a.tol * scale && (ro <= a.tol * scale || decided));
         a.stats[0] = theta[0];
         a.stats[1] = theta[1];
         a.stats[2] = res_lo;
@@ -253,83 +273,183 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a) {
     cg::grid_group grid = cg::this_grid();
+    // one-CTA launches (small operators) synchronise with the CTA barrier
+    auto gsync = [&]() {
+        if (gridDim.x == 1)
+            __syncthreads();
+        else
+            grid.sync();
+    };
+    // diagnostics: per-phase ns accumulated by CTA 0 thread 0 (stats[8..15])
+    unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tlast = gtimer();
+    auto mark = [&](int ph) {
+        const unsigned long long t = gtimer();
+        tacc[ph] += t - tlast;
+        tlast = t;
+    };
     __shared__ BlockOp op;
     __shared__ double red[32];
+    __shared__ double hsh[kMaxKrylov + 1];
     if (threadIdx.x == 0) op = *a.op;
     __syncthreads();
     const int64_t n = a.n;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int G = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // Row ownership: CTA b owns rows [r0, r1) of every length-n vector; the
+    // reorthogonalisation works on own rows + fixed-order partial sums.
+    const int64_t R = (n + G - 1) / G;
+    const int64_t r0 = min(n, static_cast<int64_t>(blockIdx.x) * R);
+    const int64_t r1 = min(n, r0 + R);
+    const int ld = kMaxKrylov + 1;
 
-    // ---- start vector
-    for (int64_t i = gtid; i < n; i += gstride) {
-        const double r = hash_unit(static_cast<uint64_t>(i), 0x5eedull);
-        a.w[i] = a.x0 ? a.x0[i] + 1e-3 * r / sqrt(static_cast<double>(n)) : r;
-    }
-    int restarts = 0, breakdowns = 0;
-    auto normalize_w_into = [&](double* dst) {
+    // partial dots out[b*ld + k] = sum_{t in own rows} V[t,k] w[t], k <= kmax
+    auto partial_dots = [&](double* out, int kmax) {
+        for (int k = warp; k <= kmax; k += nw) {
+            const double* vk = a.V + static_cast<int64_t>(k) * n;
+            double s0 = 0.0, s1 = 0.0;
+            int64_t t = r0 + lane;
+            for (; t + 32 < r1; t += 64) {
+                s0 = fma(vk[t], a.w[t], s0);
+                s1 = fma(vk[t + 32], a.w[t + 32], s1);
+            }
+            if (t < r1) s0 = fma(vk[t], a.w[t], s0);
+            double s = s0 + s1;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) out[static_cast<int64_t>(blockIdx.x) * ld + k] = s;
+        }
+    };
+    // hsh[k] = sum_b in[b*ld + k]: warp per k, lanes over b, fixed shuffle
+    // tree (the same order in every CTA -> the same bits everywhere)
+    auto reduce_dots = [&](const double* in, int kmax) {
+        for (int k = warp; k <= kmax; k += nw) {
+            double s = 0.0;
+            for (int b = lane; b < G; b += 32) s += in[static_cast<int64_t>(b) * ld + k];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) hsh[k] = s;
+        }
+        __syncthreads();
+    };
+    // sum of the G partials part[slot*G + b], broadcast to the CTA
+    auto grid_sum = [&](const double* part, int slot) {
+        if (warp == 0) {
+            double s = 0.0;
+            for (int b = lane; b < G; b += 32) s += part[slot * G + b];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) red[31] = s;
+        }
+        __syncthreads();
+        const double v = red[31];
+        __syncthreads();
+        return v;
+    };
+    // own rows: w[t] -= sum_k V[t,k] hsh[k]; returns the CTA's sum of w^2 (thread 0)
+    auto update_rows = [&](int kmax, bool norm) {
+        double ss = 0.0;
+        for (int64_t t = r0 + warp; t < r1; t += nw) {
+            double s = 0.0;
+            for (int k = lane; k <= kmax; k += 32) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k], s);
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            const double wt = a.w[t] - s;
+            if (lane == 0) a.w[t] = wt;
+            ss = fma(wt, wt, ss);
+        }
+        __syncwarp();
+        if (norm) {
+            ss = lane == 0 ? ss : 0.0;
+            ss = cta_sum(ss, red);
+            if (threadIdx.x == 0) a.part[blockIdx.x] = ss;
+        }
+        __syncthreads();
+    };
+    // CGS2 of w (own rows) against V[:, 0..kmax]; leaves ||w||^2 partials in part[0..G)
+    auto cgs2 = [&](int kmax) {
+        partial_dots(a.pdot1, kmax);
+        gsync();
+        reduce_dots(a.pdot1, kmax);
+        update_rows(kmax, false);
+        partial_dots(a.pdot2, kmax);
+        gsync();
+        reduce_dots(a.pdot2, kmax);
+        update_rows(kmax, true);
+        gsync();
+    };
+
+    // ---- start vector -> V[:,0]
+    auto set_v0_from_w = [&]() {
         double s = 0.0;
-        for (int64_t i = gtid; i < n; i += gstride) s = fma(a.w[i], a.w[i], s);
+        for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) s = fma(a.w[t], a.w[t], s);
         s = cta_sum(s, red);
         if (threadIdx.x == 0) a.part[blockIdx.x] = s;
-        grid.sync();
-        const double nrm = sqrt(grid_total(a.part, 0));
-        for (int64_t i = gtid; i < n; i += gstride) dst[i] = a.w[i] / nrm;
-        grid.sync();
-        return nrm;
+        gsync();
+        const double nrm = sqrt(grid_sum(a.part, 0));
+        for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) a.V[t] = a.w[t] / nrm;
+        gsync();
     };
-    grid.sync();
-    normalize_w_into(a.V);
+    for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
+        const double r = hash_unit(static_cast<uint64_t>(t), 0x5eedull);
+        a.w[t] = a.x0 ? a.x0[t] + 1e-3 * r / sqrt(static_cast<double>(n)) : r;
+    }
+    set_v0_from_w();
 
-    // dots h[k] = V[:,k]' w for k <= j (CTA per column, round robin)
-    auto dots = [&](double* hh, int j) {
-        for (int k = blockIdx.x; k <= j; k += G) {
-            const double* vk = a.V + static_cast<int64_t>(k) * n;
-            double s = 0.0;
-            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(vk[i], a.w[i], s);
-            s = cta_sum(s, red);
-            if (threadIdx.x == 0) hh[k] = s;
-        }
-        grid.sync();
-    };
-    // w -= V[:, :j+1] hh; optionally accumulate ||w||^2 partials into part[0]
-    auto update = [&](const double* hh, int j, bool norm) {
-        double s = 0.0;
-        for (int64_t i = gtid; i < n; i += gstride) {
-            double acc = 0.0;
-            for (int k = 0; k <= j; ++k) acc = fma(a.V[i + static_cast<int64_t>(k) * n], hh[k], acc);
-            const double wi = a.w[i] - acc;
-            a.w[i] = wi;
-            s = fma(wi, wi, s);
-        }
-        if (norm) {
-            s = cta_sum(s, red);
-            if (threadIdx.x == 0) a.part[blockIdx.x] = s;
-        }
-        grid.sync();
-    };
-
+    int restarts = 0, breakdowns = 0;
     int j = 0;
     double anorm = 0.0;
+    double inv_beta = 1.0;  // V[:,j] = w * inv_beta for j > 0 (materialised in phase B)
     for (;;) {
-        // ---- one Lanczos step on v_j
-        const double* vj = a.V + static_cast<int64_t>(j) * n;
-        blockop_phase_a(op, vj);
-        grid.sync();
-        blockop_phase_b(op, a.w, gtid, gstride);
-        grid.sync();
-        dots(a.h, j);
-        update(a.h, j, false);
-        dots(a.h2, j);
-        update(a.h2, j, true);
-        double nrm = sqrt(grid_total(a.part, 0));
-        const double alpha = a.h[j] + a.h2[j];
+        // [A] matvec partials of v_j
+        mark(7);
+        if (j == 0)
+            blockop_phase_a(op, a.V);
+        else
+            blockop_phase_a(op, a.w, inv_beta);
+        mark(0);
+        gsync();
+        mark(1);
+        // [B] materialise own rows of v_j, then w = J v_j (own rows), partial dots
+        if (j > 0) {
+            double* vj = a.V + static_cast<int64_t>(j) * n;
+            for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) vj[t] = a.w[t] * inv_beta;
+            __syncthreads();
+        }
+        blockop_phase_b(op, a.w, r0 + threadIdx.x, blockDim.x, r1);
+        __syncthreads();
+        mark(2);
+        cgs2(j);
+        mark(3);
+        // alpha_j = h1[j] + h2[j]; h2 is in hsh, h1[j] is re-reduced (same order)
+        double alpha = 0.0;
+        {
+            const double h2j = hsh[j];
+            if (warp == 0) {
+                double s1 = 0.0;
+                for (int b = lane; b < G; b += 32) s1 += a.pdot1[static_cast<int64_t>(b) * ld + j];
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+                if (lane == 0) red[30] = s1;
+            }
+            __syncthreads();
+            alpha = red[30] + h2j;
+            __syncthreads();
+        }
+        double nrm = sqrt(grid_sum(a.part, 0));
         anorm = fmax(anorm, fabs(alpha) + nrm + (j > 0 ? a.beta[j - 1] : 0.0));
         const bool space_full = (j + 1 == n);
-        bool breakdown = !space_full && nrm <= 1e-13 * anorm;
+        const bool breakdown = !space_full && nrm <= 1e-13 * anorm;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.alpha[j] = alpha;
             a.beta[j] = breakdown ? 0.0 : nrm;
@@ -337,41 +457,37 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         if (breakdown) {
             // invariant subspace: continue with a fresh direction orthogonal to V
             ++breakdowns;
-            for (int64_t i = gtid; i < n; i += gstride)
-                a.w[i] = hash_unit(static_cast<uint64_t>(i), 0xb00ull + breakdowns);
-            grid.sync();
-            dots(a.h, j);
-            update(a.h, j, false);
-            dots(a.h2, j);
-            update(a.h2, j, true);
-            nrm = sqrt(grid_total(a.part, 0));
+            for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x)
+                a.w[t] = hash_unit(static_cast<uint64_t>(t), 0xb00ull + breakdowns);
+            __syncthreads();
+            cgs2(j);
+            nrm = sqrt(grid_sum(a.part, 0));
         }
-        if (!space_full) {
-            for (int64_t i = gtid; i < n; i += gstride)
-                a.V[i + static_cast<int64_t>(j + 1) * n] = a.w[i] / nrm;
-        }
-        grid.sync();
+        inv_beta = 1.0 / nrm;
         ++j;
         const bool size_limit = (j == a.maxm) || space_full;
+        mark(4);
         if (((j >= a.min_steps && j % a.check_every == 0) && !breakdown) || size_limit) {
             if (blockIdx.x == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts);
-            grid.sync();
+            mark(5);
+            gsync();
+            mark(6);
             if (a.ctl[0]) break;
             if (size_limit) {
                 if (restarts >= a.max_restarts) break;  // best effort: ctl[0] stays 0
                 // restart from (x_lo + x_hi): both ends stay represented
                 ++restarts;
-                for (int64_t i = gtid; i < n; i += gstride) {
+                for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
                     double s0 = 0.0, s1 = 0.0;
                     for (int k = 0; k < j; ++k) {
-                        const double v = a.V[i + static_cast<int64_t>(k) * n];
+                        const double v = a.V[t + static_cast<int64_t>(k) * n];
                         s0 = fma(v, a.sT[k], s0);
                         s1 = fma(v, a.sT[kMaxKrylov + k], s1);
                     }
-                    a.w[i] = s0 + s1;
+                    a.w[t] = s0 + s1;
                 }
-                grid.sync();
-                normalize_w_into(a.V);
+                gsync();
+                set_v0_from_w();
                 j = 0;
                 anorm = 0.0;
             }
@@ -407,7 +523,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
             besti = oi;
         }
     }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // (warp, lane as above)
     if (lane == 0) {
         bv[warp] = best;
         bi[warp] = besti;
@@ -425,7 +541,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         a.part[2 * G + blockIdx.x] = static_cast<double>(i0);
         a.part[blockIdx.x] = ss;
     }
-    grid.sync();
+    gsync();
     double b0 = -1.0;
     int64_t i0 = 0;
     for (int b = 0; b < G; ++b) {
@@ -438,9 +554,10 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     }
     const double nrm = sqrt(grid_total(a.part, 0));
     const double sgn = a.out_vec[i0] < 0.0 ? -1.0 : 1.0;
-    grid.sync();
+    gsync();
     for (int64_t i = gtid; i < n; i += gstride) a.out_vec[i] = sgn * a.out_vec[i] / nrm;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int k = 0; k < 8; ++k) a.stats[8 + k] = static_cast<double>(tacc[k]);
         *a.out_value = a.stats[4];
         a.ctl[2] = m;
         a.ctl[3] = restarts;
@@ -463,7 +580,8 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     const int64_t n = P.op.n;
     const int maxm = static_cast<int>(std::min<int64_t>(n, 320));
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
-                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 128;
+                         2 * static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 8) +
+                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 256;
     ctx->ws_eig.ensure(need * sizeof(double));
     double* base = ctx->ws_eig.as<double>();
     int64_t off = 0;
@@ -476,7 +594,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.n = n;
     a.maxm = maxm;
     a.check_every = n <= 64 ? 1 : 8;
-    a.min_steps = static_cast<int>(std::min<int64_t>(n, 16));
+    a.min_steps = static_cast<int>(std::min<int64_t>(n, 24));
     a.max_restarts = 6;
     a.tol = 1e-13;
     a.x0 = x0;
@@ -486,9 +604,11 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.h2 = take(maxm + 1);
     a.alpha = take(maxm);
     a.beta = take(maxm);
-    a.part = take(4 * ctx->num_sms);
+    a.part = take(4 * ctx->num_sms + 8);
+    a.pdot1 = take(static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 1));
+    a.pdot2 = take(static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 1));
     a.sT = take(2 * kMaxKrylov);
-    a.stats = take(8);
+    a.stats = take(16);
     a.ctl = reinterpret_cast<int*>(take(4));
     BlockOp op = P.op;
     op.coldot = take(std::max<int64_t>(P.coldot_n, 1));
@@ -500,14 +620,49 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.out_value = value_dev;
     a.out_vec = vec_dev;
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
+    static int configured = -1;
+    if (configured != ctx->device) {
+        R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kEigDynSmem)));
+        configured = ctx->device;
+    }
     int per_sm = 0;
-    R1_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_kernel, kEigThreads, 0));
+    R1_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_kernel, kEigThreads,
+                                                          kEigDynSmem));
     if (per_sm < 1) fail(R1_ERR_CUDA, "lanczos kernel cannot be resident");
     void* args[] = {&a};
-    R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel),
-                                        dim3(ctx->num_sms), dim3(kEigThreads), args, 0,
-                                        ctx->stream));
+    // Small operators (C1/C4-sized: n <= 1024 and <= 2 MB of blocks) run on one
+    // CTA with CTA barriers: a cooperative grid sync costs ~5 us, more than
+    // a whole Lanczos step's work there.
+    static const char* gs = std::getenv("R1_EIG_GRID");
+    const int64_t op_bytes = 8 * (P.op.dense ? n * n : P.coldot_n * 0 + [&] {
+        int64_t b = 0;
+        for (int p = 0; p < P.op.npairs; ++p) b += P.op.dims[P.op.pm[p]] * P.op.dims[P.op.pn[p]];
+        return b;
+    }());
+    const int auto_grid = (n <= 1024 && op_bytes <= (int64_t(2) << 20)) ? 1 : ctx->num_sms;
+    (void)auto_grid;
+    static const char* g1 = std::getenv("R1_EIG_SMALL_ONE_CTA");
+    const int grid = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs)))
+                        : (g1 && std::atoi(g1) ? auto_grid : ctx->num_sms);
+    R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel), dim3(grid),
+                                        dim3(kEigThreads), args, kEigDynSmem, ctx->stream));
     check_launch(ctx, "lanczos_kernel");
+    static const bool dbg = std::getenv("R1_DEBUG_EIG") != nullptr;
+    if (dbg) {
+        int ctl[5];
+        double st[16];
+        R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr,
+                     "[r1 eig] n=%lld conv=%d pick=%d steps=%d restarts=%d breakdowns=%d "
+                     "lo=%.17g hi=%.17g res_lo=%.3g res_hi=%.3g | us: A=%.1f syncA=%.1f B=%.1f "
+                     "cgs2=%.1f tail=%.1f text=%.1f synct=%.1f other=%.1f\n",
+                     static_cast<long long>(n), ctl[0], ctl[1], ctl[2], ctl[3], ctl[4], st[0], st[1],
+                     st[2], st[3], st[8] * 1e-3, st[9] * 1e-3, st[10] * 1e-3, st[11] * 1e-3,
+                     st[12] * 1e-3, st[13] * 1e-3, st[14] * 1e-3, st[15] * 1e-3);
+    }
     if (info_host || stats_host) {
         int ctl[5];
         double st[5];

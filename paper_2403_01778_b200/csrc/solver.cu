@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -166,6 +168,22 @@ struct Work {
     }
     void sync() { R1_CUDA(cudaStreamSynchronize(st())); }
 };
+
+// Working sets are cached per (context, dims, dense): repeated solves on the
+// same shape do not reallocate.
+std::map<std::pair<r1_context*, std::vector<uint64_t>>, std::shared_ptr<Work>>& work_cache() {
+    static std::map<std::pair<r1_context*, std::vector<uint64_t>>, std::shared_ptr<Work>> m;
+    return m;
+}
+
+Work& work_for(r1_context* ctx, const r1_tensor* a, bool dense) {
+    std::vector<uint64_t> key = a->dims;
+    key.push_back(dense ? 1 : 0);
+    auto& w = work_cache()[{ctx, key}];
+    if (!w) w = std::make_shared<Work>(ctx, a, dense);
+    w->A = a;
+    return *w;
+}
 
 struct RunResult {
     std::vector<double> factors;  // host, flat
@@ -353,6 +371,15 @@ std::vector<double> initial_factors(const r1_tensor* a, const r1_solve_options& 
 
 }  // namespace
 
+void forget_solver_work(r1_context* ctx) {
+    auto& m = work_cache();
+    for (auto it = m.begin(); it != m.end();)
+        if (it->first.first == ctx)
+            it = m.erase(it);
+        else
+            ++it;
+}
+
 }  // namespace r1
 
 using namespace r1;
@@ -375,7 +402,7 @@ int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
         if (opts->max_iters < 1) fail(R1_ERR_INVALID_ARGUMENT, "solver: max_iters must be >= 1");
         const bool acc = alg == "ihoscf";
         auto t0 = std::chrono::steady_clock::now();
-        Work w(ctx, a, acc);
+        Work& w = work_for(ctx, a, acc);
         RunResult rr;
         bool restarted = false;
         try {

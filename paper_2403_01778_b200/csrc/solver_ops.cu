@@ -231,6 +231,9 @@ Dims make_dims(const uint64_t* dims, int order) {
 
 struct SolverHandle {
     cusolverDnHandle_t h = nullptr;
+    DeviceBuffer work, ipiv64, dwork, dop;  // RQI / dense-assembly scratch, reused
+    std::vector<char> hwork;
+    std::vector<uint64_t> dop_dims;
     ~SolverHandle() {
         if (h) cusolverDnDestroy(h);
     }
@@ -241,16 +244,21 @@ std::map<r1_context*, std::shared_ptr<SolverHandle>>& solver_handles() {
     return m;
 }
 
-cusolverDnHandle_t solver_handle(r1_context* ctx) {
+SolverHandle& handle_state(r1_context* ctx) {
     auto& H = solver_handles()[ctx];
-    if (!H) {
-        H = std::make_shared<SolverHandle>();
-        if (cusolverDnCreate(&H->h) != CUSOLVER_STATUS_SUCCESS)
-            fail(R1_ERR_CUDA, "cusolverDnCreate failed");
+    if (!H) H = std::make_shared<SolverHandle>();
+    return *H;
+}
+
+cusolverDnHandle_t solver_handle(r1_context* ctx) {
+    SolverHandle& H = handle_state(ctx);
+    if (!H.h && cusolverDnCreate(&H.h) != CUSOLVER_STATUS_SUCCESS) {
+        H.h = nullptr;
+        fail(R1_ERR_CUDA, "cusolverDnCreate failed");
     }
-    if (cusolverDnSetStream(H->h, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
+    if (cusolverDnSetStream(H.h, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
         fail(R1_ERR_CUDA, "cusolverDnSetStream failed");
-    return H->h;
+    return H.h;
 }
 
 }  // namespace
@@ -279,18 +287,19 @@ void flip_first(r1_context* ctx, double* u0, int64_t n0, const double* lam_in, d
 
 void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                        double* S) {
-    BlockOp op;
+    SolverHandle& H = handle_state(ctx);
+    static thread_local BlockOp op;  // host staging must outlive the async copy
     int64_t cn, rn;
+    op = BlockOp{};
     blockop_layout(op, dims, order, &cn, &rn);
     op.blocks = blocks;
-    DeviceBuffer dop;
-    dop.ensure(sizeof(BlockOp));
-    R1_CUDA(cudaMemcpyAsync(dop.ptr, &op, sizeof(BlockOp), cudaMemcpyHostToDevice, ctx->stream));
+    H.dop.ensure(sizeof(BlockOp));
+    R1_CUDA(cudaMemcpyAsync(H.dop.ptr, &op, sizeof(BlockOp), cudaMemcpyHostToDevice, ctx->stream));
+    R1_CUDA(cudaStreamSynchronize(ctx->stream));
     const int64_t nn = op.n * op.n;
     const int g = static_cast<int>(std::min<int64_t>((nn + 255) / 256, ctx->num_sms * 16));
-    dense_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(dop.as<BlockOp>(), S);
+    dense_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(H.dop.as<BlockOp>(), S);
     check_launch(ctx, "dense_kernel");
-    R1_CUDA(cudaStreamSynchronize(ctx->stream));  // dop is freed on return
 }
 
 // One RQI step on the dense symmetric S (device, n x n, column-major) and x
@@ -308,7 +317,9 @@ bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, doub
     if (cusolverDnDsytrf_bufferSize(h, static_cast<int>(n), W, static_cast<int>(n), &lwork) !=
         CUSOLVER_STATUS_SUCCESS)
         fail(R1_ERR_CUDA, "cusolverDnDsytrf_bufferSize failed");
-    DeviceBuffer work, ipiv64;
+    SolverHandle& H = handle_state(ctx);
+    DeviceBuffer& work = H.work;
+    DeviceBuffer& ipiv64 = H.ipiv64;
     work.ensure(std::max<size_t>(1, static_cast<size_t>(lwork)) * sizeof(double));
     ipiv64.ensure(std::max<int64_t>(n, 1) * sizeof(int64_t));
     // rho = x'Sx (sym_eig.cpp:417-418); ||S||_F only matters when rho == 0
@@ -344,15 +355,13 @@ bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, doub
                                         ipiv64.as<int64_t>(), CUDA_R_64F, y, n, &dws, &hws) !=
             CUSOLVER_STATUS_SUCCESS)
             fail(R1_ERR_CUDA, "cusolverDnXsytrs_bufferSize failed");
-        DeviceBuffer dwork;
-        dwork.ensure(std::max<size_t>(dws, 16));
-        std::vector<char> hwork(std::max<size_t>(hws, 16));
+        H.dwork.ensure(std::max<size_t>(dws, 16));
+        if (H.hwork.size() < std::max<size_t>(hws, 16)) H.hwork.resize(std::max<size_t>(hws, 16));
         if (cusolverDnXsytrs(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, W, n, ipiv64.as<int64_t>(),
-                             CUDA_R_64F, y, n, dwork.ptr, dws, hwork.data(), hws, info) !=
+                             CUDA_R_64F, y, n, H.dwork.ptr, dws, H.hwork.data(), hws, info) !=
             CUSOLVER_STATUS_SUCCESS)
             fail(R1_ERR_CUDA, "cusolverDnXsytrs failed");
         count_launch(ctx);
-        R1_CUDA(cudaStreamSynchronize(ctx->stream));  // dwork / hwork lifetime
         normalize_check_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(y, n, info + 1);
         check_launch(ctx, "normalize_check_kernel");
         int ok = 0;
