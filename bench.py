@@ -245,6 +245,23 @@ def run_b200(args):
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0, dist)
     e2e_value = sweep_bytes(dims) * e2e_steps / e2e_s / 1e9
+
+    # e2e with the tensor resident (uploaded once, as in a solve): per step the
+    # factors go H2D and the blocks come back D2H through the same C-ABI calls
+    def e2e_resident_step():
+        fac.copy_(fac_host, non_blocking=True)
+        step()
+        blocks_host.copy_(gblocks, non_blocking=True)
+        stream.synchronize()
+
+    e2e_resident_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_resident_step()
+    barrier()
+    e2e_res_s = max_over_ranks(time.perf_counter() - t0, dist)
+    e2e_res_value = sweep_bytes(dims) * args.steps / e2e_res_s / 1e9
     h2d = 8 * int(np.prod(dims)) + 8 * sum(dims)
     d2h = 8 * nb
 
@@ -262,6 +279,15 @@ def run_b200(args):
                         "sweeps": rep.total_sweeps, "converged": rep.converged,
                         "lambda": rep.result.lambda_,
                         "t_build_j": round(rep.wall_build_j(), 6), "t_eig": round(rep.wall_eig(), 6)}
+
+    # ---- the other BASELINE configs (single GPU): sweep throughput and
+    # time-to-converge on device-generated inputs
+    other = None
+    if world == 1 and not args.skip_configs:
+        del t
+        a_dev = None
+        torch.cuda.empty_cache()
+        other = other_configs(r1, _lib, ctx, stream)
 
     # ---- CPU baseline: the compiled reference on this host (rank 0, N=1)
     cpu = None
@@ -309,17 +335,91 @@ def run_b200(args):
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                     "path": "r1_tensor_copy_from_host (pinned) + r1_build_j_device + D2H blocks"},
+            "e2e_resident": {"value": round(e2e_res_value, 3), "unit": "GB/s",
+                             "h2d_bytes_per_step": 8 * sum(dims), "d2h_bytes_per_step": d2h,
+                             "steps": args.steps,
+                             "path": "tensor resident (one upload per solve); factors H2D + "
+                                     "r1_build_j_device + blocks D2H per step"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
         if ttc is not None:
             out["time_to_converge"] = ttc
+        if other is not None:
+            out["configs"] = other
         if cpu is not None:
             out["cpu_baseline"] = cpu
         emit(out)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+OTHER_CONFIGS = [
+    # name, cfg, reference dims, solves: (alg, options)
+    ("C1", 1, (100, 100, 100), [("hoscf", dict(tol=1e-300, max_iters=500, init="provided",
+                                              scf_lambda_rtol=1e-12))]),
+    ("C3", 3, (200, 200, 200, 200), [("hoscf", dict(tol=1e-300, max_iters=100, record_kkt=False))]),
+    ("C4", 4, (60, 60, 60, 60, 60), [("hoscf", dict(tol=1e-10, max_iters=100)),
+                                     ("ihoscf", dict(tol=1e-10, max_iters=100))]),
+    ("C5", 5, (500, 2000, 4000), [("hoscf", dict(tol=1e-10, max_iters=200)),
+                                  ("ihoscf", dict(tol=1e-10, max_iters=200))]),
+]
+
+
+def other_configs(r1, _lib, ctx, stream):
+    import torch
+    res = {}
+    L = _lib.lib()
+    for name, cfg, dims, solves in OTHER_CONFIGS:
+        n = int(np.prod(dims))
+        a = torch.empty(n + 2, dtype=torch.float64, device="cuda")
+        t = r1.DeviceTensor.wrap(a.data_ptr(), dims, ctx, keepalive=a)
+        gd = _lib.dims_arr(dims)
+        _lib.check(L.r1_generate_config(ctx.handle, t.handle, cfg, cfg, _lib.u64p(gd), len(dims), 0))
+        fl = np.concatenate(uniform01_factors(dims, cfg))
+        fac = torch.from_numpy(fl).cuda()
+        nb = int(sum(dims[m] * dims[k] for m in range(len(dims)) for k in range(m + 1, len(dims))))
+        blocks = torch.empty(nb, dtype=torch.float64, device="cuda")
+
+        def sweep():
+            _lib.check(L.r1_build_j_device(ctx.handle, t.handle, fac.data_ptr(), blocks.data_ptr(),
+                                           None))
+
+        for _ in range(3):
+            sweep()
+        reps = 20
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            sweep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        entry = {"dims_reference_order": list(dims), "tensor_bytes": 8 * n,
+                 "sweep_ms": round(ms, 4), "sweep_gbs": round(sweep_bytes(dims) / ms / 1e6, 2)}
+        for alg, kw in solves:
+            init = kw.pop("init", None)
+            o = r1.SolveOptions(seed=cfg, **kw)
+            kw["init"] = init
+            if init == "provided":  # C1: normalised all-ones (BASELINE config 1)
+                o.init = "provided"
+                o.init_factors = [np.ones(d) for d in dims]
+            torch.cuda.synchronize()
+            ts = time.perf_counter()
+            rep = r1.solve(alg, t, o, ctx)
+            te = time.perf_counter() - ts
+            entry[alg] = {"seconds": round(te, 6), "iterations": rep.iterations,
+                          "sweeps": rep.total_sweeps, "converged": rep.converged,
+                          "lambda": rep.result.lambda_, "t_build_j": round(rep.wall_build_j(), 6),
+                          "t_eig": round(rep.wall_eig(), 6), "options": {k: v for k, v in kw.items()
+                                                                         if v is not None}}
+        res[name] = entry
+        del t, a, blocks
+        torch.cuda.empty_cache()
+    return res
 
 
 def uniform01_factors(dims, seed):
@@ -464,6 +564,7 @@ def main():
     ap.add_argument("--cpu-slices", type=int, default=200)
     ap.add_argument("--skip-solve", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-configs", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -355,6 +355,8 @@ class Options:
     rqi_accept_rule: str = "magnitude"
     record_kkt: bool = True
     scf_lambda_rtol: float = 0.0
+    stop_rule: str = "kkt"           # baselines only (solvers.hpp:16, 25)
+    asvd_disjoint_pairs: bool = False
 
 
 @dataclass
@@ -464,7 +466,125 @@ def _run(a, dims, opts: Options, u, accelerated: bool) -> Report:
     return rep
 
 
-def _solve(a, dims, opts: Options, accelerated: bool) -> Report:
+# ------------------------------------------------------------- baselines --
+
+def contract_leaving(a, dims, factors, mode: int) -> np.ndarray:
+    """contract_leaving (tensor.cpp:220-233): A contracted with every factor but
+    `mode` (tensordot chain, highest mode first like ttvc, :157-170)."""
+    r = np.asarray(a).reshape(tuple(dims), order="F")
+    for k in reversed(range(len(dims))):
+        if k != mode:
+            r = np.tensordot(r, factors[k], axes=([k], [0]))
+    return np.asarray(r, dtype=np.float64).reshape(-1)
+
+
+def build_block(a, dims, factors, m: int, n: int) -> np.ndarray:
+    """build_block (nepv.hpp:54): I_m x I_n matrix A x_{k not in {m,n}} u_k."""
+    r = np.asarray(a).reshape(tuple(dims), order="F")
+    for k in reversed(range(len(dims))):
+        if k not in (m, n):
+            r = np.tensordot(r, factors[k], axes=([k], [0]))
+    return np.asarray(r, dtype=np.float64)
+
+
+def top_singular_pair(b: np.ndarray):
+    """top_singular_pair (solvers.cpp:358-381) via the [[0,B],[B',0]] embedding."""
+    r, c = b.shape
+    e = np.zeros((r + c, r + c))
+    e[:r, r:] = b
+    e[r:, :r] = b.T
+    val, vec = largest_magnitude_eigenpair(e)
+    if val < 0.0:
+        vec = vec.copy()
+        vec[r:] = -vec[r:]
+        val = -val
+    left, right = vec[:r].copy(), vec[r:].copy()
+    nl, nr = _norm2(left), _norm2(right)
+    if nl > 0:
+        left /= nl
+    if nr > 0:
+        right /= nr
+    if nl < 1e-12 or nr < 1e-12:
+        raise _Degenerate()
+    return val, left, right
+
+
+def asvd_pairs(d: int, disjoint: bool, iteration: int):
+    """asvd_pairs (solvers.cpp:383-397)."""
+    if disjoint:
+        off = (iteration - 1) % 2 if d > 2 else 0
+        return [(m, m + 1) for m in range(off, d - 1, 2)]
+    pairs = [(m, m + 1) for m in range(d - 1)]
+    if d > 2:
+        pairs.append((0, d - 1))
+    return pairs
+
+
+def _baseline_stop(a, dims, u, lam, lam_prev, a_norm, opts: Options):
+    """baseline_stop (solvers.cpp:100-127): (value, eq11, kkt_max)."""
+    blocks = build_j(a, dims, u) if len(dims) > 2 else np.asarray(a, dtype=np.float64).copy()
+    _, kkt_max, _ = kkt_from_blocks(dims, blocks, u)
+    nan = float("nan")
+    if opts.stop_rule == "eq11":
+        eq = scf_stopping_value(dims, blocks, stack_factors(u), lam)
+        return eq, eq, (kkt_max if opts.record_kkt else nan)
+    if opts.stop_rule == "lambda_delta":
+        v = abs(lam - lam_prev) / max(abs(lam), 1e-300)
+        return v, nan, (kkt_max if opts.record_kkt else nan)
+    return kkt_max / max(a_norm, 1e-300), nan, kkt_max
+
+
+def _run_baseline(a, dims, opts: Options, u, kind: str) -> Report:
+    """run_power_sweep (solvers.cpp:299-354) / run_asvd (:400-447)."""
+    rep = Report(kind)
+    d = len(dims)
+    u = [np.asarray(x, dtype=np.float64).copy() for x in u]
+    rep.lambda0 = multilinear_value(a, dims, u)
+    a_norm = float(np.sqrt(np.dot(a, a)))
+    lam_prev = rep.lambda0
+    for k in range(1, opts.max_iters + 1):
+        if kind == "hopm":
+            for n in range(d):
+                w = contract_leaving(a, dims, u, n)
+                nrm = _norm2(w)
+                if nrm < 1e-300:
+                    raise _Degenerate()
+                u[n] = w / nrm
+                lam = nrm
+        elif kind == "jacobi_hopm":
+            ws = [contract_leaving(a, dims, u, n) for n in range(d)]
+            for n in range(d):
+                nrm = _norm2(ws[n])
+                if nrm < 1e-300:
+                    raise _Degenerate()
+                u[n] = ws[n] / nrm
+            lam = multilinear_value(a, dims, u)
+        else:
+            jacobi = kind == "jacobi_asvd"
+            snap = [x.copy() for x in u]
+            nxt = [x.copy() for x in u]
+            for m, n in asvd_pairs(d, opts.asvd_disjoint_pairs, k):
+                src = snap if jacobi else nxt
+                _, left, right = top_singular_pair(build_block(a, dims, src, m, n))
+                nxt[m], nxt[n] = left, right
+            u = nxt
+            lam = multilinear_value(a, dims, u)
+        value, eq, kkt = _baseline_stop(a, dims, u, lam, lam_prev, a_norm, opts)
+        rep.trace.append({"lambda": lam, "stop_value": value, "eq11": eq, "kkt": kkt})
+        rep.iterations = k
+        lam_prev = lam
+        if value <= opts.tol:
+            rep.converged = True
+            break
+    lam = multilinear_value(a, dims, u)
+    if lam < 0:
+        lam = -lam
+        u[0] = -u[0]
+    rep.lam, rep.factors = lam, u
+    return rep
+
+
+def _solve(a, dims, opts: Options, accelerated) -> Report:
     """validate + with_restart (solvers.cpp:28-32, 78-91)."""
     if len(dims) < 2:
         raise ValueError("solver: tensor order must be >= 2")
@@ -472,11 +592,16 @@ def _solve(a, dims, opts: Options, accelerated: bool) -> Report:
         raise ValueError("solver: tol must be > 0")
     if opts.max_iters < 1:
         raise ValueError("solver: max_iters must be >= 1")
+    def go(u):
+        if isinstance(accelerated, str):
+            return _run_baseline(a, dims, opts, u, accelerated)
+        return _run(a, dims, opts, u, accelerated)
+
     try:
-        return _run(a, dims, opts, _initial(dims, opts), accelerated)
+        return go(_initial(dims, opts))
     except _Degenerate:
         try:
-            rep = _run(a, dims, opts, random_unit_factors(dims, opts.seed, 3), accelerated)
+            rep = go(random_unit_factors(dims, opts.seed, 3))
             rep.restarted = True
             return rep
         except _Degenerate as e:
@@ -489,3 +614,19 @@ def hoscf(a, dims, opts: Options) -> Report:
 
 def ihoscf(a, dims, opts: Options) -> Report:
     return _solve(a, dims, opts, True)
+
+
+def hopm(a, dims, opts: Options) -> Report:
+    return _solve(a, dims, opts, "hopm")
+
+
+def jacobi_hopm(a, dims, opts: Options) -> Report:
+    return _solve(a, dims, opts, "jacobi_hopm")
+
+
+def asvd(a, dims, opts: Options) -> Report:
+    return _solve(a, dims, opts, "asvd")
+
+
+def jacobi_asvd(a, dims, opts: Options) -> Report:
+    return _solve(a, dims, opts, "jacobi_asvd")

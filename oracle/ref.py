@@ -286,7 +286,8 @@ class SolveReportC(ctypes.Structure):
 
 
 def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None,
-          rqi_accept_rule=0, record_kkt=True, determinism=True, threads=0):
+          rqi_accept_rule=0, record_kkt=True, determinism=True, threads=0, stop_rule=0,
+          asvd_disjoint_pairs=False):
     """rank1::solve through the reference; returns a dict mirroring SolveReport."""
     a, ap = _d(a)
     dd, dp = _dims(dims)
@@ -298,6 +299,8 @@ def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None
     o.rqi_accept_rule = rqi_accept_rule
     o.record_kkt = 1 if record_kkt else 0
     o.threads = threads
+    o.stop_rule = stop_rule
+    o.asvd_disjoint_pairs = 1 if asvd_disjoint_pairs else 0
     keep = None
     if init_factors is not None:
         keep = np.ascontiguousarray(np.concatenate([np.asarray(f, dtype=np.float64)

@@ -573,6 +573,7 @@ def _options_c(o: SolveOptions, dims):
     c.threads = o.threads
     c.record_kkt = 1 if o.record_kkt else 0
     c.reuse_intermediates = 1 if o.reuse_intermediates else 0
+    c.asvd_disjoint_pairs = 1 if o.asvd_disjoint_pairs else 0
     c.scf_lambda_rtol = o.scf_lambda_rtol
     keep = None
     if o.init == "provided":
@@ -589,8 +590,9 @@ def _options_c(o: SolveOptions, dims):
 
 
 def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
-    """solvers.hpp:86: hoscf | ihoscf on the device.  The CPU baselines of the
-    reference are not on the device path and raise InvalidArgument."""
+    """solvers.hpp:86: every solver of the reference on the device —
+    hoscf | ihoscf (SCF on J(u)) and the baselines hopm | jacobi_hopm | asvd |
+    jacobi_asvd (solvers.cpp:299-447) on the same device sweep."""
     ctx = ctx or default_context()
     if algorithm not in _SOLVERS:
         raise InvalidArgument("unknown solver: " + algorithm)
@@ -625,7 +627,8 @@ def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None) 
     rep.iterations = int(r.iterations)
     rep.lambda0 = r.lambda0
     rep.restarted = bool(r.restarted)
-    rep.final_x = StackedVector(dims, fx.copy())
+    # SCF solvers: last stacked eigenvector; baselines: empty (solvers.hpp:56)
+    rep.final_x = StackedVector(dims, fx.copy()) if algorithm in ("hoscf", "ihoscf") else None
     rep.total_sweeps = int(r.total_sweeps)
     rep.t_total = r.t_total
     for i in range(rep.iterations):
@@ -645,3 +648,23 @@ def hoscf(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
 def ihoscf(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
     """solvers.hpp:68."""
     return solve("ihoscf", a, opts, ctx)
+
+
+def hopm(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
+    """solvers.hpp:70-72: Gauss-Seidel power sweep (ALS)."""
+    return solve("hopm", a, opts, ctx)
+
+
+def jacobi_hopm(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
+    """solvers.hpp:74-76: power sweep in Jacobi form."""
+    return solve("jacobi_hopm", a, opts, ctx)
+
+
+def asvd(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
+    """solvers.hpp:78-80: alternating SVD over adjacent mode pairs."""
+    return solve("asvd", a, opts, ctx)
+
+
+def jacobi_asvd(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
+    """solvers.hpp:82-83: asvd with all pair subproblems from the previous iterate."""
+    return solve("jacobi_asvd", a, opts, ctx)

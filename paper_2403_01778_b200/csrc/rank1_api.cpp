@@ -455,6 +455,7 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
     o.threads = opts.threads;
     o.record_kkt = opts.record_kkt ? 1 : 0;
     o.reuse_intermediates = opts.reuse_intermediates ? 1 : 0;
+    o.asvd_disjoint_pairs = opts.asvd_disjoint_pairs ? 1 : 0;
     std::vector<double> init;
     if (opts.init == InitKind::provided) {
         if (opts.init_factors.size() != a.order())
@@ -491,7 +492,8 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
     rep.iterations = r.iterations;
     rep.lambda0 = r.lambda0;
     rep.restarted = r.restarted != 0;
-    rep.final_x = StackedVector(a.dims(), fx);
+    // SCF solvers: last stacked eigenvector; baselines leave it empty (solvers.hpp:56)
+    if (algorithm == "hoscf" || algorithm == "ihoscf") rep.final_x = StackedVector(a.dims(), fx);
     for (int i = 0; i < r.iterations; ++i) {
         IterationRecord q;
         q.lambda = tr[i].lambda;
@@ -510,6 +512,14 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
 
 SolveReport hoscf(const DenseTensor& a, const SolveOptions& opts) { return solve("hoscf", a, opts); }
 SolveReport ihoscf(const DenseTensor& a, const SolveOptions& opts) { return solve("ihoscf", a, opts); }
+SolveReport hopm(const DenseTensor& a, const SolveOptions& opts) { return solve("hopm", a, opts); }
+SolveReport jacobi_hopm(const DenseTensor& a, const SolveOptions& opts) {
+    return solve("jacobi_hopm", a, opts);
+}
+SolveReport asvd(const DenseTensor& a, const SolveOptions& opts) { return solve("asvd", a, opts); }
+SolveReport jacobi_asvd(const DenseTensor& a, const SolveOptions& opts) {
+    return solve("jacobi_asvd", a, opts);
+}
 
 const std::vector<std::string>& solver_names() {
     static const std::vector<std::string> names = {"hoscf", "ihoscf", "hopm",

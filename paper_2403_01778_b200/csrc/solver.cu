@@ -351,6 +351,196 @@ RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
     return rr;
 }
 
+// ---- the reference's sweep baselines on the device sweep -------------------
+// run_power_sweep (solvers.cpp:299-354) and run_asvd (:400-447).  Every
+// contraction they need comes out of the fused sweep at the current factors:
+//   contract_leaving(A, u, n) = w_n = sqrt(d) (J(u) xhat)_n (one pass over A,
+//   like the reference's single-output TTV chain), contract_leaving_all = all
+//   d of them from the same pass, build_block(A, u, m, n) = block (m, n) of
+//   J(u), multilinear_value = u_0' w_0, kkt_report = the post step.
+// The stop evaluation at the new factors (baseline_stop, :100-127) is one
+// sweep whose J also feeds the next iteration's first contraction, so
+// Jacobi-HOPM and Jacobi-ASVD cost one pass over A per iteration, HOPM d
+// and ASVD one per pair whose inputs changed.
+enum class Baseline { hopm, jacobi_hopm, asvd, jacobi_asvd };
+
+// asvd_pairs (solvers.cpp:383-397)
+std::vector<std::pair<int, int>> asvd_pairs(int d, bool disjoint, int iteration) {
+    std::vector<std::pair<int, int>> pairs;
+    if (disjoint) {
+        const int offset = d > 2 ? (iteration - 1) % 2 : 0;
+        for (int m = offset; m + 1 < d; m += 2) pairs.emplace_back(m, m + 1);
+        return pairs;
+    }
+    for (int m = 0; m + 1 < d; ++m) pairs.emplace_back(m, m + 1);
+    if (d > 2) pairs.emplace_back(0, d - 1);
+    return pairs;
+}
+
+RunResult run_baseline(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
+                       Baseline kind) {
+    RunResult rr;
+    Events ev;
+    r1_context* ctx = w.ctx;
+    const cudaStream_t st = w.st();
+    const int d = w.d;
+    const int64_t n = w.n;
+    const uint64_t* dims = w.dims.data();
+    double* h = w.hst.as<double>();
+    int* hf = reinterpret_cast<int*>(h + 60);
+    double* norms = w.dotv + 8;  // d <= 16 entries
+    R1_CUDA(cudaMemcpyAsync(w.U, u0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+
+    // ||A||_F for the kkt rule (solvers.cpp:305, 108)
+    double a_norm = 0.0;
+    if (o.stop_rule == R1_STOP_KKT) {
+        sumsq_device(ctx, w.A->dev, numel_of(dims, d), w.dotv);
+        w.fetch(h, w.dotv, 1);
+        w.sync();
+        a_norm = std::sqrt(h[0]);
+    }
+    struct Sweep {
+        int iter;
+        cudaEvent_t a, b;
+    };
+    std::vector<Sweep> sweeps;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> marks;
+    auto sweep = [&](int iter) {
+        cudaEvent_t a = ev.rec(st);
+        w.sweep(w.U, w.J, w.fro2);
+        sweeps.push_back({iter, a, ev.rec(st)});
+        rr.sweeps += 1;
+    };
+    // y = J(u) xhat: the leave-one-out vectors of the current factors
+    auto loo_eval = [&](int iter) {
+        sweep(iter);
+        split_stack(ctx, dims, d, w.U, nullptr, w.Xhat, nullptr);
+        block_matvec(ctx, dims, d, w.J, w.Xhat, w.Y);
+    };
+    // loo_eval + lambda, Eq. 11 (mu = lambda of the iteration) and KKT
+    auto full_eval = [&](int iter, const double* mu_dev) {
+        loo_eval(iter);
+        if (mu_dev)
+            r1::post_step(ctx, dims, d, w.Y, w.Xhat, w.U, w.fro2, mu_dev, 0.0, w.post);
+        else
+            post_step_self(ctx, dims, d, w.Y, w.Xhat, w.U, w.fro2, w.post);
+    };
+
+    full_eval(0, nullptr);
+    w.fetch(h, w.post, 5);
+    w.sync();
+    rr.lambda0 = h[4];  // multilinear_value(a, u) (solvers.cpp:303)
+    double lambda_prev = rr.lambda0;
+    const char* what = kind == Baseline::hopm          ? "hopm: zero contraction vector"
+                       : kind == Baseline::jacobi_hopm ? "jacobi_hopm: zero contraction vector"
+                                                       : "asvd: singular vector block collapsed to zero";
+    std::vector<uint64_t> dims2(2);
+
+    for (int k = 1; k <= o.max_iters; ++k) {
+        r1_iteration_record rec{};
+        rec.lambda_pre_rqi = kNan;
+        cudaEvent_t t0 = ev.rec(st);
+        const size_t nsw0 = sweeps.size();
+        double lambda = 0.0;
+        switch (kind) {
+            case Baseline::hopm:
+                // Gauss-Seidel: mode n contracts against the already-updated 0..n-1
+                for (int m = 0; m < d; ++m) {
+                    if (m > 0) loo_eval(k);
+                    loo_update(ctx, dims, d, w.Y, w.U, m, m + 1, norms, w.flags, m > 0);
+                }
+                // lambda = ||w_{d-1}|| (solvers.cpp:329)
+                full_eval(k, norms + d - 1);
+                break;
+            case Baseline::jacobi_hopm:
+                loo_update(ctx, dims, d, w.Y, w.U, 0, d, norms, w.flags, false);
+                full_eval(k, nullptr);  // lambda = multilinear_value at the new u (:321)
+                break;
+            case Baseline::asvd:
+            case Baseline::jacobi_asvd: {
+                const bool jacobi = kind == Baseline::jacobi_asvd;
+                std::vector<char> dirty(d, 0);
+                bool first = true;
+                for (auto [m, nn] : asvd_pairs(d, o.asvd_disjoint_pairs != 0, k)) {
+                    if (!jacobi) {
+                        bool stale = false;
+                        for (int q = 0; q < d; ++q) stale |= dirty[q] && q != m && q != nn;
+                        if (stale) {
+                            sweep(k);
+                            std::fill(dirty.begin(), dirty.end(), 0);
+                        }
+                    }
+                    dims2[0] = dims[m];
+                    dims2[1] = dims[nn];
+                    eig_blocks(ctx, dims2.data(), 2, w.J + block_offset(dims, d, m, nn), nullptr,
+                               w.mu, w.X, nullptr, nullptr);
+                    asvd_take(ctx, dims, d, m, nn, w.X, w.mu, w.U, w.flags, !first);
+                    dirty[m] = dirty[nn] = 1;
+                    first = false;
+                }
+                full_eval(k, nullptr);  // lambda = multilinear_value (:423)
+                break;
+            }
+        }
+        w.fetch(h, w.post, 5);
+        w.fetch(h + 8, norms, d);
+        w.fetch(hf, w.flags, 1);
+        w.sync();
+        if (hf[0]) throw Degenerate(what);
+        lambda = kind == Baseline::hopm ? h[8 + d - 1] : h[4];
+        // baseline_stop (solvers.cpp:100-127)
+        const double kkt_max = h[2];
+        switch (o.stop_rule) {
+            case R1_STOP_EQ11:
+                rec.eq11_value = h[1];
+                rec.stop_value = h[1];
+                rec.kkt_max_residual = o.record_kkt ? kkt_max : kNan;
+                break;
+            case R1_STOP_LAMBDA_DELTA:
+                rec.eq11_value = kNan;
+                rec.stop_value = std::abs(lambda - lambda_prev) / std::max(std::abs(lambda), 1e-300);
+                rec.kkt_max_residual = o.record_kkt ? kkt_max : kNan;
+                break;
+            default:
+                rec.eq11_value = kNan;
+                rec.kkt_max_residual = kkt_max;
+                rec.stop_value = kkt_max / std::max(a_norm, 1e-300);
+                break;
+        }
+        rec.lambda = lambda;
+        rec.n_sweeps = static_cast<int>(sweeps.size() - nsw0);
+        lambda_prev = lambda;
+        marks.emplace_back(t0, ev.rec(st));
+        rr.trace.push_back(rec);
+        rr.iterations = k;
+        if (rec.stop_value <= o.tol) {
+            rr.converged = true;
+            break;
+        }
+    }
+    // finalize_sign (solvers.cpp:70-76) with lambda of the last evaluation
+    double lam = h[4];
+    rr.factors.resize(n);
+    w.fetch(rr.factors.data(), w.U, n);
+    w.sync();
+    if (lam < 0.0) {
+        lam = -lam;
+        for (uint64_t i = 0; i < w.dims[0]; ++i) rr.factors[i] = -rr.factors[i];
+    }
+    rr.lambda = lam;
+    // device sweep time per iteration -> t_build_j, the rest -> t_other
+    for (size_t k = 0; k < marks.size(); ++k) {
+        auto& r = rr.trace[k];
+        double tb = 0.0;
+        for (const auto& s : sweeps)
+            if (s.iter == static_cast<int>(k) + 1) tb += Events::secs(s.a, s.b);
+        r.t_build_j = tb;
+        r.t_eig = 0.0;
+        r.t_other = std::max(0.0, Events::secs(marks[k].first, marks[k].second) - tb);
+    }
+    return rr;
+}
+
 std::vector<double> initial_factors(const r1_tensor* a, const r1_solve_options& o) {
     const int d = static_cast<int>(a->dims.size());
     if (o.init == R1_INIT_PROVIDED) {
@@ -392,9 +582,10 @@ int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         const std::string alg = algorithm ? algorithm : "";
-        if (alg == "hopm" || alg == "jacobi_hopm" || alg == "asvd" || alg == "jacobi_asvd")
-            fail(R1_ERR_INVALID_ARGUMENT, "solver " + alg + " is not on the device path");
-        if (alg != "hoscf" && alg != "ihoscf") fail(R1_ERR_INVALID_ARGUMENT, "unknown solver: " + alg);
+        const bool baseline =
+            alg == "hopm" || alg == "jacobi_hopm" || alg == "asvd" || alg == "jacobi_asvd";
+        if (alg != "hoscf" && alg != "ihoscf" && !baseline)
+            fail(R1_ERR_INVALID_ARGUMENT, "unknown solver: " + alg);
         if (!a || !opts || !report) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         // validate (solvers.cpp:28-32)
         if (a->dims.size() < 2) fail(R1_ERR_INVALID_ARGUMENT, "solver: tensor order must be >= 2");
@@ -405,11 +596,18 @@ int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
         Work& w = work_for(ctx, a, acc);
         RunResult rr;
         bool restarted = false;
+        const Baseline bk = alg == "hopm"          ? Baseline::hopm
+                            : alg == "jacobi_hopm" ? Baseline::jacobi_hopm
+                            : alg == "asvd"        ? Baseline::asvd
+                                                   : Baseline::jacobi_asvd;
+        auto go = [&](const std::vector<double>& u0) {
+            return baseline ? run_baseline(w, *opts, u0, bk) : run(w, *opts, u0, acc);
+        };
         try {
-            rr = run(w, *opts, initial_factors(a, *opts), acc);
+            rr = go(initial_factors(a, *opts));
         } catch (const Degenerate&) {
             try {
-                rr = run(w, *opts, random_unit_factors(a->dims, opts->seed, kStreamRestart), acc);
+                rr = go(random_unit_factors(a->dims, opts->seed, kStreamRestart));
                 restarted = true;
             } catch (const Degenerate& e) {
                 fail(R1_ERR_RUNTIME, std::string("solver failed after restart: ") + e.what());
@@ -422,8 +620,11 @@ int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
         report->iterations = rr.iterations;
         report->lambda0 = rr.lambda0;
         report->restarted = restarted ? 1 : 0;
-        if (report->final_x)
+        // baselines: final_x stays empty (solvers.hpp:56), reported as zeros
+        if (report->final_x) {
+            std::memset(report->final_x, 0, rr.factors.size() * sizeof(double));
             std::memcpy(report->final_x, rr.final_x.data(), rr.final_x.size() * sizeof(double));
+        }
         for (int i = 0; i < rr.iterations; ++i) report->trace[i] = rr.trace[i];
         report->total_sweeps = rr.sweeps;
         report->t_total = std::chrono::duration<double>(t1 - t0).count();

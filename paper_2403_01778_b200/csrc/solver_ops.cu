@@ -89,7 +89,6 @@ __global__ void post_kernel(Dims dm, const double* __restrict__ y, const double*
     }
     const double res = sqrt(block_reduce_sum(s, sh));
     const double fro = sqrt(2.0 * fro2[0]) / static_cast<double>(dm.d - 1);
-    const double mu = use_mu_dev ? mu_dev[0] : mu_host;
     const double sqd = sqrt(static_cast<double>(dm.d));
     // lambda = u_0' w_0
     s = 0.0;
@@ -106,6 +105,9 @@ __global__ void post_kernel(Dims dm, const double* __restrict__ y, const double*
         if (threadIdx.x == 0) out[5 + k] = rk;
         mx = fmax(mx, rk);
     }
+    // mu: the eigenvalue (device / host) or, for the sweep baselines, the
+    // full contraction lambda of these factors (baseline_stop, solvers.cpp:112-118)
+    const double mu = use_mu_dev == 1 ? mu_dev[0] : (use_mu_dev == 2 ? lam : mu_host);
     if (threadIdx.x == 0) {
         out[0] = rho;
         out[1] = res / (fro + fabs(mu));
@@ -113,6 +115,62 @@ __global__ void post_kernel(Dims dm, const double* __restrict__ y, const double*
         out[3] = fro;
         out[4] = lam;
     }
+}
+
+// Leave-one-out update of the power sweeps (solvers.cpp:316-331): for the
+// modes k in [lo, hi), w_k = sqrt(d) y_k = A x_{-k} u, u_k = w_k / ||w_k||
+// (normalize, matrix.cpp:62-67), norms[k] = ||w_k||, degenerate below 1e-300.
+__global__ void loo_update_kernel(Dims dm, const double* __restrict__ y, double* __restrict__ u,
+                                  int lo, int hi, double* __restrict__ norms,
+                                  int* __restrict__ flags, int accumulate) {
+    __shared__ double sh[32];
+    const double sqd = sqrt(static_cast<double>(dm.d));
+    int deg = 0;
+    for (int k = lo; k < hi; ++k) {
+        const int64_t o = dm.offs[k], len = dm.offs[k + 1] - dm.offs[k];
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const double v = sqd * y[o + i];
+            s = fma(v, v, s);
+        }
+        const double nrm = sqrt(block_reduce_sum(s, sh));
+        deg |= nrm < 1e-300 ? 1 : 0;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const double v = sqd * y[o + i];
+            u[o + i] = nrm > 0.0 ? v / nrm : v;
+        }
+        if (threadIdx.x == 0) norms[k] = nrm;
+    }
+    if (threadIdx.x == 0) flags[0] = (accumulate ? flags[0] : 0) | deg;
+}
+
+// ASVD pair update (top_singular_pair, solvers.cpp:358-381): x = the
+// largest-magnitude eigenvector of [[0,B],[B',0]] (rows I_m then I_n); a
+// negative eigenvalue flips the right block; both blocks are normalised
+// (degenerate below 1e-12) into u_m, u_n.
+__global__ void asvd_take_kernel(Dims dm, int m, int n, const double* __restrict__ x,
+                                 const double* __restrict__ value, double* __restrict__ u,
+                                 int* __restrict__ flags, int accumulate) {
+    __shared__ double sh[32];
+    const int64_t lm = dm.offs[m + 1] - dm.offs[m], ln = dm.offs[n + 1] - dm.offs[n];
+    const double sgn = value[0] < 0.0 ? -1.0 : 1.0;
+    int deg = 0;
+    for (int part = 0; part < 2; ++part) {
+        const int64_t len = part ? ln : lm, src = part ? lm : 0, dst = dm.offs[part ? n : m];
+        const double f = part ? sgn : 1.0;
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const double v = f * x[src + i];
+            s = fma(v, v, s);
+        }
+        const double nrm = sqrt(block_reduce_sum(s, sh));
+        deg |= nrm < 1e-12 ? 1 : 0;
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const double v = f * x[src + i];
+            u[dst + i] = nrm > 0.0 ? v / nrm : v;
+        }
+    }
+    if (threadIdx.x == 0) flags[0] = (accumulate ? flags[0] : 0) | deg;
 }
 
 __global__ void dense_kernel(const BlockOp* __restrict__ opp, double* __restrict__ S) {
@@ -278,6 +336,27 @@ void post_step(r1_context* ctx, const uint64_t* dims, int order, const double* y
     post_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(make_dims(dims, order), y, xhat, u, fro2_dev,
                                                    mu_dev, mu_host, mu_dev ? 1 : 0, out_dev);
     check_launch(ctx, "post_kernel");
+}
+
+void post_step_self(r1_context* ctx, const uint64_t* dims, int order, const double* y,
+                    const double* xhat, const double* u, const double* fro2_dev, double* out_dev) {
+    post_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(make_dims(dims, order), y, xhat, u, fro2_dev,
+                                                   nullptr, 0.0, 2, out_dev);
+    check_launch(ctx, "post_kernel");
+}
+
+void loo_update(r1_context* ctx, const uint64_t* dims, int order, const double* y, double* u,
+                int lo, int hi, double* norms_dev, int* flags_dev, bool accumulate) {
+    loo_update_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(make_dims(dims, order), y, u, lo, hi,
+                                                         norms_dev, flags_dev, accumulate ? 1 : 0);
+    check_launch(ctx, "loo_update_kernel");
+}
+
+void asvd_take(r1_context* ctx, const uint64_t* dims, int order, int m, int n, const double* x,
+               const double* value_dev, double* u, int* flags_dev, bool accumulate) {
+    asvd_take_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(make_dims(dims, order), m, n, x, value_dev,
+                                                        u, flags_dev, accumulate ? 1 : 0);
+    check_launch(ctx, "asvd_take_kernel");
 }
 
 void flip_first(r1_context* ctx, double* u0, int64_t n0, const double* lam_in, double* lam_out) {

@@ -13,6 +13,13 @@ void split_stack(r1_context* ctx, const uint64_t* dims, int order, const double*
 void post_step(r1_context* ctx, const uint64_t* dims, int order, const double* y,
                const double* xhat, const double* u, const double* fro2_dev, const double* mu_dev,
                double mu_host, double* out_dev);
+// post_step with mu = the full contraction lambda it computes (baselines)
+void post_step_self(r1_context* ctx, const uint64_t* dims, int order, const double* y,
+                    const double* xhat, const double* u, const double* fro2_dev, double* out_dev);
+void loo_update(r1_context* ctx, const uint64_t* dims, int order, const double* y, double* u,
+                int lo, int hi, double* norms_dev, int* flags_dev, bool accumulate);
+void asvd_take(r1_context* ctx, const uint64_t* dims, int order, int m, int n, const double* x,
+               const double* value_dev, double* u, int* flags_dev, bool accumulate);
 void flip_first(r1_context* ctx, double* u0, int64_t n0, const double* lam_in, double* lam_out);
 void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                        double* S);

@@ -115,7 +115,7 @@ int main() {
         CHECK(threw);
     }
     // hoscf / ihoscf vs the reference (tolerances of the north star)
-    for (const char* alg : {"hoscf", "ihoscf"}) {
+    for (const char* alg : {"hoscf", "ihoscf", "hopm", "jacobi_asvd"}) {
         std::vector<std::size_t> dims{7, 5, 9};
         DenseTensor a = gaussian(dims, 11);
         SolveOptions o;
@@ -140,11 +140,18 @@ int main() {
         CHECK(rep.result.lambda >= 0.0);
         CHECK(static_cast<int>(rep.trace.size()) == rep.iterations);
     }
-    // baselines are not on the device path
+    // the named baseline entry points (solvers.hpp:70-83) run on the device too
     {
+        DenseTensor a = gaussian({6, 5, 4}, 2);
+        SolveOptions o;
+        o.tol = 1e-10;
+        const SolveReport h = hopm(a, o), j = jacobi_hopm(a, o), s = asvd(a, o), t = jacobi_asvd(a, o);
+        CHECK(h.algorithm == "hopm" && j.algorithm == "jacobi_hopm");
+        CHECK(s.algorithm == "asvd" && t.algorithm == "jacobi_asvd");
+        CHECK(h.final_x.total_dim() == 0 && h.result.lambda >= 0.0);
         bool threw = false;
         try {
-            solve("hopm", gaussian({3, 3}, 1), SolveOptions{});
+            solve("nope", a, o);
         } catch (const std::invalid_argument&) {
             threw = true;
         }

@@ -13,7 +13,7 @@ import pytest
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
 
-from golden.gen_golden import SOLVES, SWEEP_SHAPES, solve_input  # noqa: E402
+from golden.gen_golden import BASELINE_SOLVES, SOLVES, SWEEP_SHAPES, solve_input  # noqa: E402
 
 
 def tag(dims):
@@ -105,6 +105,35 @@ def test_oracle_solvers_vs_reference(oracle, case):
     assert abs(rep.iterations - it_ref) <= (3 if chaotic else 1)
     assert abs(rep.lam - lam_ref) <= 1e-10 * abs(lam_ref)
     assert abs(rep.lambda0 - meta[3]) <= 1e-12 * max(1.0, abs(meta[3]))
+    if rep.iterations == it_ref:
+        fac = GOLD[f"solve_{name}_factors"]
+        o = 0
+        for u in rep.factors:
+            v = fac[o:o + len(u)]
+            o += len(u)
+            assert min(np.max(np.abs(u - v)), np.max(np.abs(u + v))) <= 1e-8
+
+
+@pytest.mark.parametrize("case", BASELINE_SOLVES, ids=[c[0] for c in BASELINE_SOLVES])
+def test_oracle_baselines_vs_reference(oracle, case):
+    """The numpy restatement of run_power_sweep / run_asvd (solvers.cpp:299-447)
+    against the reference's own runs (golden): sigma 1e-10, factors 1e-8 up to
+    sign, iterations +-1, per-iteration lambda trace 1e-9."""
+    name, alg, kind, dims, tol, iters, seed, rule, disjoint = case
+    a = solve_input(kind, dims, seed)
+    rep = getattr(oracle, alg)(a, dims, oracle.Options(
+        tol=tol, max_iters=iters, seed=seed, stop_rule=["kkt", "eq11", "lambda_delta"][rule],
+        asvd_disjoint_pairs=disjoint))
+    meta = GOLD[f"solve_{name}_meta"]
+    lam_ref, conv_ref, it_ref = meta[0], bool(meta[1]), int(meta[2])
+    assert rep.converged == conv_ref
+    assert abs(rep.iterations - it_ref) <= 1, (rep.iterations, it_ref)
+    assert abs(rep.lam - lam_ref) <= 1e-10 * abs(lam_ref)
+    assert abs(rep.lambda0 - meta[3]) <= 1e-12 * max(1.0, abs(meta[3]))
+    lt = GOLD[f"solve_{name}_lambda_trace"]
+    k = min(len(lt), len(rep.trace))
+    got = np.array([t["lambda"] for t in rep.trace[:k]])
+    assert np.max(np.abs(got - lt[:k])) <= 1e-9 * np.max(np.abs(lt))
     if rep.iterations == it_ref:
         fac = GOLD[f"solve_{name}_factors"]
         o = 0

@@ -161,5 +161,5 @@ def test_solver_validation(gpu_ctx):
         r1.hoscf(a, r1.SolveOptions(max_iters=0))
     with pytest.raises(ValueError, match="unknown solver"):
         r1.solve("nope", a, r1.SolveOptions())
-    with pytest.raises(ValueError, match="not on the device path"):
-        r1.solve("hopm", a, r1.SolveOptions())
+    with pytest.raises(ValueError, match="tol must be > 0"):
+        r1.solve("hopm", a, r1.SolveOptions(tol=0.0))
