@@ -61,6 +61,10 @@ struct Seg {
 struct SweepArgs {
     const double* A;
     int64_t I0, I1, O;
+    // box kernel: merged-column view (alignment classes, see tile_level):
+    // M[r, c, o] = A[r mod I0, K c + r / I0, o], MI0 = K I0 rows, MI1 = I1 / K
+    int K;
+    int64_t MI0, MI1;
     const double* u0;
     const double* u1;
     const double* W;
@@ -399,10 +403,11 @@ struct BoxMaps {
 // keeps the same volume in flight — in a saturated memory system an SM's share
 // of bandwidth follows its bytes in flight.  The consumer thread grid is fixed
 // (RMAX x CMAX); rows/columns beyond the tile read finite neighbours (the ring
-// is zeroed once) and carry zero weights, and are never stored.  Lane l owns
-// rows 64p + 2l + {0,1} (one 128-bit LDS per pair), warp w owns columns
-// w + NWC*b.  Each thread copies its slice to registers and releases the
-// stage before computing.
+// is zeroed once) and carry zero weights, and are never stored.  Tiles live in
+// the merged-column view (alignment classes, tile_level): lane l owns the NRA
+// consecutive merged rows NRA*l.. (NRA/2 128-bit LDS), all in one class, warp
+// w owns columns w + NWC*b.  Each thread copies its slice to registers and
+// releases the stage before computing.
 template <int NRA, int NCB, int NWC, bool STAGE_REGS>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     sweep3_box_kernel(const SweepArgs p, const __grid_constant__ BoxMaps maps, int nst,
@@ -421,6 +426,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // A lane's NRA rows are NP 16-B pairs at byte offset 32*lane: lanes l and
+    // l+4 of a quarter warp would hit the same banks, so odd quarter-lanes take
+    // their pairs in swapped order (pair slot q holds pair q ^ hsw).
+    const int hsw = NP > 1 ? (lane >> 2) & 1 : 0;
     for (int i = threadIdx.x; i < ring_dbl / 2; i += blockDim.x)
         reinterpret_cast<double2*>(ring)[i] = make_double2(0.0, 0.0);
     if (threadIdx.x == 0) {
@@ -435,10 +444,12 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
 
     const int seg_begin = p.cta_seg[blockIdx.x];
     const int seg_end = p.cta_seg[blockIdx.x + 1];
-    const int64_t I0 = p.I0, I1 = p.I1;
-    const int G1 = static_cast<int>((I1 + p.t1 - 1) / p.t1);
-    const int rem0 = static_cast<int>(I0 - static_cast<int64_t>(p.G0 - 1) * p.r0);
-    const int rem1 = static_cast<int>(I1 - static_cast<int64_t>(G1 - 1) * p.t1);
+    const int64_t I0 = p.I0, I1 = p.I1;      // real extents
+    const int64_t MI0 = p.MI0, MI1 = p.MI1;  // merged view (tiles live here)
+    const int K = p.K;
+    const int G1 = static_cast<int>((MI1 + p.t1 - 1) / p.t1);
+    const int rem0 = static_cast<int>(MI0 - static_cast<int64_t>(p.G0 - 1) * p.r0);
+    const int rem1 = static_cast<int>(MI1 - static_cast<int64_t>(G1 - 1) * p.t1);
 
     // Schedule (producer-driven): the static segments [seg_begin, seg_end) of
     // this CTA, then chunks of the dynamic tail taken from a work counter by
@@ -497,6 +508,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     int rbuf = 0;
     int s = -1;
     int g0 = 0, g1 = 0, r0e = 0, t1e = 0, cst = 0;
+    int pcls = 0, cls_lo = 0, cls_hi = 0;  // alignment class of this thread's rows / the tile's
     int64_t R0s = 0, R1s = 0;
     double u0r[NRA], u1c[NCB];
     double acc[NRA][NCB];
@@ -515,21 +527,27 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             g1 = tile / p.G0;
             R0s = static_cast<int64_t>(g0) * p.r0;
             R1s = static_cast<int64_t>(g1) * p.t1;
-            r0e = static_cast<int>(min64(p.r0, I0 - R0s));
-            t1e = static_cast<int>(min64(p.t1, I1 - R1s));
+            r0e = static_cast<int>(min64(p.r0, MI0 - R0s));
+            t1e = static_cast<int>(min64(p.t1, MI1 - R1s));
             cst = r0e;  // smem column stride (doubles) = box rows
+            // lane owns NRA consecutive merged rows; I0 % NRA == 0 keeps them in
+            // one alignment class (one real column per merged column)
+            cls_lo = static_cast<int>(R0s / I0);
+            cls_hi = static_cast<int>((R0s + r0e - 1) / I0);
+            const int lr = NRA * lane;
+            const bool live = lr < r0e;
+            pcls = live ? static_cast<int>((R0s + lr) / I0) : cls_hi;
+            const int64_t i0s = R0s + lr - static_cast<int64_t>(pcls) * I0;
 #pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int i = 64 * q + 2 * lane + h;
-                    u0r[2 * q + h] = i < r0e ? __ldg(p.u0 + R0s + i) : 0.0;
-                }
+            for (int a = 0; a < NRA; ++a) {
+                const int off = 2 * ((a >> 1) ^ hsw) + (a & 1);
+                u0r[a] = lr + off < r0e ? __ldg(p.u0 + i0s + off) : 0.0;
+            }
 #pragma unroll
             for (int b = 0; b < NCB; ++b) {
                 const int j = warp + NWC * b;
-                u1c[b] = j < t1e ? __ldg(p.u1 + R1s + j) : 0.0;
-                coff[b] = (min(j, t1e - 1) * cst) / 2 + lane;
+                u1c[b] = (j < t1e && live) ? __ldg(p.u1 + K * (R1s + j) + pcls) : 0.0;
+                coff[b] = (min(j, t1e - 1) * cst) / 2 + (NRA / 2) * lane;
 #pragma unroll
                 for (int a = 0; a < NRA; ++a) acc[a][b] = 0.0;
             }
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
 #pragma unroll
                 for (int b = 0; b < NCB; ++b)
 #pragma unroll
-                    for (int q = 0; q < NP; ++q) v[b][q] = st[coff[b] + 32 * q];
+                    for (int q = 0; q < NP; ++q) v[b][q] = st[coff[b] + (q ^ hsw)];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
 #pragma unroll
@@ -581,7 +599,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 for (int b = 0; b < NCB; ++b) {
                     double2 v[NP];
 #pragma unroll
-                    for (int q = 0; q < NP; ++q) v[q] = st[coff[b] + 32 * q];
+                    for (int q = 0; q < NP; ++q) v[q] = st[coff[b] + (q ^ hsw)];
                     column(b, v);
                 }
                 __syncwarp();
@@ -592,23 +610,40 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 phase ^= 1;
             }
 
-            int col;
-            const double c1 = warp_transpose_sum<NCB>(c1v, lane, &col);
-            if (P1row && (lane & (32 / NCB - 1)) == 0) {
-                const int j = warp + NWC * col;
-                if (j < t1e) P1row[static_cast<int64_t>(o) * I1 + j] = c1;
+            if (P1row) {
+                // C1 of merged column j, class c = real column K j + c, stored
+                // class-major (c MI1 + j) so the second stage reads only the
+                // classes a row tile holds; a tile spanning several classes
+                // reduces each class's lanes separately
+                double* dst = P1row + static_cast<int64_t>(o) * I1;
+                int col;
+                if (cls_lo == cls_hi) {
+                    const double c1 = warp_transpose_sum<NCB>(c1v, lane, &col);
+                    const int j = warp + NWC * col;
+                    if ((lane & (32 / NCB - 1)) == 0 && j < t1e) dst[cls_lo * MI1 + j] = c1;
+                } else {
+                    for (int c = cls_lo; c <= cls_hi; ++c) {
+                        double mv[NCB];
+#pragma unroll
+                        for (int b = 0; b < NCB; ++b) mv[b] = pcls == c ? c1v[b] : 0.0;
+                        const double c1 = warp_transpose_sum<NCB>(mv, lane, &col);
+                        const int j = warp + NWC * col;
+                        if ((lane & (32 / NCB - 1)) == 0 && j < t1e) dst[c * MI1 + j] = c1;
+                    }
+                }
             }
 
-            double2* rb = reinterpret_cast<double2*>(red + rbuf * NWC * RMAX + warp * RMAX) + lane;
+            double2* rb =
+                reinterpret_cast<double2*>(red + rbuf * NWC * RMAX + warp * RMAX) + (NRA / 2) * lane;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) rb[32 * q] = make_double2(c0p[2 * q], c0p[2 * q + 1]);
+            for (int q = 0; q < NP; ++q) rb[q ^ hsw] = make_double2(c0p[2 * q], c0p[2 * q + 1]);
             asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory");
             const double* rr = red + rbuf * NWC * RMAX;
             for (int i = threadIdx.x; i < r0e; i += NWC * 32) {
                 double sum = 0.0;
 #pragma unroll
                 for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX + i];
-                P0row[static_cast<int64_t>(o) * I0 + i] = sum;
+                P0row[static_cast<int64_t>(o) * MI0 + i] = sum;
             }
             rbuf ^= 1;
             if (md.w & kLast) {
@@ -619,10 +654,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                     const int j = warp + NWC * b;
                     if (j >= t1e) continue;
 #pragma unroll
-                    for (int q = 0; q < NP; ++q) {
-                        const int i = 64 * q + 2 * lane;
-                        if (i < r0e) dst[j * p.r0 + i] = acc[2 * q][b];
-                        if (i + 1 < r0e) dst[j * p.r0 + i + 1] = acc[2 * q + 1][b];
+                    for (int a = 0; a < NRA; ++a) {
+                        const int i = NRA * lane + 2 * ((a >> 1) ^ hsw) + (a & 1);
+                        if (i < r0e) dst[j * p.r0 + i] = acc[a][b];
                     }
                 }
             }
@@ -639,32 +673,112 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     }
 }
 
-// out[i] = sum_{c<K} in[c*stride + i], fixed order.
-__global__ void reduce_copies_kernel(const double* __restrict__ in, int64_t stride, int K,
-                                     int64_t n, double* __restrict__ out) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double s = in[i];
-        for (int c = 1; c < K; ++c) s += in[c * stride + i];
-        out[i] = s;
+// Second stage of one level, all outputs in one launch, every sum in a fixed
+// order (bit-reproducible for any schedule of the first stage):
+//   B01[i0 + I0 i1] = sum over the tile's segments (o order) of P01 partials;
+//       tiles live in the merged view: (i0, i1) is merged row (i1 mod K) I0 + i0
+//       of merged column i1 / K;
+//   C0[i0 + I0 o]   = sum_{g1 < G1} sum_{p < K} P0[g1 stride0 + o K I0 + p I0 + i0];
+//   C1[i1 + I1 o]   = sum over the row tiles g0 holding class p = i1 mod K
+//       (merged rows [p I0, (p+1) I0)) of P1[g0 stride1 + o I1 + p MI1 + i1 / K].
+// A null P0 / P1 means the first stage wrote that output in place.
+struct FinishArgs {
+    const double* P01;
+    const int* tile_seg;
+    int64_t I0, I1, O, MI1;
+    int K, lgK, r0, t1, G0, G1;
+    double* b01;
+    const double* P0;
+    int64_t stride0;
+    double* c0;
+    const double* P1;
+    int64_t stride1;
+    double* c1;
+    int64_t n_b01, n_c0, n_c1;
+};
+
+// Element per thread.  With K == 1 the C0 / C1 partial copies have the output
+// layout (a plain sum of copies); K is a power of two.  IDX is the index type
+// (32-bit whenever the level's element counts allow).
+template <typename IDX>
+__global__ void finish_kernel(const FinishArgs f) {
+    const IDX nb = static_cast<IDX>(f.n_b01), n0 = static_cast<IDX>(f.n_c0);
+    const IDX total = nb + n0 + static_cast<IDX>(f.n_c1);
+    const IDX I0 = static_cast<IDX>(f.I0), I1 = static_cast<IDX>(f.I1);
+    const int K = f.K;
+    const int64_t tile_elems = static_cast<int64_t>(f.r0) * f.t1;
+    for (IDX e = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<IDX>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        if (e < nb) {
+            const IDX i1 = e / I0, i0 = e - i1 * I0;
+            const IDX p = i1 & (K - 1), c = i1 >> f.lgK;
+            const IDX r = p * I0 + i0;
+            const int g0 = static_cast<int>(r / f.r0), g1 = static_cast<int>(c / f.t1);
+            const int tile = g0 + f.G0 * g1;
+            const double* src = f.P01 + static_cast<int64_t>(c - static_cast<IDX>(g1) * f.t1) * f.r0 +
+                                (r - static_cast<IDX>(g0) * f.r0);
+            const int sb = __ldg(f.tile_seg + tile), se = __ldg(f.tile_seg + tile + 1);
+#pragma unroll 4
+            for (int k = sb; k < se; ++k) s += __ldcs(src + k * tile_elems);
+            f.b01[e] = s;
+        } else if (e < nb + n0) {
+            const IDX x = e - nb;
+            if (K == 1) {
+                const double* src = f.P0 + x;
+#pragma unroll 6
+                for (int g = 0; g < f.G1; ++g) s += __ldcs(src + g * f.stride0);
+            } else {
+                const IDX o = x / I0, i0 = x - o * I0;
+                const double* src = f.P0 + static_cast<int64_t>(o) * K * f.I0 + i0;
+                for (int g = 0; g < f.G1; ++g)
+#pragma unroll 4
+                    for (int q = 0; q < K; ++q) s += __ldcs(src + g * f.stride0 + q * f.I0);
+            }
+            f.c0[x] = s;
+        } else {
+            const IDX x = e - nb - n0;
+            if (K == 1) {
+                const double* src = f.P1 + x;
+#pragma unroll 4
+                for (int g = 0; g < f.G0; ++g) s += __ldcs(src + g * f.stride1);
+            } else {
+                const IDX o = x / I1, i1 = x - o * I1;
+                const int p = static_cast<int>(i1 & (K - 1));
+                const int ga = static_cast<int>(p * f.I0 / f.r0);
+                const int gb = static_cast<int>(((p + 1) * f.I0 - 1) / f.r0);
+                const double* src = f.P1 + static_cast<int64_t>(o) * f.I1 + p * f.MI1 + (i1 >> f.lgK);
+#pragma unroll 4
+                for (int g = ga; g <= gb; ++g) s += __ldcs(src + g * f.stride1);
+            }
+            f.c1[x] = s;
+        }
     }
 }
 
-// B01[i0 + I0*i1] = sum over the tile's segments (in o order) of P01 partials.
-__global__ void reduce_b01_kernel(const double* __restrict__ P01, const int* __restrict__ tile_seg,
-                                  int64_t I0, int64_t I1, int r0, int t1, int G0,
-                                  double* __restrict__ out) {
-    const int64_t n = I0 * I1;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i0 = e % I0, i1 = e / I0;
-        const int g0 = static_cast<int>(i0 / r0), g1 = static_cast<int>(i1 / t1);
-        const int tile = g0 + G0 * g1;
-        const int64_t local = (i1 - static_cast<int64_t>(g1) * t1) * r0 + (i0 - int64_t(g0) * r0);
-        const int sb = tile_seg[tile], se = tile_seg[tile + 1];
+// B01 when tiles hold many segments (deep o ranges split over many CTAs, e.g.
+// a single 60 x 60 face tile): a warp per element, lanes over the segments,
+// then a fixed-pattern butterfly — still one fixed summation order.
+__global__ void finish_b01_warp_kernel(const FinishArgs f) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tile_elems = static_cast<int64_t>(f.r0) * f.t1;
+    const int K = f.K;
+    for (int64_t e = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+         e < f.n_b01; e += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const int64_t i1 = e / f.I0, i0 = e - i1 * f.I0;
+        const int64_t p = i1 & (K - 1), c = i1 >> f.lgK;
+        const int64_t r = p * f.I0 + i0;
+        const int g0 = static_cast<int>(r / f.r0), g1 = static_cast<int>(c / f.t1);
+        const int tile = g0 + f.G0 * g1;
+        const double* src = f.P01 + (c - static_cast<int64_t>(g1) * f.t1) * f.r0 +
+                            (r - static_cast<int64_t>(g0) * f.r0);
+        const int sb = __ldg(f.tile_seg + tile), se = __ldg(f.tile_seg + tile + 1);
         double s = 0.0;
-        for (int k = sb; k < se; ++k) s += P01[static_cast<int64_t>(k) * r0 * t1 + local];
-        out[e] = s;
+#pragma unroll 4
+        for (int k = sb + lane; k < se; k += 32) s += __ldcs(src + k * tile_elems);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) f.b01[e] = s;
     }
 }
 
@@ -706,6 +820,8 @@ struct Level {
     Ref input;
     // view & tiling
     int64_t I0 = 0, I1 = 0, O = 0;
+    int K = 1;                 // alignment classes merged per column (box kernel)
+    int64_t MI0 = 0, MI1 = 0;  // merged view K I0 x I1/K (tiles live here)
     int nra = 4, ncb = 8, stages = 3;
     int stage_dbl = 0;
     int dyn_first = 0, ndyn = 0;  // dynamic-tail segments (box kernel only)
@@ -739,6 +855,32 @@ size_t smem_bytes(int nra, int ncb, int stages, bool tma) {
            static_cast<size_t>(2) * kNWC * rmax * 8 + 2 * stages * 8;
 }
 
+// Alignment classes.  TMA moves whole 128-B lines: a box row that starts or
+// ends inside a line fetches the full line, and the neighbouring tile fetches
+// it again (measured: 6.4% extra DRAM reads at I0 = 1000, whose 8000-B column
+// pitch puts every other column at a 64-B offset).  Columns whose start
+// offsets mod 128 B differ are "classes"; K consecutive columns (one of each
+// class) are merged into one column of K I0 rows, whose pitch is a multiple of
+// 128 B.  Row tiles of whole lines (r0 % 16 == 0) then never share a line.
+// The box kernel maps merged rows back to (i0, class): lane rows stay inside
+// one class because I0 % 4 == 0.
+int alignment_classes(const Level& L) {
+    // R1_SWEEP_MERGE: 0 never merge, 1 (default) when it keeps tiles full, 2 whenever legal
+    static const char* env = std::getenv("R1_SWEEP_MERGE");
+    const int mode = env ? std::atoi(env) : 1;
+    if (mode == 0) return 1;
+    if (!L.tma || L.I0 % 4 != 0) return 1;
+    const int64_t pitch = 8 * L.I0;
+    int64_t g = 128;
+    while (pitch % g) g >>= 1;
+    const int K = static_cast<int>(128 / g);
+    if (K == 1 || L.I1 % K != 0 || (8 * L.I0 * L.I1) % 128 != 0) return 1;
+    // Worth it only when the merged view keeps full tiles: a class fills at
+    // least one row tile and there are >= 4 full column tiles (I1 / K columns).
+    if (mode == 1 && (L.I0 < 128 || L.I1 / K < 4 * kBoxNWC * kBoxNCB)) return 1;
+    return K;
+}
+
 void tile_level(Level& L, int num_sms) {
     L.nra = L.I0 > 64 ? 4 : (L.I0 > 32 ? 2 : 1);
     L.ncb = 8;
@@ -746,24 +888,27 @@ void tile_level(Level& L, int num_sms) {
     // TMA needs 16-B global strides (I0 even) and an int32 outer coordinate.
     L.tma = (L.I0 % 2 == 0) && L.O < (int64_t(1) << 31) && L.I1 < (int64_t(1) << 31);
     L.smem = smem_bytes(L.nra, L.ncb, L.stages, L.tma);
+    L.K = alignment_classes(L);
+    L.MI0 = L.K * L.I0;
+    L.MI1 = L.I1 / L.K;
     const int rmax = 32 * L.nra, cmax = kNWC * L.ncb;
     // Balance row tiles: G0 = ceil(I0/rmax), r0 = ceil(I0/G0) (same for cols);
     // on the TMA path r0 is even so interior boxes hold exactly the tile.
     if (L.tma) {
-        // Balanced tiles on the fixed RMAX x CMAX consumer grid.
-        if (L.nra == 1) L.nra = 2;
+        // Balanced tiles on the fixed RMAX x CMAX consumer grid, in the merged view.
+        L.nra = L.MI0 > 64 ? 4 : 2;
         const int rm = 32 * L.nra, cm = kBoxNWC * kBoxNCB;
-        L.G0 = static_cast<int>((L.I0 + rm - 1) / rm);
-        L.r0 = static_cast<int>((L.I0 + L.G0 - 1) / L.G0);
-        // Whole 32-B sectors per tile row when the column pitch allows (else
-        // 16-B, the TMA minimum): neighbouring row tiles never share a DRAM
-        // sector, which would otherwise be fetched twice.
-        const int q = (L.I0 % 4 == 0) ? 4 : 2;
+        L.G0 = static_cast<int>((L.MI0 + rm - 1) / rm);
+        L.r0 = static_cast<int>((L.MI0 + L.G0 - 1) / L.G0);
+        // Whole 128-B lines per tile row when the (merged) column pitch is a
+        // multiple of 128 B; else whole 32-B sectors (16 B, the TMA minimum,
+        // for I0 % 4 != 0).
+        const int q = (L.MI0 % 16 == 0) ? 16 : ((L.I0 % 4 == 0) ? 4 : 2);
         L.r0 = std::min(rm, (L.r0 + q - 1) / q * q);
-        L.G0 = static_cast<int>((L.I0 + L.r0 - 1) / L.r0);
-        L.G1 = static_cast<int>((L.I1 + cm - 1) / cm);
-        L.t1 = static_cast<int>((L.I1 + L.G1 - 1) / L.G1);
-        L.G1 = static_cast<int>((L.I1 + L.t1 - 1) / L.t1);
+        L.G0 = static_cast<int>((L.MI0 + L.r0 - 1) / L.r0);
+        L.G1 = static_cast<int>((L.MI1 + cm - 1) / cm);
+        L.t1 = static_cast<int>((L.MI1 + L.G1 - 1) / L.G1);
+        L.G1 = static_cast<int>((L.MI1 + L.t1 - 1) / L.t1);
         L.ntiles = L.G0 * L.G1;
         const size_t red = static_cast<size_t>(2) * kBoxNWC * rm * 8;
         const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16;
@@ -797,8 +942,8 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     const int64_t npanels = static_cast<int64_t>(L.ntiles) * L.O;
     auto panel_cost = [&](int tile) {
         const int g0 = tile % L.G0, g1 = tile / L.G0;
-        const int64_t r = std::min<int64_t>(L.r0, L.I0 - int64_t(g0) * L.r0);
-        const int64_t c = std::min<int64_t>(L.t1, L.I1 - int64_t(g1) * L.t1);
+        const int64_t r = std::min<int64_t>(L.r0, L.MI0 - int64_t(g0) * L.r0);
+        const int64_t c = std::min<int64_t>(L.t1, L.MI1 - int64_t(g1) * L.t1);
         // bytes dominate; zero-filled edge boxes still cost consumer issue time
         return static_cast<double>(r * c) + 512.0;
     };
@@ -926,8 +1071,11 @@ void plan_rec(SweepPlan& P, const uint64_t* full_dims, int full_order, int order
     }
     L.w = work(static_cast<uint64_t>(L.O));
     L.p01 = work(static_cast<uint64_t>(L.nseg) * L.r0 * L.t1);
-    L.p0 = L.G1 > 1 ? work(static_cast<uint64_t>(L.G1) * L.I0 * L.O) : L.out_c0;
-    if (need_c1) L.p1 = L.G0 > 1 ? work(static_cast<uint64_t>(L.G0) * L.I1 * L.O) : L.out_c1;
+    // C0 / C1 partials per column / row tile (merged rows for C0), summed by
+    // the second stage; written in place when there is a single tile and class
+    L.p0 = (L.G1 > 1 || L.K > 1) ? work(static_cast<uint64_t>(L.G1) * L.MI0 * L.O) : L.out_c0;
+    if (need_c1)
+        L.p1 = (L.G0 > 1 || L.K > 1) ? work(static_cast<uint64_t>(L.G0) * L.I1 * L.O) : L.out_c1;
     P.levels.push_back(L);
 
     if (order >= 4) {
@@ -995,9 +1143,9 @@ EncodeTiledFn encode_fn() {
 CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t box_cols) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
-    const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(L.I0), static_cast<cuuint64_t>(L.I1),
+    const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(L.MI0), static_cast<cuuint64_t>(L.MI1),
                                 static_cast<cuuint64_t>(L.O)};
-    const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(L.I0) * 8,
+    const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(L.MI0) * 8,
                                    static_cast<cuuint64_t>(L.I0) * L.I1 * 8};
     const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols),
                                1};
@@ -1033,8 +1181,8 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
         configured_device = ctx->device;
     }
     BoxMaps maps;
-    const int64_t rem0 = L.I0 - static_cast<int64_t>(L.G0 - 1) * L.r0;
-    const int64_t rem1 = L.I1 - static_cast<int64_t>(L.G1 - 1) * L.t1;
+    const int64_t rem0 = L.MI0 - static_cast<int64_t>(L.G0 - 1) * L.r0;
+    const int64_t rem1 = L.MI1 - static_cast<int64_t>(L.G1 - 1) * L.t1;
     maps.m[0] = make_map(a.A, L, L.r0, L.t1);
     maps.m[1] = make_map(a.A, L, rem0, L.t1);
     maps.m[2] = make_map(a.A, L, L.r0, rem1);
@@ -1127,6 +1275,9 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.I0 = L.I0;
         s.I1 = L.I1;
         s.O = L.O;
+        s.K = L.K;
+        s.MI0 = L.MI0;
+        s.MI1 = L.MI1;
         s.u0 = factors_dev + foff[L.modes[0]];
         s.u1 = factors_dev + foff[L.modes[1]];
         s.W = oa.W;
@@ -1138,7 +1289,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.cta_seg = meta + L.cta_off;
         s.P01 = resolve(L.p01);
         s.P0 = resolve(L.p0);
-        s.P0_stride = L.I0 * L.O;
+        s.P0_stride = L.MI0 * L.O;
         s.P1 = L.out_c1.where == Where::None ? nullptr : resolve(L.p1);
         s.P1_stride = L.I1 * L.O;
         s.trace = (&L == &P->levels.front()) ? ctx->dbg_sweep_trace : nullptr;
@@ -1158,22 +1309,56 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         else
             launch_sweep<1, 8, 8>(ctx, L, s);
 
-        // second stage: fixed-order partial sums
-        reduce_b01_kernel<<<grid_for(L.I0 * L.I1, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
-            s.P01, meta + L.tile_off, L.I0, L.I1, L.r0, L.t1, L.G0, resolve(L.out_b01));
-        check_launch(ctx, "reduce_b01_kernel");
-        if (L.G1 > 1) {
-            const int64_t n0 = L.I0 * L.O;
-            reduce_copies_kernel<<<grid_for(n0, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
-                s.P0, s.P0_stride, L.G1, n0, resolve(L.out_c0));
-            check_launch(ctx, "reduce_copies_kernel(C0)");
+        // second stage: fixed-order partial sums, one launch
+        FinishArgs f{};
+        f.P01 = s.P01;
+        f.tile_seg = meta + L.tile_off;
+        f.I0 = L.I0;
+        f.I1 = L.I1;
+        f.O = L.O;
+        f.MI1 = L.MI1;
+        f.K = L.K;
+        f.lgK = 0;
+        while ((1 << f.lgK) < L.K) ++f.lgK;
+        f.r0 = L.r0;
+        f.t1 = L.t1;
+        f.G0 = L.G0;
+        f.G1 = L.G1;
+        f.b01 = resolve(L.out_b01);
+        if (L.G1 > 1 || L.K > 1) {
+            f.P0 = s.P0;
+            f.stride0 = s.P0_stride;
+            f.c0 = resolve(L.out_c0);
+            f.n_c0 = L.I0 * L.O;
         }
-        if (s.P1 && L.G0 > 1) {
-            const int64_t n1 = L.I1 * L.O;
-            reduce_copies_kernel<<<grid_for(n1, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
-                s.P1, s.P1_stride, L.G0, n1, resolve(L.out_c1));
-            check_launch(ctx, "reduce_copies_kernel(C1)");
+        if (s.P1 && (L.G0 > 1 || L.K > 1)) {
+            f.P1 = s.P1;
+            f.stride1 = s.P1_stride;
+            f.c1 = resolve(L.out_c1);
+            f.n_c1 = L.I1 * L.O;
         }
+        f.n_b01 = L.I0 * L.I1;
+        if (L.nseg >= 64 * L.ntiles) {
+            // many segments per tile: B01 by warps, C0/C1 (if any) below
+            const int64_t warps = f.n_b01;
+            const int grid = static_cast<int>(std::max<int64_t>(
+                1, std::min<int64_t>((warps * 32 + 255) / 256, int64_t(32) * ctx->num_sms)));
+            finish_b01_warp_kernel<<<grid, 256, 0, ctx->stream>>>(f);
+            check_launch(ctx, "finish_b01_warp_kernel");
+            f.b01 = nullptr;
+            f.n_b01 = 0;
+            if (f.n_c0 + f.n_c1 == 0) continue;
+        }
+        {
+            const int64_t total = f.n_b01 + f.n_c0 + f.n_c1;
+            const int grid = static_cast<int>(
+                std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, int64_t(32) * ctx->num_sms)));
+            if (total < (int64_t(1) << 31))
+                finish_kernel<int><<<grid, 256, 0, ctx->stream>>>(f);
+            else
+                finish_kernel<int64_t><<<grid, 256, 0, ctx->stream>>>(f);
+        }
+        check_launch(ctx, "finish_kernel");
     }
 }
 
@@ -1191,6 +1376,7 @@ void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* 
     info[7] = static_cast<int64_t>(P->work_elems);
     info[8] = static_cast<int64_t>(L.smem);
     info[9] = L.nra;
+    info[10] = L.K;
 }
 
 }  // namespace r1

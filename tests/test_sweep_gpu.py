@@ -12,6 +12,11 @@ SHAPES = [
     (3, 4), (5, 7), (2, 2, 2), (7, 5, 9), (30, 20, 10), (100, 100, 100), (129, 65, 33),
     (1, 1, 1), (1, 7, 3), (300, 2, 5), (3, 300, 5), (257, 130, 17), (6, 5, 4, 3),
     (4, 3, 5, 2, 3), (2, 3, 4, 5, 6, 2), (20, 20, 20, 20), (10, 10, 10, 10, 10), (65, 64, 3, 3),
+    # merged alignment classes (K = 128 / gcd(8 I0, 128) columns per merged
+    # column): one tile holding 4 classes, tiles straddling a class boundary,
+    # K = 2 and 4 at several row-tile counts, recursion levels with K > 1
+    (20, 8, 5), (200, 10, 7), (500, 8, 3), (60, 60, 9), (1000, 4, 3), (60, 8, 5, 3),
+    (40, 12, 6, 2), (100, 4, 2, 2, 2),
 ]
 
 
@@ -79,3 +84,38 @@ def test_build_j_errors(gpu_ctx, oracle):
         r1.build_block(a, r1.FactorSet(0.0, f), 1, 1)
     with pytest.raises(ValueError, match="order mismatch"):
         r1.build_j(a, r1.FactorSet(0.0, f[:2]))
+
+
+MERGE_SHAPES = [(20, 8, 5), (200, 10, 7), (500, 8, 3), (60, 60, 9), (1000, 4, 3), (60, 8, 5, 3),
+                (40, 12, 6, 2), (100, 4, 2, 2, 2), (20, 20, 20, 20), (100, 100, 100)]
+
+
+def test_build_j_merged_classes_forced():
+    """Every merged-alignment-class configuration (R1_SWEEP_MERGE=2 forces the
+    merged view whenever legal, including tiles holding up to 4 classes) in a
+    fresh process, against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {root!r})
+import paper_2403_01778_b200 as r1
+from oracle import rank1_oracle as o
+ctx = r1.default_context()
+for dims in {MERGE_SHAPES!r}:
+    a = o.oracle_random_tensor(dims, 5)
+    f = o.oracle_random_unit_factors(dims, 6)
+    want = o.build_j(a, dims, f)
+    got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
+    scale = o.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
+    assert ctx.sweep_plan_info(dims)["K"] > 1 or dims[0] % 16 == 0 or dims[0] % 4, dims
+    err = np.max(np.abs(got - want) / (scale + 1e-300))
+    assert err <= 1e-13, (dims, err)
+print("ok")
+"""
+    env = dict(os.environ, R1_SWEEP_MERGE="2")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -66,17 +66,29 @@ def run(name, dims, reps, warm_ms, s):
         sweep()
         torch.cuda.synchronize()
         _lib.check(_lib.lib().r1x_set_sweep_trace(ctx.handle, None))
-        t = tr.view(-1, 3).cpu().numpy()
-        t0 = t[:, 0].min()
-        st = (t[:, 0] - t0) / 1e3
-        en = (t[:, 1] - t0) / 1e3
+        tt = tr.view(-1, 3).cpu().numpy()
+        t0 = tt[:, 0].min()
+        st = (tt[:, 0] - t0) / 1e3
+        en = (tt[:, 1] - t0) / 1e3
         dur = en - st
         print(f"   trace: start max {st.max():.1f} us; end min {en.min():.1f} med {np.median(en):.1f} "
               f"max {en.max():.1f} us; dur min {dur.min():.1f} max {dur.max():.1f}")
         order = np.argsort(en)
-        print("   slowest CTAs (cta, smid, end us):", [(int(i), int(t[i, 2]), round(float(en[i]), 1)) for i in order[-8:]])
-        print("   fastest CTAs (cta, smid, end us):", [(int(i), int(t[i, 2]), round(float(en[i]), 1)) for i in order[:8]])
-        np.save(f"gpurun_out/trace_{name}.npy", t)
+        print("   slowest CTAs (cta, smid, end us):", [(int(i), int(tt[i, 2]), round(float(en[i]), 1)) for i in order[-8:]])
+        print("   fastest CTAs (cta, smid, end us):", [(int(i), int(tt[i, 2]), round(float(en[i]), 1)) for i in order[:8]])
+        np.save(f"gpurun_out/trace_{name}.npy", tt)
+    # live per-launch time of the top-level box kernel (CUDA events around it)
+    L = _lib.lib()
+    import ctypes
+    L.r1x_time_kernels(ctx.handle, 1)
+    kms, kn = ctypes.c_double(), ctypes.c_uint64()
+    L.r1x_kernel_time(ctx.handle, ctypes.byref(kms), ctypes.byref(kn))
+    for _ in range(reps):
+        sweep()
+    torch.cuda.synchronize()
+    L.r1x_kernel_time(ctx.handle, ctypes.byref(kms), ctypes.byref(kn))
+    L.r1x_time_kernels(ctx.handle, 0)
+    print(f"   level-0 box kernel: {kms.value / max(1, kn.value):.4f} ms/launch over {kn.value}")
     byts = 8 * n + 8 * nb + 8 * sum(dims)
     med = float(np.median(ms))
     print(f"{name} dims={dims} plan={ctx.sweep_plan_info(dims)} median {med:.3f} ms "
