@@ -212,9 +212,11 @@ int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
                        const uint64_t* global_dims, int order, uint64_t first);
 
 /* ---- solvers (solvers.hpp:63-88) -------------------------------------------- */
-/* algorithm: "hoscf" | "ihoscf".  Other reference names are rejected with
- * R1_ERR_INVALID_ARGUMENT ("unknown solver" for unknown names, "not on the
- * device path" for the CPU baselines): there is no CPU fallback. */
+/* algorithm: "hoscf" | "ihoscf" (SCF on J(u)) | "hopm" | "jacobi_hopm" |
+ * "asvd" | "jacobi_asvd" (the reference's baselines, solvers.cpp:299-447, on
+ * the same device sweep).  Unknown names: R1_ERR_INVALID_ARGUMENT "unknown
+ * solver".  report->final_x (SCF solvers: last stacked eigenvector) is zeroed
+ * for the baselines (the reference leaves it empty, solvers.hpp:56). */
 int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
              const r1_solve_options* opts, r1_solve_report* report);
 
