@@ -136,6 +136,8 @@ int r1_tensor_wrap_device(r1_context* ctx, const double* dev, const uint64_t* di
                           r1_tensor** out);
 /* Asynchronous H2D of the full tensor on the context stream. */
 int r1_tensor_copy_from_host(r1_context* ctx, r1_tensor* t, const double* host);
+/* D2H of the whole tensor (synchronous on the context stream). */
+int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host);
 int r1_tensor_destroy(r1_tensor* t);
 double* r1_tensor_device_ptr(const r1_tensor* t);
 
@@ -219,6 +221,41 @@ int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
  * for the baselines (the reference leaves it empty, solvers.hpp:56). */
 int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
              const r1_solve_options* opts, r1_solve_report* report);
+
+/* ---- greedy rank-R deflation (greedy.hpp:11-22, greedy.cpp:7-35) --------------- */
+/* Mirrors GreedyReport: terms in deflation order, ||R||_F / ||A||_F after each
+ * term, completed = 0 with `failure` = "term k: <solver error>" when a term's
+ * solve fails (partial report, status R1_OK, like the reference).  The
+ * residual lives on the device (a copy of `a`; `a` is not modified). */
+typedef struct r1_greedy_report {
+    int32_t completed;
+    int32_t terms;              /* terms solved (<= r) */
+    double* lambdas;            /* [r] caller-owned: FactorSet::lambda per term */
+    double* factors;            /* [r * sum I_k] caller-owned: factors per term */
+    double* residual_ratios;    /* [r] caller-owned */
+    r1_solve_report* solves;    /* [r] optional per-term reports (their arrays caller-owned) */
+    char failure[256];
+} r1_greedy_report;
+
+/* r >= 1 (else R1_ERR_INVALID_ARGUMENT "greedy_rank_r: rank must be >= 1");
+ * a zero tensor is R1_ERR_INVALID_ARGUMENT "greedy_rank_r: zero input tensor".
+ * Term k solves with opts->seed + k. */
+int r1_greedy_rank_r(r1_context* ctx, const r1_tensor* a, uint64_t r, const char* solver,
+                     const r1_solve_options* opts, r1_greedy_report* report);
+
+/* t -= lambda * u_0 o u_1 o ... (rank_one_expand, tensor.cpp:246-265, fused
+ * with the subtraction); *norm_out = ||t||_F afterwards (nullable). */
+int r1_rank_one_subtract(r1_context* ctx, r1_tensor* t, double lambda, const double* factors_host,
+                         double* norm_out);
+
+/* ---- .dt1 files straight to / from the device (tensor_io.hpp:9-21) -------------- */
+/* read_dt1 (tensor_io.cpp:66-100): same validation and messages (R1_ERR_RUNTIME:
+ * "read_dt1: cannot open|bad magic|tensor order must be >= 2|invalid
+ * dimension|size overflow|truncated payload|trailing bytes ..."); the payload
+ * streams through pinned staging buffers into a new device tensor. */
+int r1_tensor_read_dt1(r1_context* ctx, const char* path, r1_tensor** out);
+/* write_dt1 (tensor_io.cpp:47-64). */
+int r1_tensor_write_dt1(r1_context* ctx, const r1_tensor* t, const char* path);
 
 #ifdef __cplusplus
 }

@@ -630,3 +630,91 @@ def asvd(a, dims, opts: Options) -> Report:
 
 def jacobi_asvd(a, dims, opts: Options) -> Report:
     return _solve(a, dims, opts, "jacobi_asvd")
+
+
+# ------------------------------------------------------- greedy deflation --
+
+def rank_one_expand(lam, factors, dims) -> np.ndarray:
+    """rank_one_expand (tensor.cpp:246-265): buf = [lambda]; mode by mode
+    next[i |buf| + p] = buf[p] u_n[i] — the left-to-right product."""
+    buf = np.array([lam], dtype=np.float64)
+    for n, d in enumerate(dims):
+        u = np.asarray(factors[n], dtype=np.float64)
+        buf = np.outer(u, buf).reshape(-1)  # next[i * |buf| + p] = u[i] * buf[p]
+    return buf
+
+
+def greedy_rank_r(a, dims, r, solver: str, opts: Options):
+    """greedy_rank_r (greedy.cpp:7-35): returns dict(lambdas, terms, ratios,
+    iterations, completed, failure)."""
+    if r < 1:
+        raise ValueError("greedy_rank_r: rank must be >= 1")
+    a = np.asarray(a, dtype=np.float64)
+    base = float(np.sqrt(np.dot(a, a)))
+    if base == 0.0:
+        raise ValueError("greedy_rank_r: zero input tensor")
+    res = a.copy()
+    out = dict(lambdas=[], terms=[], ratios=[], iterations=[], completed=False, failure="")
+    fn = {"hoscf": hoscf, "ihoscf": ihoscf, "hopm": hopm, "jacobi_hopm": jacobi_hopm,
+          "asvd": asvd, "jacobi_asvd": jacobi_asvd}[solver]
+    for term in range(r):
+        o = Options(**{**opts.__dict__, "seed": opts.seed + term})
+        try:
+            rep = fn(res, dims, o)
+        except Exception as e:  # greedy.cpp:19-23
+            out["failure"] = f"term {term + 1}: {e}"
+            return out
+        res = res - rank_one_expand(rep.lam, rep.factors, dims)
+        out["lambdas"].append(rep.lam)
+        out["terms"].append([np.asarray(u).copy() for u in rep.factors])
+        out["ratios"].append(float(np.sqrt(np.dot(res, res))) / base)
+        out["iterations"].append(rep.iterations)
+    out["completed"] = True
+    return out
+
+
+# ------------------------------------------------------------------ .dt1 --
+
+DT1_MAGIC = b"DTEN1\0"
+
+
+def write_dt1(path, a, dims) -> None:
+    """write_dt1 (tensor_io.cpp:47-64): magic, u8 order, u64le dims, f64le payload."""
+    if len(dims) < 2:
+        raise ValueError("write_dt1: tensor order must be >= 2")
+    with open(path, "wb") as f:
+        f.write(DT1_MAGIC)
+        f.write(bytes([len(dims)]))
+        for d in dims:
+            f.write(int(d).to_bytes(8, "little"))
+        f.write(np.ascontiguousarray(a, dtype="<f8").tobytes())
+
+
+def read_dt1(path):
+    """read_dt1 (tensor_io.cpp:66-100) with the same checks and messages."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise RuntimeError(f"read_dt1: cannot open {path}")
+    with f:
+        if f.read(6) != DT1_MAGIC:
+            raise RuntimeError(f"read_dt1: bad magic in {path}")
+        b = f.read(1)
+        if len(b) != 1 or b[0] < 2:
+            raise RuntimeError("read_dt1: tensor order must be >= 2")
+        dims, count = [], 1
+        for _ in range(b[0]):
+            v = f.read(8)
+            d = int.from_bytes(v, "little") if len(v) == 8 else 0
+            if d == 0:
+                raise RuntimeError("read_dt1: invalid dimension")
+            if count > (2 ** 64 - 1) // d:
+                raise RuntimeError("read_dt1: size overflow")
+            dims.append(d)
+            count *= d
+        payload = f.read()
+    if len(payload) < 8 * count:
+        raise RuntimeError(f"read_dt1: truncated payload in {path}")
+    if len(payload) > 8 * count:
+        raise RuntimeError(f"read_dt1: trailing bytes in {path}")
+    return np.frombuffer(payload, dtype="<f8").astype(np.float64), dims

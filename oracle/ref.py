@@ -329,3 +329,47 @@ def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None
                 converged=bool(r.converged), iterations=r.iterations, lambda0=r.lambda0,
                 restarted=bool(r.restarted), final_x=fx.copy(), trace=trace,
                 sweeps=r.total_sweeps, seconds=r.t_total)
+
+
+def greedy(solver, a, dims, r, tol=1e-4, max_iters=500, seed=0, stop_rule=0):
+    """rank1::greedy_rank_r through the reference."""
+    a, ap = _d(a)
+    dd, dp = _dims(dims)
+    o = SolveOptionsC()
+    o.tol, o.max_iters, o.seed, o.determinism, o.record_kkt = tol, max_iters, seed, 1, 1
+    o.stop_rule = stop_rule
+    n = sum(dims)
+    lam = np.zeros(r)
+    fac = np.zeros(r * n)
+    rat = np.zeros(r)
+    its = np.zeros(r, dtype=np.int32)
+    nt, comp = ctypes.c_int(), ctypes.c_int()
+    fail = ctypes.create_string_buffer(512)
+    _check(lib().ref_greedy(solver.encode(), ap, dp, len(dims), ctypes.c_uint64(r), ctypes.byref(o),
+                            lam.ctypes.data_as(_dp), fac.ctypes.data_as(_dp),
+                            rat.ctypes.data_as(_dp), its.ctypes.data_as(_ip), ctypes.byref(nt),
+                            ctypes.byref(comp), fail, 512))
+    k = nt.value
+    offs = np.concatenate([[0], np.cumsum(dims)]).astype(int)
+    terms = [[fac[i * n + offs[m]:i * n + offs[m + 1]].copy() for m in range(len(dims))]
+             for i in range(k)]
+    return dict(lambdas=lam[:k].copy(), terms=terms, ratios=rat[:k].copy(),
+                iterations=its[:k].tolist(), completed=bool(comp.value),
+                failure=fail.value.decode())
+
+
+def write_dt1(path, a, dims):
+    a, ap = _d(a)
+    dd, dp = _dims(dims)
+    _check(lib().ref_write_dt1(str(path).encode(), ap, dp, len(dims)))
+
+
+def read_dt1(path):
+    dims = (ctypes.c_uint64 * 256)()
+    order = ctypes.c_int()
+    _check(lib().ref_read_dt1(str(path).encode(), dims, ctypes.byref(order), None, ctypes.c_uint64(0)))
+    d = [int(dims[k]) for k in range(order.value)]
+    out = np.empty(int(np.prod(d)))
+    _check(lib().ref_read_dt1(str(path).encode(), dims, ctypes.byref(order), out.ctypes.data_as(_dp),
+                              ctypes.c_uint64(out.size)))
+    return out, d

@@ -11,6 +11,7 @@
 // become status codes (same codes as include/rank1_b200.h).
 
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -19,12 +20,14 @@
 #include <vector>
 
 #include "rank1/generators.hpp"
+#include "rank1/greedy.hpp"
 #include "rank1/nepv.hpp"
 #include "rank1/rng.hpp"
 #include "rank1/solvers.hpp"
 #include "rank1/stacked.hpp"
 #include "rank1/sym_eig.hpp"
 #include "rank1/tensor.hpp"
+#include "rank1/tensor_io.hpp"
 #include "rank1_b200.h"
 
 #ifdef _OPENMP
@@ -392,6 +395,48 @@ int ref_solve(const char* algorithm, const double* a, const uint64_t* dims, int 
         }
         rep->total_sweeps = sweeps;
         rep->t_total = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+// greedy_rank_r (greedy.cpp:7-35).  Arrays sized r (factors r * sum I_k);
+// *nterms = terms solved, *completed, failure text (rep.failure) into `failure`.
+int ref_greedy(const char* solver, const double* a, const uint64_t* dims, int order, uint64_t r,
+               const r1_solve_options* opts, double* lambdas, double* factors, double* ratios,
+               int* iters, int* nterms, int* completed, char* failure, int failure_len) {
+    return guarded([&] {
+        DenseTensor t = make_tensor(a, dims, order);
+        SolveOptions so = make_opts(opts, dims, order);
+        GreedyReport g = greedy_rank_r(t, r, solver, so);
+        std::size_t sum = 0;
+        for (int k = 0; k < order; ++k) sum += dims[k];
+        for (std::size_t i = 0; i < g.terms.size(); ++i) {
+            lambdas[i] = g.terms[i].lambda;
+            std::size_t off = 0;
+            for (int k = 0; k < order; ++k) {
+                std::memcpy(factors + i * sum + off, g.terms[i].factors[k].data(),
+                            sizeof(double) * dims[k]);
+                off += dims[k];
+            }
+            ratios[i] = g.residual_ratios[i];
+            iters[i] = g.solves[i].iterations;
+        }
+        *nterms = static_cast<int>(g.terms.size());
+        *completed = g.completed ? 1 : 0;
+        std::snprintf(failure, failure_len, "%s", g.failure.c_str());
+    });
+}
+
+// write_dt1 / read_dt1 (tensor_io.cpp:47-100)
+int ref_write_dt1(const char* path, const double* a, const uint64_t* dims, int order) {
+    return guarded([&] { write_dt1(path, make_tensor(a, dims, order)); });
+}
+
+int ref_read_dt1(const char* path, uint64_t* dims, int* order, double* out, uint64_t cap) {
+    return guarded([&] {
+        DenseTensor t = read_dt1(path);
+        *order = static_cast<int>(t.order());
+        for (std::size_t k = 0; k < t.order(); ++k) dims[k] = t.dim(k);
+        if (out && t.size() <= cap) std::memcpy(out, t.data(), sizeof(double) * t.size());
     });
 }
 

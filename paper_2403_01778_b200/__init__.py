@@ -124,6 +124,28 @@ class DeviceTensor:
         a = np.ascontiguousarray(np.asarray(data, dtype=np.float64).reshape(-1))
         check(lib().r1_tensor_copy_from_host(self.ctx.handle, self.handle, dptr(a)))
 
+    def to_host(self) -> np.ndarray:
+        out = np.empty(int(np.prod(self.dims)))
+        check(lib().r1_tensor_copy_to_host(self.ctx.handle, self.handle, dptr(out)))
+        return out
+
+    @classmethod
+    def read_dt1(cls, path, ctx: Optional[Context] = None) -> "DeviceTensor":
+        """read_dt1 (tensor_io.cpp:66-100) straight into HBM."""
+        ctx = ctx or default_context()
+        h = ctypes.c_void_p()
+        check(lib().r1_tensor_read_dt1(ctx.handle, str(path).encode(), ctypes.byref(h)))
+        # the header was validated by the loader; re-read its dims for the wrapper
+        with open(path, "rb") as f:
+            f.read(6)
+            d = f.read(1)[0]
+            dims = [int.from_bytes(f.read(8), "little") for _ in range(d)]
+        return cls(ctx, h, dims)
+
+    def write_dt1(self, path):
+        """write_dt1 (tensor_io.cpp:47-64) straight from HBM."""
+        check(lib().r1_tensor_write_dt1(self.ctx.handle, self.handle, str(path).encode()))
+
     def close(self):
         if self.handle:
             lib().r1_tensor_destroy(self.handle)
@@ -668,3 +690,85 @@ def asvd(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
 def jacobi_asvd(a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
     """solvers.hpp:82-83: asvd with all pair subproblems from the previous iterate."""
     return solve("jacobi_asvd", a, opts, ctx)
+
+
+# ------------------------------------------------------- greedy deflation --
+
+@dataclass
+class GreedyReport:
+    """greedy.hpp:11-17."""
+    terms: list = field(default_factory=list)            # FactorSet per term
+    residual_ratios: list = field(default_factory=list)  # ||R||_F / ||A||_F after each term
+    solves: list = field(default_factory=list)           # SolveReport per term
+    completed: bool = False
+    failure: str = ""
+
+
+def greedy_rank_r(a, r: int, solver: str, opts: SolveOptions,
+                  ctx: Optional[Context] = None) -> GreedyReport:
+    """greedy_rank_r (greedy.hpp:21-22, greedy.cpp:7-35) with the residual kept in
+    HBM: per term a device solve (seed + term) and one fused subtract + norm pass."""
+    ctx = ctx or default_context()
+    if r < 1:
+        raise InvalidArgument("greedy_rank_r: rank must be >= 1")
+    owned = None
+    if isinstance(a, DenseTensor):
+        owned = DeviceTensor.from_host(a.data, a.dims(), ctx)
+        t = owned
+    else:
+        t = a
+    dims = list(t.dims)
+    n = sum(dims)
+    c, keep = _options_c(opts, dims)
+    lam = np.zeros(r)
+    fac = np.zeros(r * n)
+    rat = np.zeros(r)
+    solves = (_lib.SolveReportC * r)()
+    bufs = []
+    for i in range(r):
+        f_, x_ = np.empty(n), np.empty(n)
+        tr = (_lib.IterationRecordC * max(1, opts.max_iters))()
+        bufs.append((f_, x_, tr))
+        solves[i].factors = dptr(f_)
+        solves[i].final_x = dptr(x_)
+        solves[i].trace = tr
+    g = _lib.GreedyReportC()
+    g.lambdas, g.factors, g.residual_ratios = dptr(lam), dptr(fac), dptr(rat)
+    g.solves = solves
+    try:
+        check(lib().r1_greedy_rank_r(ctx.handle, t.handle, ctypes.c_uint64(r), solver.encode(),
+                                     ctypes.byref(c), ctypes.byref(g)))
+    finally:
+        if owned is not None:
+            owned.close()
+    offs = np.concatenate([[0], np.cumsum(dims)]).astype(int)
+    rep = GreedyReport(completed=bool(g.completed), failure=g.failure.decode())
+    for i in range(g.terms):
+        rep.terms.append(FactorSet(lam[i], [fac[i * n + offs[k]:i * n + offs[k + 1]].copy()
+                                            for k in range(len(dims))]))
+        rep.residual_ratios.append(float(rat[i]))
+        s_ = solves[i]
+        sr = SolveReport(algorithm=solver)
+        sr.result = rep.terms[-1]
+        sr.converged, sr.iterations = bool(s_.converged), int(s_.iterations)
+        sr.lambda0, sr.restarted = s_.lambda0, bool(s_.restarted)
+        sr.total_sweeps = int(s_.total_sweeps)
+        rep.solves.append(sr)
+    return rep
+
+
+def read_dt1(path, ctx: Optional[Context] = None) -> DeviceTensor:
+    """tensor_io.hpp:17: a .dt1 file straight into HBM."""
+    return DeviceTensor.read_dt1(path, ctx)
+
+
+def write_dt1(path, a) -> None:
+    """tensor_io.hpp:16: a DeviceTensor (from HBM) or a DenseTensor to a .dt1 file."""
+    if isinstance(a, DeviceTensor):
+        a.write_dt1(path)
+        return
+    t = DeviceTensor.from_host(a.data, a.dims())
+    try:
+        t.write_dt1(path)
+    finally:
+        t.close()

@@ -66,6 +66,12 @@ class SolveReportC(ctypes.Structure):
                 ("t_total", ctypes.c_double)]
 
 
+class GreedyReportC(ctypes.Structure):
+    _fields_ = [("completed", ctypes.c_int32), ("terms", ctypes.c_int32), ("lambdas", _dp),
+                ("factors", _dp), ("residual_ratios", _dp),
+                ("solves", ctypes.POINTER(SolveReportC)), ("failure", ctypes.c_char * 256)]
+
+
 # name -> (restype, argtypes): every symbol include/rank1_b200.h declares.
 SIGNATURES = {
     "r1_abi_version": (ctypes.c_int, []),
@@ -81,6 +87,7 @@ SIGNATURES = {
     "r1_tensor_create": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, ctypes.POINTER(_vp)]),
     "r1_tensor_wrap_device": (ctypes.c_int, [_vp, _vp, _u64p, ctypes.c_int, ctypes.POINTER(_vp)]),
     "r1_tensor_copy_from_host": (ctypes.c_int, [_vp, _vp, _dp]),
+    "r1_tensor_copy_to_host": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_destroy": (ctypes.c_int, [_vp]),
     "r1_tensor_device_ptr": (_vp, [_vp]),
     "r1_blocks_numel": (ctypes.c_uint64, [_u64p, ctypes.c_int]),
@@ -101,6 +108,11 @@ SIGNATURES = {
                                           ctypes.c_int, ctypes.c_uint64]),
     "r1_solve": (ctypes.c_int, [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(SolveOptionsC),
                                 ctypes.POINTER(SolveReportC)]),
+    "r1_greedy_rank_r": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, ctypes.c_char_p,
+                                        ctypes.POINTER(SolveOptionsC), ctypes.POINTER(GreedyReportC)]),
+    "r1_rank_one_subtract": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _dp, _dp]),
+    "r1_tensor_read_dt1": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "r1_tensor_write_dt1": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p]),
 }
 
 # Diagnostics not in the public header (tests / bench only).

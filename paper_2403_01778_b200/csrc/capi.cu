@@ -236,6 +236,16 @@ int r1_tensor_copy_from_host(r1_context* ctx, r1_tensor* t, const double* host) 
     });
 }
 
+int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host) {
+    return abi_guard([&] {
+        bind(ctx);
+        if (!t || !host) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaMemcpyAsync(host, t->dev, t->numel * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int r1_tensor_destroy(r1_tensor* t) {
     return abi_guard([&] {
         if (!t) return;

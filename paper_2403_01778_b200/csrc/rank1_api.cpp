@@ -5,6 +5,7 @@
 // mapped back to the reference's exception types (invalid_argument /
 // runtime_error).
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -12,11 +13,13 @@
 #include <stdexcept>
 #include <string>
 
+#include "rank1/greedy.hpp"
 #include "rank1/nepv.hpp"
 #include "rank1/solvers.hpp"
 #include "rank1/stacked.hpp"
 #include "rank1/sym_eig.hpp"
 #include "rank1/tensor.hpp"
+#include "rank1/tensor_io.hpp"
 #include "rank1_b200.h"
 
 namespace rank1 {
@@ -436,11 +439,10 @@ double SolveReport::wall_total() const {
     return s;
 }
 
-SolveReport solve(const std::string& algorithm, const DenseTensor& a, const SolveOptions& opts) {
-    if (algorithm != "hoscf" && algorithm != "ihoscf" && algorithm != "hopm" &&
-        algorithm != "jacobi_hopm" && algorithm != "asvd" && algorithm != "jacobi_asvd")
-        throw std::invalid_argument("unknown solver: " + algorithm);
-    if (a.order() < 2) throw std::invalid_argument("solver: tensor order must be >= 2");
+namespace {
+
+// SolveOptions -> r1_solve_options (init factors flattened into `init`).
+r1_solve_options c_options(const DenseTensor& a, const SolveOptions& opts, std::vector<double>& init) {
     r1_solve_options o;
     r1_solve_options_default(&o);
     o.tol = opts.tol;
@@ -456,7 +458,7 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
     o.record_kkt = opts.record_kkt ? 1 : 0;
     o.reuse_intermediates = opts.reuse_intermediates ? 1 : 0;
     o.asvd_disjoint_pairs = opts.asvd_disjoint_pairs ? 1 : 0;
-    std::vector<double> init;
+    init.clear();
     if (opts.init == InitKind::provided) {
         if (opts.init_factors.size() != a.order())
             throw std::invalid_argument("solver: provided init has wrong order");
@@ -468,24 +470,29 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
         o.init = R1_INIT_PROVIDED;
         o.init_factors = init.data();
     }
-    const auto dims = u64(a.dims());
-    r1_tensor* t = nullptr;
-    raise(r1_tensor_from_host(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), &t));
-    std::unique_ptr<r1_tensor, int (*)(r1_tensor*)> guard(t, r1_tensor_destroy);
-    const std::size_t n = std::accumulate(a.dims().begin(), a.dims().end(), std::size_t{0});
-    std::vector<double> fac(n), fx(n);
-    std::vector<r1_iteration_record> tr(std::max(1, opts.max_iters));
+    return o;
+}
+
+// caller-owned arrays of one r1_solve_report
+struct ReportBuffers {
+    std::vector<double> fac, fx;
+    std::vector<r1_iteration_record> tr;
     r1_solve_report r{};
-    r.factors = fac.data();
-    r.final_x = fx.data();
-    r.trace = tr.data();
-    raise(r1_solve(ctx(), algorithm.c_str(), t, &o, &r));
+    ReportBuffers(std::size_t n, int max_iters) : fac(n), fx(n), tr(std::max(1, max_iters)) {
+        r.factors = fac.data();
+        r.final_x = fx.data();
+        r.trace = tr.data();
+    }
+};
+
+SolveReport from_c(const std::string& algorithm, const DenseTensor& a, const ReportBuffers& b) {
+    const r1_solve_report& r = b.r;
     SolveReport rep;
     rep.algorithm = algorithm;
     rep.result.lambda = r.lambda;
     std::size_t off = 0;
     for (std::size_t k = 0; k < a.order(); ++k) {
-        rep.result.factors.emplace_back(fac.begin() + off, fac.begin() + off + a.dim(k));
+        rep.result.factors.emplace_back(b.fac.begin() + off, b.fac.begin() + off + a.dim(k));
         off += a.dim(k);
     }
     rep.converged = r.converged != 0;
@@ -493,21 +500,124 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
     rep.lambda0 = r.lambda0;
     rep.restarted = r.restarted != 0;
     // SCF solvers: last stacked eigenvector; baselines leave it empty (solvers.hpp:56)
-    if (algorithm == "hoscf" || algorithm == "ihoscf") rep.final_x = StackedVector(a.dims(), fx);
+    if (algorithm == "hoscf" || algorithm == "ihoscf") rep.final_x = StackedVector(a.dims(), b.fx);
     for (int i = 0; i < r.iterations; ++i) {
         IterationRecord q;
-        q.lambda = tr[i].lambda;
-        q.stop_value = tr[i].stop_value;
-        q.eq11_value = tr[i].eq11_value;
-        q.kkt_max_residual = tr[i].kkt_max_residual;
-        q.rqi_accepted = tr[i].rqi_accepted != 0;
-        q.lambda_pre_rqi = tr[i].lambda_pre_rqi;
-        q.t_build_j = tr[i].t_build_j;
-        q.t_eig = tr[i].t_eig;
-        q.t_other = tr[i].t_other;
+        q.lambda = b.tr[i].lambda;
+        q.stop_value = b.tr[i].stop_value;
+        q.eq11_value = b.tr[i].eq11_value;
+        q.kkt_max_residual = b.tr[i].kkt_max_residual;
+        q.rqi_accepted = b.tr[i].rqi_accepted != 0;
+        q.lambda_pre_rqi = b.tr[i].lambda_pre_rqi;
+        q.t_build_j = b.tr[i].t_build_j;
+        q.t_eig = b.tr[i].t_eig;
+        q.t_other = b.tr[i].t_other;
         rep.trace.push_back(q);
     }
     return rep;
+}
+
+struct TensorGuard {
+    r1_tensor* t = nullptr;
+    ~TensorGuard() {
+        if (t) r1_tensor_destroy(t);
+    }
+};
+
+}  // namespace
+
+SolveReport solve(const std::string& algorithm, const DenseTensor& a, const SolveOptions& opts) {
+    if (algorithm != "hoscf" && algorithm != "ihoscf" && algorithm != "hopm" &&
+        algorithm != "jacobi_hopm" && algorithm != "asvd" && algorithm != "jacobi_asvd")
+        throw std::invalid_argument("unknown solver: " + algorithm);
+    if (a.order() < 2) throw std::invalid_argument("solver: tensor order must be >= 2");
+    std::vector<double> init;
+    r1_solve_options o = c_options(a, opts, init);
+    const auto dims = u64(a.dims());
+    TensorGuard t;
+    raise(r1_tensor_from_host(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), &t.t));
+    const std::size_t n = std::accumulate(a.dims().begin(), a.dims().end(), std::size_t{0});
+    ReportBuffers b(n, opts.max_iters);
+    raise(r1_solve(ctx(), algorithm.c_str(), t.t, &o, &b.r));
+    return from_c(algorithm, a, b);
+}
+
+// greedy.hpp:21-22 on the device (residual resident in HBM).
+GreedyReport greedy_rank_r(const DenseTensor& a, std::size_t r, const std::string& solver,
+                           const SolveOptions& opts) {
+    if (r < 1) throw std::invalid_argument("greedy_rank_r: rank must be >= 1");
+    std::vector<double> init;
+    r1_solve_options o = c_options(a, opts, init);
+    const auto dims = u64(a.dims());
+    TensorGuard t;
+    raise(r1_tensor_from_host(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), &t.t));
+    const std::size_t n = std::accumulate(a.dims().begin(), a.dims().end(), std::size_t{0});
+    std::vector<double> lam(r), fac(r * n), rat(r);
+    std::vector<std::unique_ptr<ReportBuffers>> bufs;
+    std::vector<r1_solve_report> reps(r);
+    for (std::size_t i = 0; i < r; ++i) {
+        bufs.push_back(std::make_unique<ReportBuffers>(n, opts.max_iters));
+        reps[i] = bufs.back()->r;
+    }
+    r1_greedy_report g{};
+    g.lambdas = lam.data();
+    g.factors = fac.data();
+    g.residual_ratios = rat.data();
+    g.solves = reps.data();
+    raise(r1_greedy_rank_r(ctx(), t.t, r, solver.c_str(), &o, &g));
+    GreedyReport rep;
+    for (int i = 0; i < g.terms; ++i) {
+        bufs[i]->r = reps[i];
+        SolveReport s = from_c(solver, a, *bufs[i]);
+        rep.terms.push_back(s.result);
+        rep.residual_ratios.push_back(rat[i]);
+        rep.solves.push_back(std::move(s));
+    }
+    rep.completed = g.completed != 0;
+    rep.failure = g.failure;
+    return rep;
+}
+
+// tensor_io.hpp:16-20: the file is staged through the device loader, so the
+// host API and r1_tensor_read_dt1 share one validation path.
+DenseTensor read_dt1(const std::string& path) {
+    TensorGuard t;
+    raise(r1_tensor_read_dt1(ctx(), path.c_str(), &t.t));
+    // dims from the validated header
+    std::vector<std::size_t> dims;
+    {
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        if (!f) throw std::runtime_error("read_dt1: cannot open " + path);
+        unsigned char hdr[7];
+        if (std::fread(hdr, 1, 7, f) != 7) {
+            std::fclose(f);
+            throw std::runtime_error("read_dt1: bad magic in " + path);
+        }
+        for (int k = 0; k < hdr[6]; ++k) {
+            unsigned char b[8];
+            if (std::fread(b, 1, 8, f) != 8) break;
+            uint64_t v = 0;
+            for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(b[i]) << (8 * i);
+            dims.push_back(static_cast<std::size_t>(v));
+        }
+        std::fclose(f);
+    }
+    DenseTensor out(dims);
+    raise(r1_tensor_copy_to_host(ctx(), t.t, out.data()));
+    return out;
+}
+
+void write_dt1(const std::string& path, const DenseTensor& a) {
+    if (a.order() < 2) throw std::invalid_argument("write_dt1: tensor order must be >= 2");
+    const auto dims = u64(a.dims());
+    TensorGuard t;
+    raise(r1_tensor_from_host(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), &t.t));
+    raise(r1_tensor_write_dt1(ctx(), t.t, path.c_str()));
+}
+
+void write_dt1(const std::string& path, const Matrix& m) {
+    DenseTensor t({m.rows(), m.cols()}, std::vector<double>(m.values().begin(), m.values().end()));
+    write_dt1(path, t);
 }
 
 SolveReport hoscf(const DenseTensor& a, const SolveOptions& opts) { return solve("hoscf", a, opts); }

@@ -9,16 +9,21 @@
 #include <stdexcept>
 #include <vector>
 
+#include "rank1/greedy.hpp"
 #include "rank1/nepv.hpp"
 #include "rank1/solvers.hpp"
 #include "rank1/stacked.hpp"
 #include "rank1/sym_eig.hpp"
+#include "rank1/tensor_io.hpp"
 #include "rank1_b200.h"
 
 extern "C" {
 int ref_build_j(const double*, const uint64_t*, int, const double*, int, int, int, int, double*, double*);
 int ref_solve(const char*, const double*, const uint64_t*, int, const r1_solve_options*, r1_solve_report*);
 int ref_rng_draws(uint64_t, uint64_t, int, int64_t, double*);
+int ref_greedy(const char*, const double*, const uint64_t*, int, uint64_t, const r1_solve_options*,
+               double*, double*, double*, int*, int*, int*, char*, int);
+int ref_read_dt1(const char*, uint64_t*, int*, double*, uint64_t);
 }
 
 using namespace rank1;
@@ -153,6 +158,53 @@ int main() {
         try {
             solve("nope", a, o);
         } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // greedy.hpp: device deflation vs the reference's greedy_rank_r
+    {
+        DenseTensor a = gaussian({7, 5, 9}, 11);
+        SolveOptions o;
+        o.tol = 1e-10;
+        o.seed = 1;
+        const GreedyReport g = greedy_rank_r(a, 3, "hoscf", o);
+        r1_solve_options ro;
+        r1_solve_options_default(&ro);
+        ro.tol = 1e-10;
+        ro.seed = 1;
+        const uint64_t dims[3] = {7, 5, 9};
+        double lam[3], fac[3 * 21], rat[3];
+        int its[3], nt = 0, comp = 0;
+        char fail[256];
+        ref_greedy("hoscf", a.data(), dims, 3, 3, &ro, lam, fac, rat, its, &nt, &comp, fail, 256);
+        CHECK(g.completed && comp == 1 && g.terms.size() == 3 && nt == 3);
+        for (int i = 0; i < 3 && i < static_cast<int>(g.terms.size()); ++i) {
+            CHECK(std::abs(g.terms[i].lambda - lam[i]) <= 1e-10 * lam[i]);
+            CHECK(std::abs(g.residual_ratios[i] - rat[i]) <= 1e-9);
+        }
+        o.tol = 0.0;
+        const GreedyReport bad = greedy_rank_r(a, 2, "hoscf", o);
+        CHECK(!bad.completed && bad.failure == "term 1: solver: tol must be > 0");
+    }
+    // tensor_io.hpp: write with the device writer, read with the reference's reader
+    {
+        DenseTensor a = gaussian({4, 3, 5}, 4);
+        write_dt1("/tmp/r1_dropin_test.dt1", a);
+        uint64_t dims[8];
+        int order = 0;
+        std::vector<double> back(60);
+        CHECK(ref_read_dt1("/tmp/r1_dropin_test.dt1", dims, &order, back.data(), 60) == 0);
+        CHECK(order == 3 && dims[0] == 4 && dims[1] == 3 && dims[2] == 5);
+        bool same = true;
+        for (std::size_t i = 0; i < 60; ++i) same = same && back[i] == a[i];
+        CHECK(same);
+        const DenseTensor r = read_dt1("/tmp/r1_dropin_test.dt1");
+        CHECK(r.dims() == a.dims() && r[7] == a[7]);
+        bool threw = false;
+        try {
+            read_dt1("/tmp/r1_dropin_missing.dt1");
+        } catch (const std::runtime_error&) {
             threw = true;
         }
         CHECK(threw);

@@ -13,7 +13,8 @@ import pytest
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
 
-from golden.gen_golden import BASELINE_SOLVES, SOLVES, SWEEP_SHAPES, solve_input  # noqa: E402
+from golden.gen_golden import (BASELINE_SOLVES, DT1_DIMS, GREEDY_CASES, SOLVES, SWEEP_SHAPES,  # noqa: E402
+                               solve_input)
 
 
 def tag(dims):
@@ -141,6 +142,48 @@ def test_oracle_baselines_vs_reference(oracle, case):
             v = fac[o:o + len(u)]
             o += len(u)
             assert min(np.max(np.abs(u - v)), np.max(np.abs(u + v))) <= 1e-8
+
+
+@pytest.mark.parametrize("case", GREEDY_CASES, ids=[c[0] for c in GREEDY_CASES])
+def test_oracle_greedy_vs_reference(oracle, case):
+    """greedy_rank_r (greedy.cpp:7-35) restated on the oracle solvers."""
+    name, solver, kind, dims, r, tol, seed = case
+    a = solve_input(kind, dims, seed)
+    g = oracle.greedy_rank_r(a, dims, r, solver, oracle.Options(tol=tol, seed=seed))
+    meta = GOLD[f"greedy_{name}_meta"]
+    assert g["completed"] == bool(meta[0]) and len(g["terms"]) == int(meta[1])
+    assert g["failure"] == bytes(GOLD[f"greedy_{name}_failure"]).decode()
+    if g["terms"]:
+        np.testing.assert_allclose(g["lambdas"], GOLD[f"greedy_{name}_lambdas"], rtol=1e-10)
+        np.testing.assert_allclose(g["ratios"], GOLD[f"greedy_{name}_ratios"], rtol=1e-9, atol=1e-12)
+
+
+def test_oracle_rank_one_expand_kat(oracle):
+    """rank_one_expand: out[i0 + I0 i1 + ...] = ((lambda u0[i0]) u1[i1]) ..."""
+    dims = (3, 2, 4)
+    f = oracle.oracle_random_unit_factors(dims, 7)
+    e = oracle.rank_one_expand(2.5, f, dims)
+    want = 2.5 * np.einsum("i,j,k->ijk", *f).reshape(-1, order="F")
+    np.testing.assert_allclose(e, want, rtol=1e-15)
+
+
+def test_oracle_dt1_vs_reference_file(oracle, tmp_path):
+    """tests/golden/ref_7x5x9.dt1 was written by the reference's write_dt1."""
+    path = os.path.join(HERE, "golden", "ref_7x5x9.dt1")
+    a, dims = oracle.read_dt1(path)
+    assert dims == list(DT1_DIMS)
+    assert np.array_equal(a, oracle.oracle_random_tensor(DT1_DIMS, 21))
+    out = tmp_path / "o.dt1"
+    oracle.write_dt1(out, a, dims)
+    assert out.read_bytes() == open(path, "rb").read()
+    bad = tmp_path / "bad.dt1"
+    raw = open(path, "rb").read()
+    for blob, msg in [(b"XTEN1\0" + raw[6:], "bad magic"), (raw[:6] + bytes([1]) + raw[7:], "order must be"),
+                      (raw[:-8], "truncated payload"), (raw + b"\0", "trailing bytes"),
+                      (raw[:7] + (0).to_bytes(8, "little") + raw[15:], "invalid dimension")]:
+        bad.write_bytes(blob)
+        with pytest.raises(RuntimeError, match=msg):
+            oracle.read_dt1(bad)
 
 
 # -------------------------------------------------- reference KATs (tests/) --
