@@ -138,6 +138,8 @@ int r1_tensor_wrap_device(r1_context* ctx, const double* dev, const uint64_t* di
 int r1_tensor_copy_from_host(r1_context* ctx, r1_tensor* t, const double* host);
 /* D2H of the whole tensor (synchronous on the context stream). */
 int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host);
+/* frobenius_norm (tensor.hpp:67, tensor.cpp:240-244) of a device tensor. */
+int r1_tensor_frobenius(r1_context* ctx, const r1_tensor* t, double* out);
 int r1_tensor_destroy(r1_tensor* t);
 double* r1_tensor_device_ptr(const r1_tensor* t);
 
@@ -212,6 +214,11 @@ int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host,
  * scope; this exists so benchmarks never stage 8-32 GB through the host.) */
 int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
                        const uint64_t* global_dims, int order, uint64_t first);
+/* generate(name, dims, seed) (generators.hpp, generators.cpp:101-116) into `t`
+ * (the tensor's dims): "gaussian" (N(0,1), stream 1) | "exp" | "arcsin" | "tan"
+ * — the reference's named inputs for the experiment harness.  exp / arcsin are
+ * bit-identical to the reference; gaussian / tan to ~1 ulp (device log/cos/tan). */
+int r1_generate(r1_context* ctx, r1_tensor* t, const char* name, uint64_t seed);
 
 /* ---- solvers (solvers.hpp:63-88) -------------------------------------------- */
 /* algorithm: "hoscf" | "ihoscf" (SCF on J(u)) | "hopm" | "jacobi_hopm" |

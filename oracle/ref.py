@@ -373,3 +373,17 @@ def read_dt1(path):
     _check(lib().ref_read_dt1(str(path).encode(), dims, ctypes.byref(order), out.ctypes.data_as(_dp),
                               ctypes.c_uint64(out.size)))
     return out, d
+
+
+def experiment_csv(generator, a, dims, algos, seeds, base_seed=0, tol=1e-4, max_iters=500):
+    """run_experiment + experiment_csv(zero_timings) + summary_table of the reference."""
+    a, ap = _d(a)
+    dd, dp = _dims(dims)
+    o = SolveOptionsC()
+    o.tol, o.max_iters, o.determinism, o.record_kkt = tol, max_iters, 1, 1
+    buf = ctypes.create_string_buffer(1 << 20)
+    _check(lib().ref_experiment_csv(generator.encode(), ap, dp, len(dims), ",".join(algos).encode(),
+                                    ctypes.c_uint64(seeds), ctypes.c_uint64(base_seed),
+                                    ctypes.byref(o), buf, 1 << 20))
+    csv_text, _, table = buf.value.decode().partition("\n\n")
+    return csv_text + "\n", table

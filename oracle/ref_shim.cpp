@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "rank1/experiment.hpp"
 #include "rank1/generators.hpp"
 #include "rank1/greedy.hpp"
 #include "rank1/nepv.hpp"
@@ -437,6 +438,34 @@ int ref_read_dt1(const char* path, uint64_t* dims, int* order, double* out, uint
         *order = static_cast<int>(t.order());
         for (std::size_t k = 0; k < t.order(); ++k) dims[k] = t.dim(k);
         if (out && t.size() <= cap) std::memcpy(out, t.data(), sizeof(double) * t.size());
+    });
+}
+
+// run_experiment + experiment_csv(zero_timings=true) + summary_table
+// (experiment.cpp:81-193) on a given tensor; algos comma-separated.
+int ref_experiment_csv(const char* generator, const double* a, const uint64_t* dims, int order,
+                       const char* algos, uint64_t seeds, uint64_t base_seed,
+                       const r1_solve_options* opts, char* out, int out_len) {
+    return guarded([&] {
+        DenseTensor t = make_tensor(a, dims, order);
+        ExperimentSpec spec;
+        spec.generator = generator;
+        spec.seeds = seeds;
+        spec.base_seed = base_seed;
+        spec.opts = make_opts(opts, dims, order);
+        spec.algorithms.clear();
+        std::string s(algos), tok;
+        for (char c : s + ",") {
+            if (c == ',') {
+                if (!tok.empty()) spec.algorithms.push_back(tok);
+                tok.clear();
+            } else {
+                tok += c;
+            }
+        }
+        ExperimentResult r = run_experiment(spec, t);
+        const std::string text = experiment_csv(r.rows, true) + "\n" + summary_table(r.summaries);
+        std::snprintf(out, out_len, "%s", text.c_str());
     });
 }
 

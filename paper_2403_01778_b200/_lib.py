@@ -88,6 +88,7 @@ SIGNATURES = {
     "r1_tensor_wrap_device": (ctypes.c_int, [_vp, _vp, _u64p, ctypes.c_int, ctypes.POINTER(_vp)]),
     "r1_tensor_copy_from_host": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_copy_to_host": (ctypes.c_int, [_vp, _vp, _dp]),
+    "r1_tensor_frobenius": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_destroy": (ctypes.c_int, [_vp]),
     "r1_tensor_device_ptr": (_vp, [_vp]),
     "r1_blocks_numel": (ctypes.c_uint64, [_u64p, ctypes.c_int]),
@@ -106,6 +107,7 @@ SIGNATURES = {
                                                  ctypes.POINTER(ctypes.c_int)]),
     "r1_generate_config": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_uint64, _u64p,
                                           ctypes.c_int, ctypes.c_uint64]),
+    "r1_generate": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p, ctypes.c_uint64]),
     "r1_solve": (ctypes.c_int, [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(SolveOptionsC),
                                 ctypes.POINTER(SolveReportC)]),
     "r1_greedy_rank_r": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, ctypes.c_char_p,

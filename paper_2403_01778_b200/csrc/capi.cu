@@ -246,6 +246,21 @@ int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host) {
     });
 }
 
+// frobenius_norm (tensor.cpp:240-244), deterministic fixed-order device sum.
+int r1_tensor_frobenius(r1_context* ctx, const r1_tensor* t, double* out) {
+    return abi_guard([&] {
+        bind(ctx);
+        if (!t || !out) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceBuffer b;
+        b.ensure(64);
+        sumsq_device(ctx, t->dev, t->numel, b.as<double>());
+        double h = 0.0;
+        R1_CUDA(cudaMemcpyAsync(&h, b.ptr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = std::sqrt(h);
+    });
+}
+
 int r1_tensor_destroy(r1_tensor* t) {
     return abi_guard([&] {
         if (!t) return;

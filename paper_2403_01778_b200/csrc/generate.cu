@@ -15,7 +15,9 @@
 // ~1 ulp per entry; parity tests upload host-generated inputs instead.
 #include "common.cuh"
 
+#include <algorithm>
 #include <cmath>
+#include <string>
 #include <vector>
 
 namespace r1 {
@@ -127,6 +129,51 @@ std::vector<double> planted_factor(uint64_t seed, int k, uint64_t len) {
     return u;
 }
 
+// The reference's named generators (generators.cpp:50-116), 1-based multi-
+// indices in layout order.  exp / arcsin take their transcendental values from
+// host tables (std::exp / std::asin of the same arguments) and add them in the
+// reference's order without contraction: bit-identical.  tan and gaussian
+// evaluate tan / log / cos on the device (last-ulp differences from glibc).
+struct NamedArgs {
+    int kind;  // 0 gaussian, 1 exp, 2 arcsin, 3 tan
+    int order;
+    uint64_t dims[16];
+    uint64_t count;
+    uint64_t key;
+    const double* tab;  // exp: exp(-k), k = 0..maxdim; arcsin: asin table [j][idx]
+    uint64_t tab_stride;
+    double* out;
+};
+
+__global__ void named_gen_kernel(const NamedArgs a) {
+    for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < a.count;
+         p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double v = 0.0;
+        if (a.kind == 0) {
+            v = draw_gauss(a.key, p);
+        } else {
+            uint64_t q = p;
+            bool zero = false;
+            for (int j = 1; j <= a.order; ++j) {
+                const uint64_t idx = q % a.dims[j - 1] + 1;
+                q /= a.dims[j - 1];
+                const double sgn = ((j + 1) % 2 == 0) ? 1.0 : -1.0;
+                if (a.kind == 1) {
+                    v = __dadd_rn(v, __dmul_rn(sgn * static_cast<double>(j), a.tab[idx]));
+                } else if (a.kind == 2) {
+                    if (idx < static_cast<uint64_t>(j)) zero = true;
+                    else v = __dadd_rn(v, a.tab[(j - 1) * a.tab_stride + idx]);
+                } else {
+                    v = __dadd_rn(v, __ddiv_rn(sgn * static_cast<double>(idx), static_cast<double>(j)));
+                }
+            }
+            if (a.kind == 2 && zero) v = 0.0;
+            if (a.kind == 3) v = tan(v);
+        }
+        a.out[p] = v;
+    }
+}
+
 }  // namespace
 
 }  // namespace r1
@@ -214,6 +261,52 @@ int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
         const int g = 8 * ctx->num_sms;
         gen_kernel<<<g, 256, 0, ctx->stream>>>(a);
         check_launch(ctx, "gen_kernel");
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// generate(name, dims, seed) (generators.cpp:109-116) into `t` (its dims are
+// the tensor's dims): "gaussian" | "exp" | "arcsin" | "tan".
+int r1_generate(r1_context* ctx, r1_tensor* t, const char* name, uint64_t seed) {
+    return abi_guard([&] {
+        if (!ctx || !t || !name) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        const std::string nm(name);
+        NamedArgs a{};
+        a.kind = nm == "gaussian" ? 0 : nm == "exp" ? 1 : nm == "arcsin" ? 2 : nm == "tan" ? 3 : -1;
+        if (a.kind < 0) fail(R1_ERR_INVALID_ARGUMENT, "unknown generator: " + nm);
+        a.order = static_cast<int>(t->dims.size());
+        if (a.order < 2) fail(R1_ERR_INVALID_ARGUMENT, "generator: tensor order must be >= 2");
+        uint64_t maxd = 0;
+        for (int k = 0; k < a.order; ++k) {
+            a.dims[k] = t->dims[k];
+            maxd = std::max<uint64_t>(maxd, t->dims[k]);
+        }
+        a.count = t->numel;
+        a.key = rng_key(seed, 1);
+        a.out = t->dev;
+        DeviceBuffer tab;
+        std::vector<double> h;
+        if (a.kind == 1) {
+            h.resize(maxd + 1);
+            for (uint64_t k = 0; k <= maxd; ++k) h[k] = std::exp(-static_cast<double>(k));
+        } else if (a.kind == 2) {
+            a.tab_stride = maxd + 1;
+            h.assign(static_cast<size_t>(a.order) * a.tab_stride, 0.0);
+            for (int j = 1; j <= a.order; ++j)
+                for (uint64_t idx = static_cast<uint64_t>(j); idx <= maxd; ++idx) {
+                    const double sgn = (idx % 2 == 0) ? 1.0 : -1.0;
+                    h[(j - 1) * a.tab_stride + idx] =
+                        std::asin(sgn * static_cast<double>(j) / static_cast<double>(idx));
+                }
+        }
+        if (!h.empty()) {
+            tab.ensure(h.size() * sizeof(double));
+            R1_CUDA(cudaMemcpy(tab.ptr, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+            a.tab = tab.as<double>();
+        }
+        named_gen_kernel<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(a);
+        check_launch(ctx, "named_gen_kernel");
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
