@@ -127,6 +127,8 @@ EXTRA_SIGNATURES = {
                                            ctypes.POINTER(ctypes.c_int), _dp]),
     "r1x_sweep_plan_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_int64)]),
+    "r1x_ldlt": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.POINTER(ctypes.c_int), _dp, _dp,
+                                ctypes.POINTER(ctypes.c_int), _dp]),
 }
 
 _lib = None

@@ -23,6 +23,7 @@
 #include <cusolverDn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace r1 {
@@ -384,7 +385,13 @@ void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const d
 // One RQI step on the dense symmetric S (device, n x n, column-major) and x
 // (device).  Returns true and y (device, unit) when accepted, false for
 // std::nullopt.  Synchronous (the accept decision is a host branch).
+bool rqi_step_bk(r1_context* ctx, int64_t n, const double* S, const double* x, double* y);
+
 bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, double* y) {
+    // the hand-written Bunch-Kaufman (bk.cu); R1_RQI_CUSOLVER=1 selects the
+    // cuSOLVER dsytrf path kept for A/B checks
+    static const char* env = std::getenv("R1_RQI_CUSOLVER");
+    if (!(env && std::atoi(env) != 0)) return rqi_step_bk(ctx, n, S, x, y);
     cusolverDnHandle_t h = solver_handle(ctx);
     const size_t nn = static_cast<size_t>(n) * n;
     ctx->ws_rqi.ensure((nn + 4 * n + 128) * sizeof(double));
@@ -445,6 +452,48 @@ bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, doub
         check_launch(ctx, "normalize_check_kernel");
         int ok = 0;
         R1_CUDA(cudaMemcpyAsync(&ok, info + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ok) return true;
+    }
+    return false;
+}
+
+size_t bk_workspace_bytes(int64_t n, int num_sms);
+void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev);
+void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const double* x, double* y,
+              int* ok_dev);
+
+// rayleigh_quotient_step (sym_eig.cpp:411-438) on the hand-written
+// Bunch-Kaufman: rho = x'Sx, attempt(rho), then attempt(bumped) once.
+bool rqi_step_bk(r1_context* ctx, int64_t n, const double* S, const double* x, double* y) {
+    const size_t nn = static_cast<size_t>(n) * n;
+    ctx->ws_rqi.ensure((nn + 2 * n + 128) * sizeof(double));
+    double* W = ctx->ws_rqi.as<double>();
+    double* scal = W + nn;  // [0] rho, [1] bumped, [2] cond, [3] ||S||_F^2
+    int* okd = reinterpret_cast<int*>(scal + 8);
+    double* sx = scal + 16;
+    SolverHandle& H = handle_state(ctx);
+    H.work.ensure(bk_workspace_bytes(n, ctx->num_sms));
+    dense_matvec_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms))),
+                          256, 0, ctx->stream>>>(S, x, n, sx);
+    check_launch(ctx, "dense_matvec_kernel");
+    dot_device(ctx, x, sx, static_cast<uint64_t>(n), scal);
+    sumsq_device(ctx, S, nn, scal + 3);
+    bump_kernel<<<1, 1, 0, ctx->stream>>>(scal, scal + 3);
+    check_launch(ctx, "bump_kernel");
+    const int g = static_cast<int>(std::min<size_t>((nn + 255) / 256, ctx->num_sms * 16));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        shift_copy_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(S, W, n, scal + attempt);
+        check_launch(ctx, "shift_copy_kernel");
+        bk_factor(ctx, n, W, H.work.ptr, scal + 2);
+        double cond = 0.0;
+        R1_CUDA(cudaMemcpyAsync(&cond, scal + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (!(cond <= 1e14)) continue;  // singular or ill-conditioned shift (sym_eig.cpp:424)
+        bk_solve(ctx, n, W, H.work.ptr, x, y, okd);
+        int ok = 0;
+        R1_CUDA(cudaMemcpyAsync(&ok, okd, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
         if (ok) return true;
     }
