@@ -265,16 +265,24 @@ def run_b200(args):
     h2d = 8 * int(np.prod(dims)) + 8 * sum(dims)
     d2h = 8 * nb
 
-    # ---- time to converge (single GPU, tensor resident): HOSCF and iHOSCF, tol 1e-10
+    # ---- time to converge (tensor resident): HOSCF and iHOSCF, tol 1e-10.  One
+    # GPU: the C++ device driver; N GPUs: the slab-sharded driver (sweep per
+    # rank + NCCL exchange, replicated eigen / RQI / stopping test)
     ttc = None
-    if world == 1 and not args.skip_solve:
+    if not args.skip_solve:
+        from paper_2403_01778_b200.distributed import solve_distributed
         ttc = {}
         for alg in ("hoscf", "ihoscf"):
             o = r1.SolveOptions(tol=1e-10, max_iters=100, seed=CONFIG2_SEED)
             torch.cuda.synchronize()
+            barrier()
             ts = time.perf_counter()
-            rep = r1.solve(alg, t, o, ctx)
-            te = time.perf_counter() - ts
+            if world == 1:
+                rep = r1.solve(alg, t, o, ctx)
+            else:
+                rep = solve_distributed(alg, t, dims, o, dist, world, rank, ctx)
+            torch.cuda.synchronize()
+            te = max_over_ranks(time.perf_counter() - ts, dist)
             ttc[alg] = {"seconds": round(te, 6), "iterations": rep.iterations,
                         "sweeps": rep.total_sweeps, "converged": rep.converged,
                         "lambda": rep.result.lambda_,

@@ -204,6 +204,11 @@ int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_h
  * *accepted = 0 reproduces std::nullopt. */
 int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host,
                               const double* x_host, double* y_host, int* accepted);
+/* The same on the device block matrix J (blocks_dev as r1_build_j_device
+ * writes them), x_dev / y_dev device vectors of sum I_k: the RQI of a
+ * distributed solve, where J is replicated on every rank. */
+int r1_rqi_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
+                         const double* x_dev, double* y_dev, int* accepted);
 
 /* ---- synthetic inputs ----------------------------------------------------------- */
 /* Fill `t` with elements [first, first + numel(t)) of BASELINE config `cfg`

@@ -59,6 +59,7 @@ class Context:
 
     def set_stream(self, stream_ptr: Optional[int]):
         check(lib().r1_context_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)))
+        self.stream_ptr = stream_ptr or 0
 
     def synchronize(self):
         check(lib().r1_context_synchronize(self.handle))

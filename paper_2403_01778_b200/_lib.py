@@ -107,6 +107,8 @@ SIGNATURES = {
                                                  ctypes.POINTER(ctypes.c_int)]),
     "r1_generate_config": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_uint64, _u64p,
                                           ctypes.c_int, ctypes.c_uint64]),
+    "r1_rqi_blocks_device": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _vp, _vp, _vp,
+                                            ctypes.POINTER(ctypes.c_int)]),
     "r1_generate": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p, ctypes.c_uint64]),
     "r1_solve": (ctypes.c_int, [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(SolveOptionsC),
                                 ctypes.POINTER(SolveReportC)]),

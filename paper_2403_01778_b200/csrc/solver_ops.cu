@@ -291,6 +291,7 @@ Dims make_dims(const uint64_t* dims, int order) {
 struct SolverHandle {
     cusolverDnHandle_t h = nullptr;
     DeviceBuffer work, ipiv64, dwork, dop;  // RQI / dense-assembly scratch, reused
+    DeviceBuffer dense;                     // dense J for r1_rqi_blocks_device
     std::vector<char> hwork;
     std::vector<uint64_t> dop_dims;
     ~SolverHandle() {
@@ -501,3 +502,26 @@ bool rqi_step_bk(r1_context* ctx, int64_t n, const double* S, const double* x, d
 }
 
 }  // namespace r1
+
+using namespace r1;
+
+extern "C" {
+
+// One RQI step on the block matrix J (device blocks, replicated on every rank
+// of a distributed solve): dense J, then rayleigh_quotient_step
+// (sym_eig.cpp:411-438).  *accepted = 0 for std::nullopt.
+int r1_rqi_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
+                         const double* x_dev, double* y_dev, int* accepted) {
+    return abi_guard([&] {
+        if (!ctx || !dims || !accepted) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        int64_t n = 0;
+        for (int k = 0; k < order; ++k) n += static_cast<int64_t>(dims[k]);
+        SolverHandle& H = handle_state(ctx);
+        H.dense.ensure(static_cast<size_t>(n) * n * sizeof(double));
+        dense_from_blocks(ctx, dims, order, blocks_dev, H.dense.as<double>());
+        *accepted = rqi_step(ctx, n, H.dense.as<double>(), x_dev, y_dev) ? 1 : 0;
+    });
+}
+
+}  // extern "C"
