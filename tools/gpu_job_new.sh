@@ -1,2 +1,2 @@
 set -x
-timeout 900 python -m pytest tests/test_distributed_gpu.py -q -x 2>&1 | tail -15
+timeout 1200 python -m pytest tests/test_fullsize_gpu.py -q -x --durations=10 2>&1 | tail -15
