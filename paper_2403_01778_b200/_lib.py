@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "librank1_b200.so")
+# R1_LIB_PATH: development A/B runs against another build of this library
+LIB_PATH = os.environ.get("R1_LIB_PATH", os.path.join(PKG, "librank1_b200.so"))
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _u64p = ctypes.POINTER(ctypes.c_uint64)

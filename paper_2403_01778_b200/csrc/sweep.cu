@@ -408,10 +408,14 @@ struct BoxMaps {
 // consecutive merged rows NRA*l.. (NRA/2 128-bit LDS), all in one class, warp
 // w owns columns w + NWC*b.  Each thread copies its slice to registers and
 // releases the stage before computing.
-template <int NRA, int NCB, int NWC, bool STAGE_REGS>
+// KO > 1 (small faces): one box holds KO consecutive o-panels of the tile, so
+// the per-panel fixed work (barrier waits, the C0 block reduction, the C1
+// warp reduction) is paid once per KO panels; segments count o-groups.
+template <int NRA, int NCB, int NWC, bool STAGE_REGS, int KO>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     sweep3_box_kernel(const SweepArgs p, const __grid_constant__ BoxMaps maps, int nst,
                       int stage_dbl) {
+    static_assert(KO * NCB <= 32, "C1 reduction holds KO * NCB values per lane");
     static_assert(NRA % 2 == 0, "rows are read in pairs");
     constexpr int RMAX = 32 * NRA;
     constexpr int CMAX = NWC * NCB;
@@ -419,8 +423,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     extern __shared__ __align__(1024) double smem[];
     double* ring = smem;
     const int ring_dbl = nst * stage_dbl + RMAX;  // + slack for over-reads
-    double* red = smem + ring_dbl;                // [2][NWC][RMAX]
-    uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * NWC * RMAX);
+    double* red = smem + ring_dbl;                // [2][KO][NWC][RMAX]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * KO * NWC * RMAX);
     uint64_t* empty = full + kMaxStages;
     int4* meta = reinterpret_cast<int4*>(empty + kMaxStages);  // per stage {seg, tile, o, flags}
 
@@ -471,14 +475,14 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
                 const bool er = g0 == p.G0 - 1, ec = g1 == G1 - 1;
                 const uint32_t bytes = static_cast<uint32_t>(er ? rem0 : p.r0) *
-                                       static_cast<uint32_t>(ec ? rem1 : p.t1) * 8u;
+                                       static_cast<uint32_t>(ec ? rem1 : p.t1) * 8u * KO;
                 const CUtensorMap* map = &maps.m[(er ? 1 : 0) | (ec ? 2 : 0)];
                 for (int o = sg.o0; o < sg.o1; ++o) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     meta[stage] = make_int4(s, sg.tile, o,
                                             (o == sg.o0 ? kFirst : 0) | (o == sg.o1 - 1 ? kLast : 0));
                     mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_3d(ring + stage * stage_dbl, map, g0 * p.r0, g1 * p.t1, o,
+                    tma_load_3d(ring + stage * stage_dbl, map, g0 * p.r0, g1 * p.t1, o * KO,
                                 &full[stage], pol);
                     if (++stage == nst) {
                         stage = 0;
@@ -555,6 +559,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             P1row = p.P1 ? p.P1 + static_cast<int64_t>(g0) * p.P1_stride + R1s : nullptr;
         }
         {
+            if constexpr (KO == 1) {
             const double wo = __ldg(p.W + o);
             const double2* st = reinterpret_cast<const double2*>(ring + stage * stage_dbl);
             if (p.debug_mode == 1) {
@@ -644,6 +649,117 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
 #pragma unroll
                 for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX + i];
                 P0row[static_cast<int64_t>(o) * MI0 + i] = sum;
+            }
+            } else {
+            const double2* st = reinterpret_cast<const double2*>(ring + stage * stage_dbl);
+            if (p.debug_mode == 1) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                if (++stage == nst) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                continue;
+            }
+            const int ob = o * KO;          // first o-panel of the box
+            const int pstride = r0e * t1e / 2;  // double2 per panel in the box
+            double c0p[KO][NRA];
+            double c1v[KO * NCB];
+#pragma unroll
+            for (int k = 0; k < KO; ++k)
+#pragma unroll
+                for (int a = 0; a < NRA; ++a) c0p[k][a] = 0.0;
+#pragma unroll
+            for (int k = 0; k < KO; ++k) {
+                const double wo = __ldg(p.W + ob + k);
+                auto column = [&](int b, const double2* v) {
+                    double c1p = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        acc[2 * q][b] = fma(v[q].x, wo, acc[2 * q][b]);
+                        acc[2 * q + 1][b] = fma(v[q].y, wo, acc[2 * q + 1][b]);
+                        c1p = fma(v[q].x, u0r[2 * q], c1p);
+                        c1p = fma(v[q].y, u0r[2 * q + 1], c1p);
+                        c0p[k][2 * q] = fma(v[q].x, u1c[b], c0p[k][2 * q]);
+                        c0p[k][2 * q + 1] = fma(v[q].y, u1c[b], c0p[k][2 * q + 1]);
+                    }
+                    c1v[k * NCB + b] = c1p;
+                };
+                const double2* sp = st + k * pstride;
+                if constexpr (STAGE_REGS) {
+                    // copy the slice to registers; the last panel releases the stage
+                    double2 v[NCB][NP];
+#pragma unroll
+                    for (int b = 0; b < NCB; ++b)
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) v[b][q] = sp[coff[b] + (q ^ hsw)];
+                    if (k == KO - 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[stage]);
+                    }
+#pragma unroll
+                    for (int b = 0; b < NCB; ++b) column(b, v[b]);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < NCB; ++b) {
+                        double2 v[NP];
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) v[q] = sp[coff[b] + (q ^ hsw)];
+                        column(b, v);
+                    }
+                    if (k == KO - 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[stage]);
+                    }
+                }
+            }
+            if (++stage == nst) {
+                stage = 0;
+                phase ^= 1;
+            }
+
+            if (P1row) {
+                // C1 of merged column j, class c = real column K j + c, stored
+                // class-major (c MI1 + j) so the second stage reads only the
+                // classes a row tile holds; a tile spanning several classes
+                // reduces each class's lanes separately.  Value index kb = panel
+                // k * NCB + column slot b.
+                constexpr int NV = KO * NCB;
+                int col;
+                if (cls_lo == cls_hi) {
+                    const double c1 = warp_transpose_sum<NV>(c1v, lane, &col);
+                    const int k = col / NCB, j = warp + NWC * (col % NCB);
+                    if ((lane & (32 / NV - 1)) == 0 && j < t1e)
+                        P1row[static_cast<int64_t>(ob + k) * I1 + cls_lo * MI1 + j] = c1;
+                } else {
+                    for (int c = cls_lo; c <= cls_hi; ++c) {
+                        double mv[NV];
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) mv[v] = pcls == c ? c1v[v] : 0.0;
+                        const double c1 = warp_transpose_sum<NV>(mv, lane, &col);
+                        const int k = col / NCB, j = warp + NWC * (col % NCB);
+                        if ((lane & (32 / NV - 1)) == 0 && j < t1e)
+                            P1row[static_cast<int64_t>(ob + k) * I1 + c * MI1 + j] = c1;
+                    }
+                }
+            }
+
+#pragma unroll
+            for (int k = 0; k < KO; ++k) {
+                double2* rb = reinterpret_cast<double2*>(red + ((rbuf * KO + k) * NWC + warp) * RMAX) +
+                              (NRA / 2) * lane;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) rb[q ^ hsw] = make_double2(c0p[k][2 * q], c0p[k][2 * q + 1]);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory");
+            const double* rr = red + rbuf * KO * NWC * RMAX;
+            for (int x = threadIdx.x; x < KO * r0e; x += NWC * 32) {
+                const int k = x / r0e, i = x - k * r0e;
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWC; ++w) sum += rr[(k * NWC + w) * RMAX + i];
+                P0row[static_cast<int64_t>(ob + k) * MI0 + i] = sum;
+            }
             }
             rbuf ^= 1;
             if (md.w & kLast) {
@@ -821,6 +937,7 @@ struct Level {
     // view & tiling
     int64_t I0 = 0, I1 = 0, O = 0;
     int K = 1;                 // alignment classes merged per column (box kernel)
+    int KO = 1;                // o-panels per box (small faces); segments count o-groups
     int64_t MI0 = 0, MI1 = 0;  // merged view K I0 x I1/K (tiles live here)
     int nra = 4, ncb = 8, stages = 3;
     int stage_dbl = 0;
@@ -910,9 +1027,20 @@ void tile_level(Level& L, int num_sms) {
         L.t1 = static_cast<int>((L.MI1 + L.G1 - 1) / L.G1);
         L.G1 = static_cast<int>((L.MI1 + L.t1 - 1) / L.t1);
         L.ntiles = L.G0 * L.G1;
-        const size_t red = static_cast<size_t>(2) * kBoxNWC * rm * 8;
+        // a single small face tile: KO panels per box amortise the per-panel
+        // reductions (C4: 60 x 60 faces)
+        L.KO = 1;
+        static const char* ko_env = std::getenv("R1_SWEEP_KO");
+        const int ko_max = ko_env ? std::atoi(ko_env) : 2;  // measured: 2 beats 4 on C4
+        if (L.ntiles == 1 && L.r0 * L.t1 <= 64 * 64 && L.nra == 2)
+            for (int ko = ko_max; ko > 1; ko >>= 1)
+                if (L.O % ko == 0) {
+                    L.KO = ko;
+                    break;
+                }
+        const size_t red = static_cast<size_t>(2) * L.KO * kBoxNWC * rm * 8;
         const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16;
-        const size_t box = static_cast<size_t>(L.r0) * L.t1 * 8;
+        const size_t box = static_cast<size_t>(L.r0) * L.t1 * 8 * L.KO;
         const size_t ring = kSmemBudget - red - bars - rm * 8 - 1024;
         L.stages = static_cast<int>(std::min<size_t>(kMaxStages, ring / box));
         L.stage_dbl = static_cast<int>(((box + 127) & ~size_t(127)) / 8);  // 128-B aligned
@@ -939,7 +1067,8 @@ void tile_level(Level& L, int num_sms) {
 // Partition (tile, o) panels into ncta contiguous chunks of equal cost and
 // cut them into segments (maximal runs inside one tile).
 void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
-    const int64_t npanels = static_cast<int64_t>(L.ntiles) * L.O;
+    const int64_t Og = L.O / L.KO;  // o-groups (KO panels each)
+    const int64_t npanels = static_cast<int64_t>(L.ntiles) * Og;
     auto panel_cost = [&](int tile) {
         const int g0 = tile % L.G0, g1 = tile / L.G0;
         const int64_t r = std::min<int64_t>(L.r0, L.MI0 - int64_t(g0) * L.r0);
@@ -948,7 +1077,7 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
         return static_cast<double>(r * c) + 512.0;
     };
     double total = 0.0;
-    for (int t = 0; t < L.ntiles; ++t) total += panel_cost(t) * static_cast<double>(L.O);
+    for (int t = 0; t < L.ntiles; ++t) total += panel_cost(t) * static_cast<double>(Og);
     // Enough CTAs to fill the chip, but at least ~16 panels each.
     int64_t ncta = std::min<int64_t>(num_sms, std::max<int64_t>(1, npanels / 16));
     L.ncta = static_cast<int>(ncta);
@@ -969,7 +1098,7 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     bool in_dyn = false;
     for (int t = 0; t < L.ntiles; ++t) {
         const double c = panel_cost(t);
-        for (int64_t o = 0; o < L.O; ++o) {
+        for (int64_t o = 0; o < Og; ++o) {
             if (!in_dyn && dyn && x + 0.5 * c >= static_total) {
                 in_dyn = true;
                 while (cur < L.ncta) cta_seg[++cur] = static_cast<int>(segs.size());
@@ -1140,7 +1269,8 @@ EncodeTiledFn encode_fn() {
 }
 
 // 3-D map over the view A[i0, i1, o] (fp64, no swizzle, zero OOB fill).
-CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t box_cols) {
+CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t box_cols,
+                     int64_t box_depth = 1) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(L.MI0), static_cast<cuuint64_t>(L.MI1),
@@ -1148,7 +1278,7 @@ CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t 
     const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(L.MI0) * 8,
                                    static_cast<cuuint64_t>(L.I0) * L.I1 * 8};
     const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols),
-                               1};
+                               static_cast<cuuint32_t>(box_depth)};
     const cuuint32_t estride[3] = {1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), gdim,
                              gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1171,10 +1301,10 @@ void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const C
     check_launch(ctx, "sweep3_kernel");
 }
 
-template <int NRA, bool SR>
+template <int NRA, bool SR, int KO>
 void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
     static int configured_device = -1;
-    auto kern = sweep3_box_kernel<NRA, kBoxNCB, kBoxNWC, SR>;
+    auto kern = sweep3_box_kernel<NRA, kBoxNCB, kBoxNWC, SR, KO>;
     if (configured_device != ctx->device) {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBudget)));
@@ -1183,10 +1313,10 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
     BoxMaps maps;
     const int64_t rem0 = L.MI0 - static_cast<int64_t>(L.G0 - 1) * L.r0;
     const int64_t rem1 = L.MI1 - static_cast<int64_t>(L.G1 - 1) * L.t1;
-    maps.m[0] = make_map(a.A, L, L.r0, L.t1);
-    maps.m[1] = make_map(a.A, L, rem0, L.t1);
-    maps.m[2] = make_map(a.A, L, L.r0, rem1);
-    maps.m[3] = make_map(a.A, L, rem0, rem1);
+    maps.m[0] = make_map(a.A, L, L.r0, L.t1, KO);
+    maps.m[1] = make_map(a.A, L, rem0, L.t1, KO);
+    maps.m[2] = make_map(a.A, L, L.r0, rem1, KO);
+    maps.m[3] = make_map(a.A, L, rem0, rem1, KO);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool timed = ctx->time_kernels && a.trace_level0;
     if (timed) {
@@ -1208,11 +1338,17 @@ void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
         static const char* sr = std::getenv("R1_SWEEP_STAGE_REGS");
         const bool stage_regs = sr ? std::atoi(sr) != 0 : true;
         if (L.nra == 4) {
-            if (stage_regs) launch_box<4, true>(ctx, L, a);
-            else launch_box<4, false>(ctx, L, a);
+            if (stage_regs) launch_box<4, true, 1>(ctx, L, a);
+            else launch_box<4, false, 1>(ctx, L, a);
+        } else if (L.KO == 4) {
+            if (stage_regs) launch_box<2, true, 4>(ctx, L, a);
+            else launch_box<2, false, 4>(ctx, L, a);
+        } else if (L.KO == 2) {
+            if (stage_regs) launch_box<2, true, 2>(ctx, L, a);
+            else launch_box<2, false, 2>(ctx, L, a);
         } else {
-            if (stage_regs) launch_box<2, true>(ctx, L, a);
-            else launch_box<2, false>(ctx, L, a);
+            if (stage_regs) launch_box<2, true, 1>(ctx, L, a);
+            else launch_box<2, false, 1>(ctx, L, a);
         }
     } else {
         CUtensorMap m;
@@ -1377,6 +1513,7 @@ void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* 
     info[8] = static_cast<int64_t>(L.smem);
     info[9] = L.nra;
     info[10] = L.K;
+    info[11] = L.KO;
 }
 
 }  // namespace r1

@@ -17,6 +17,8 @@ SHAPES = [
     # K = 2 and 4 at several row-tile counts, recursion levels with K > 1
     (20, 8, 5), (200, 10, 7), (500, 8, 3), (60, 60, 9), (1000, 4, 3), (60, 8, 5, 3),
     (40, 12, 6, 2), (100, 4, 2, 2, 2),
+    # small single-tile faces: KO o-panels per box (KO = 2 and 4)
+    (30, 20, 6), (64, 60, 12), (8, 6, 4, 2, 3),
 ]
 
 
