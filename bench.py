@@ -274,16 +274,20 @@ def run_b200(args):
         ttc = {}
         for alg in ("hoscf", "ihoscf"):
             o = r1.SolveOptions(tol=1e-10, max_iters=100, seed=CONFIG2_SEED)
-            torch.cuda.synchronize()
-            barrier()
-            ts = time.perf_counter()
-            if world == 1:
-                rep = r1.solve(alg, t, o, ctx)
-            else:
-                rep = solve_distributed(alg, t, dims, o, dist, world, rank, ctx)
-            torch.cuda.synchronize()
-            te = max_over_ranks(time.perf_counter() - ts, dist)
-            ttc[alg] = {"seconds": round(te, 6), "iterations": rep.iterations,
+            runs = []
+            for _ in range(3):  # first run includes one-time plan / workspace setup
+                torch.cuda.synchronize()
+                barrier()
+                ts = time.perf_counter()
+                if world == 1:
+                    rep = r1.solve(alg, t, o, ctx)
+                else:
+                    rep = solve_distributed(alg, t, dims, o, dist, world, rank, ctx)
+                torch.cuda.synchronize()
+                runs.append(max_over_ranks(time.perf_counter() - ts, dist))
+            te = statistics.median(runs[1:])
+            ttc[alg] = {"seconds": round(te, 6), "seconds_first_call": round(runs[0], 6),
+                        "iterations": rep.iterations,
                         "sweeps": rep.total_sweeps, "converged": rep.converged,
                         "lambda": rep.result.lambda_,
                         "t_build_j": round(rep.wall_build_j(), 6), "t_eig": round(rep.wall_eig(), 6)}
@@ -415,11 +419,16 @@ def other_configs(r1, _lib, ctx, stream):
             if init == "provided":  # C1: normalised all-ones (BASELINE config 1)
                 o.init = "provided"
                 o.init_factors = [np.ones(d) for d in dims]
-            torch.cuda.synchronize()
-            ts = time.perf_counter()
-            rep = r1.solve(alg, t, o, ctx)
-            te = time.perf_counter() - ts
-            entry[alg] = {"seconds": round(te, 6), "iterations": rep.iterations,
+            runs = []
+            for _ in range(2 if cfg in (1, 3) else 3):  # first run: one-time setup
+                torch.cuda.synchronize()
+                ts = time.perf_counter()
+                rep = r1.solve(alg, t, o, ctx)
+                torch.cuda.synchronize()
+                runs.append(time.perf_counter() - ts)
+            te = statistics.median(runs[1:])
+            entry[alg] = {"seconds": round(te, 6), "seconds_first_call": round(runs[0], 6),
+                          "iterations": rep.iterations,
                           "sweeps": rep.total_sweeps, "converged": rep.converged,
                           "lambda": rep.result.lambda_, "t_build_j": round(rep.wall_build_j(), 6),
                           "t_eig": round(rep.wall_eig(), 6), "options": {k: v for k, v in kw.items()

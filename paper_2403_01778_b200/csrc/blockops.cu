@@ -73,8 +73,8 @@ __global__ void mv_phase_b_kernel(const BlockOp* __restrict__ op, double* __rest
 
 struct MvPlan {
     BlockOp op;
-    DeviceBuffer dop, coldot, rowpart;
-    const double* blocks = nullptr;
+    DeviceBuffer coldot, rowpart;
+    DescCache<BlockOp> dop;  // one device descriptor per block buffer in use
 };
 
 std::map<std::pair<r1_context*, std::vector<uint64_t>>, std::shared_ptr<MvPlan>>& mv_plans() {
@@ -106,27 +106,22 @@ void block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double
                   const double* x, double* y) {
     if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "block_matvec: bad order");
     auto& P = mv_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
-    if (!P || P->blocks != blocks) {
-        if (!P) {
-            P = std::make_shared<MvPlan>();
-            int64_t cn = 0, rn = 0;
-            blockop_layout(P->op, dims, order, &cn, &rn);
-            P->coldot.ensure(std::max<int64_t>(cn, 1) * sizeof(double));
-            P->rowpart.ensure(std::max<int64_t>(rn, 1) * sizeof(double));
-            P->op.coldot = P->coldot.as<double>();
-            P->op.rowpart = P->rowpart.as<double>();
-            P->dop.ensure(sizeof(BlockOp));
-        }
-        P->blocks = blocks;
-        P->op.blocks = blocks;
-        R1_CUDA(cudaMemcpyAsync(P->dop.ptr, &P->op, sizeof(BlockOp), cudaMemcpyHostToDevice,
-                                ctx->stream));
+    if (!P) {
+        P = std::make_shared<MvPlan>();
+        int64_t cn = 0, rn = 0;
+        blockop_layout(P->op, dims, order, &cn, &rn);
+        P->coldot.ensure(std::max<int64_t>(cn, 1) * sizeof(double));
+        P->rowpart.ensure(std::max<int64_t>(rn, 1) * sizeof(double));
+        P->op.coldot = P->coldot.as<double>();
+        P->op.rowpart = P->rowpart.as<double>();
     }
+    P->op.blocks = blocks;
+    const BlockOp* dop = P->dop.get(P->op, ctx->stream);
     const int ga = std::max(1, std::min(P->op.ntasks, 4 * ctx->num_sms));
-    mv_phase_a_kernel<<<ga, 256, 0, ctx->stream>>>(P->dop.as<BlockOp>(), x);
+    mv_phase_a_kernel<<<ga, 256, 0, ctx->stream>>>(dop, x);
     check_launch(ctx, "mv_phase_a_kernel");
     const int gb = static_cast<int>(std::min<int64_t>((P->op.n + 255) / 256, 1024));
-    mv_phase_b_kernel<<<std::max(gb, 1), 256, 0, ctx->stream>>>(P->dop.as<BlockOp>(), y);
+    mv_phase_b_kernel<<<std::max(gb, 1), 256, 0, ctx->stream>>>(dop, y);
     check_launch(ctx, "mv_phase_b_kernel");
 }
 

@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include <cstdint>
 #include <cstdio>
 #include <map>
@@ -82,6 +84,34 @@ struct DeviceBuffer {
     template <typename T>
     T* as() const {
         return static_cast<T*>(ptr);
+    }
+};
+
+// Device copies of small host descriptors (BlockOp ...) keyed by content: a
+// descriptor uploaded before is reused, so the hot loops (HOSCF alternates two
+// block buffers) do no pageable host-to-device copy — which would make the host
+// wait for the stream.  Users share one stream, so reusing a slot is ordered
+// after the kernels that read it.
+template <typename T, int N = 4>
+struct DescCache {
+    T host[N];
+    bool used[N] = {};
+    int next = 0;
+    void* dev[N] = {};
+    ~DescCache() {
+        for (auto p : dev)
+            if (p) cudaFree(p);
+    }
+    const T* get(const T& d, cudaStream_t s) {
+        for (int i = 0; i < N; ++i)
+            if (used[i] && std::memcmp(&host[i], &d, sizeof(T)) == 0) return static_cast<T*>(dev[i]);
+        const int i = next;
+        next = (next + 1) % N;
+        std::memcpy(&host[i], &d, sizeof(T));
+        used[i] = true;
+        if (!dev[i]) R1_CUDA(cudaMalloc(&dev[i], sizeof(T)));
+        R1_CUDA(cudaMemcpyAsync(dev[i], &host[i], sizeof(T), cudaMemcpyHostToDevice, s));
+        return static_cast<T*>(dev[i]);
     }
 };
 

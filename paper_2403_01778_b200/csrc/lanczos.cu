@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
 
 struct EigPlan {
     BlockOp op;
-    DeviceBuffer dop;
+    DescCache<BlockOp> dop;
     int64_t coldot_n = 0, rowpart_n = 0;
 };
 
@@ -613,10 +613,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     BlockOp op = P.op;
     op.coldot = take(std::max<int64_t>(P.coldot_n, 1));
     op.rowpart = take(std::max<int64_t>(P.rowpart_n, 1));
-    P.dop.ensure(sizeof(BlockOp));
-    R1_CUDA(cudaMemcpyAsync(P.dop.ptr, &op, sizeof(BlockOp), cudaMemcpyHostToDevice,
-                            ctx->stream));
-    a.op = P.dop.as<BlockOp>();
+    a.op = P.dop.get(op, ctx->stream);
     a.out_value = value_dev;
     a.out_vec = vec_dev;
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));

@@ -292,6 +292,7 @@ struct SolverHandle {
     cusolverDnHandle_t h = nullptr;
     DeviceBuffer work, ipiv64, dwork, dop;  // RQI / dense-assembly scratch, reused
     DeviceBuffer dense;                     // dense J for r1_rqi_blocks_device
+    DescCache<BlockOp> dops;                // block-operator descriptors (dense assembly)
     std::vector<char> hwork;
     std::vector<uint64_t> dop_dims;
     ~SolverHandle() {
@@ -369,17 +370,14 @@ void flip_first(r1_context* ctx, double* u0, int64_t n0, const double* lam_in, d
 void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                        double* S) {
     SolverHandle& H = handle_state(ctx);
-    static thread_local BlockOp op;  // host staging must outlive the async copy
+    BlockOp op{};
     int64_t cn, rn;
-    op = BlockOp{};
     blockop_layout(op, dims, order, &cn, &rn);
     op.blocks = blocks;
-    H.dop.ensure(sizeof(BlockOp));
-    R1_CUDA(cudaMemcpyAsync(H.dop.ptr, &op, sizeof(BlockOp), cudaMemcpyHostToDevice, ctx->stream));
-    R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    const BlockOp* dop = H.dops.get(op, ctx->stream);
     const int64_t nn = op.n * op.n;
     const int g = static_cast<int>(std::min<int64_t>((nn + 255) / 256, ctx->num_sms * 16));
-    dense_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(H.dop.as<BlockOp>(), S);
+    dense_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(dop, S);
     check_launch(ctx, "dense_kernel");
 }
 
