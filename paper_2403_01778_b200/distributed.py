@@ -84,6 +84,11 @@ def exchange(local_blocks, dims, world: int, rank: int, dist, out):
             if world == 1:
                 out[s.offset:s.offset + s.rows * s.cols].copy_(mine)
                 continue
+            if dims[-1] % world == 0:
+                # even slabs: rank r's columns are the r-th chunk of the
+                # column-major block, so NCCL gathers straight into place
+                dist.all_gather_into_tensor(out[s.offset:s.offset + s.rows * s.cols], mine)
+                continue
             padded = torch.zeros(s.rows * maxs, dtype=local_blocks.dtype, device=local_blocks.device)
             padded[:mine.numel()].copy_(mine)
             gathered = torch.empty(world * s.rows * maxs, dtype=local_blocks.dtype,

@@ -89,3 +89,13 @@ def test_exchange_numpy_reference():
         locs.append(O.build_j_numpy(slab, local_dims(dims, lo, hi), list(f[:-1]) + [f[-1][lo:hi]]))
     np.testing.assert_allclose(exchange_numpy(locs, dims),
                                O.build_j_numpy(a.reshape(-1, order="F"), dims, f), rtol=1e-12, atol=1e-12)
+
+
+def test_driver_init_factors_match_reference():
+    """The distributed driver's uniform01 init (solvers.cpp:34-49) equals the
+    oracle's (pinned to the reference)."""
+    from oracle import rank1_oracle as O
+    from paper_2403_01778_b200.distributed import random_unit_factors
+    for dims, seed in [((4, 5, 6), 3), ((10, 2), 0)]:
+        for a, b in zip(random_unit_factors(dims, seed, 2), O.random_unit_factors(dims, seed, 2)):
+            np.testing.assert_allclose(a, b, rtol=1e-15)

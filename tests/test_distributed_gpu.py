@@ -33,10 +33,3 @@ def test_distributed_driver_matches_single_gpu(gpu_ctx, oracle, ref, alg, dims, 
     if got.iterations == want["iterations"]:
         for u, v in zip(got.result.factors, want["factors"]):
             assert min(np.max(np.abs(u - v)), np.max(np.abs(u + v))) <= 1e-8
-
-
-def test_random_unit_factors_match_device_init(oracle):
-    from paper_2403_01778_b200.distributed import random_unit_factors
-    for dims, seed in [((4, 5, 6), 3), ((10, 2), 0)]:
-        for a, b in zip(random_unit_factors(dims, seed, 2), oracle.random_unit_factors(dims, seed, 2)):
-            np.testing.assert_allclose(a, b, rtol=1e-15)
