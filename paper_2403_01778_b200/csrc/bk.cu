@@ -456,12 +456,18 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         cl.sync();
         mark(2);
         if (warp == 0) {
+            // all remote reads issued together: lanes < G the partials, lanes
+            // 16 / 17 the scalars c_k(k), c_k(k+1)
             double v = -1.0, sg = 0.0;
             int64_t ii = n;
             if (lane < G) {
                 v = *cl.map_shared_rank(&pub_v, lane);
                 ii = *cl.map_shared_rank(&pub_i, lane);
                 sg = *cl.map_shared_rank(&pub_s, lane);
+            } else if (lane == 16) {
+                g_sc[0] = *cl.map_shared_rank(&scal[0], owner(k));
+            } else if (lane == 17) {
+                g_sc[1] = k + 1 < n ? *cl.map_shared_rank(&scal[1], owner(k + 1)) : 0.0;
             }
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) {
@@ -478,10 +484,6 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 g_colmax = v;
                 g_imax = ii;
                 g_ckimax = sg;
-            } else if (lane == 1) {
-                g_sc[0] = *cl.map_shared_rank(&scal[0], owner(k));
-            } else if (lane == 2) {
-                g_sc[1] = k + 1 < n ? *cl.map_shared_rank(&scal[1], owner(k + 1)) : 0.0;
             }
         }
         __syncthreads();
@@ -536,13 +538,14 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
             mark(4);
             cl.sync();
             if (warp == 0) {
-                double v = lane < G ? *cl.map_shared_rank(&pub_rv, lane) : 0.0;
+                double v = 0.0;
+                if (lane < G) v = *cl.map_shared_rank(&pub_rv, lane);
+                else if (lane == 16) g_sc[2] = *cl.map_shared_rank(&scal[2], owner(imax));
+                else if (lane == 17) g_sc[3] = *cl.map_shared_rank(&scal[3], owner(k));
+                else if (lane == 18) g_sc[4] = k + 1 < n ? *cl.map_shared_rank(&scal[4], owner(k + 1)) : 0.0;
 #pragma unroll
                 for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
                 if (lane == 0) g_rowmax = v;
-                else if (lane == 1) g_sc[2] = *cl.map_shared_rank(&scal[2], owner(imax));
-                else if (lane == 2) g_sc[3] = *cl.map_shared_rank(&scal[3], owner(k));
-                else if (lane == 3) g_sc[4] = k + 1 < n ? *cl.map_shared_rank(&scal[4], owner(k + 1)) : 0.0;
             }
             __syncthreads();
             const double rowmax = fmax(g_rowmax, 0.0);
