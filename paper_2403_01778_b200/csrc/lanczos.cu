@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
 
     int restarts = 0, breakdowns = 0;
     int j = 0;
+    bool zero_op = false;
     double anorm = 0.0;
     double inv_beta = 1.0;  // V[:,j] = w * inv_beta for j > 0 (materialised in phase B)
     for (;;) {
@@ -448,6 +449,13 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         }
         double nrm = sqrt(grid_sum(a.part, 0));
         anorm = fmax(anorm, fabs(alpha) + nrm + (j > 0 ? a.beta[j - 1] : 0.0));
+        if (j == 0 && restarts == 0 && anorm == 0.0) {
+            // J v0 == 0 for a dense random v0: J is the zero matrix.  The
+            // reference's full decomposition then returns the identity's last
+            // column for the picked (highest) end (sym_eig.cpp:206-229).
+            zero_op = true;
+            break;
+        }
         const bool space_full = (j + 1 == n);
         const bool breakdown = !space_full && nrm <= 1e-13 * anorm;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -494,6 +502,18 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         }
     }
 
+    if (zero_op) {
+        for (int64_t i = gtid; i < n; i += gstride) a.out_vec[i] = i == n - 1 ? 1.0 : 0.0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            *a.out_value = 0.0;
+            a.ctl[0] = 1;
+            a.ctl[1] = 1;
+            a.ctl[2] = 1;
+            a.ctl[3] = 0;
+            a.ctl[4] = 0;
+        }
+        return;
+    }
     // ---- Ritz vector of the picked end
     const int m = j;
     const int pick = a.ctl[1];
