@@ -188,6 +188,10 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
     __shared__ double lohi[4];  // [a_lo, b_lo, a_hi, b_hi] intervals
     __shared__ int cnt[kEigThreads];
     __shared__ double theta[2];
+    // alpha/beta[m-1] were stored by thread 0 of this CTA: order them before the reads
+    __threadfence_block();
+    __syncthreads();
+
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         ta[i] = a.alpha[i];
         tb[i] = i + 1 < m ? a.beta[i] : 0.0;
@@ -215,20 +219,31 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
     const int side = threadIdx.x < half ? 0 : 1;  // 0: lowest, 1: highest
     const int k = threadIdx.x - side * half;
     __shared__ int found[2];
+    auto narrow = [&](int sd) {
+        const double lo = lohi[2 * sd], hi = lohi[2 * sd + 1];
+        return !(hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300);
+    };
     for (int round = 0; round < 10; ++round) {
+        // every thread takes every barrier: the two halves may finish in
+        // different rounds, so a finished half idles instead of leaving
+        if (!narrow(0) && !narrow(1)) break;  // uniform: read after a barrier
+        const bool active = narrow(side);
         const double lo = lohi[2 * side], hi = lohi[2 * side + 1];
-        if (hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300) break;  // uniform per CTA
-        const double x = lo + (hi - lo) * static_cast<double>(k + 1) / static_cast<double>(half + 1);
-        cnt[threadIdx.x] = sturm_count(ta, tb, m, x, pivmin);
+        if (active) {
+            const double x = lo + (hi - lo) * static_cast<double>(k + 1) / static_cast<double>(half + 1);
+            cnt[threadIdx.x] = sturm_count(ta, tb, m, x, pivmin);
+        }
         if (k == 0) found[side] = half;
         __syncthreads();
         // lowest: first point with count >= 1; highest: first with count >= m
         const int target = side == 0 ? 1 : m;
-        const bool hit = cnt[threadIdx.x] >= target;
-        const bool prev = k > 0 && cnt[threadIdx.x - 1] >= target;
-        if (hit && !prev) found[side] = k;  // counts are monotone: one writer
+        if (active) {
+            const bool hit = cnt[threadIdx.x] >= target;
+            const bool prev = k > 0 && cnt[threadIdx.x - 1] >= target;
+            if (hit && !prev) found[side] = k;  // counts are monotone: one writer
+        }
         __syncthreads();
-        if (k == 0) {
+        if (k == 0 && active) {
             const int f = found[side];
             const double nlo = f == 0 ? lo : lo + (hi - lo) * static_cast<double>(f) / (half + 1);
             const double nhi =
@@ -640,6 +655,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.op = P.dop.get(op, ctx->stream);
     a.out_value = value_dev;
     a.out_vec = vec_dev;
+
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
     static int configured = -1;
     if (configured != ctx->device) {
@@ -676,6 +692,14 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
         R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        static const bool dbg_t = std::getenv("R1_DEBUG_EIG_T") != nullptr;
+        if (dbg_t) {
+            std::vector<double> al(ctl[2]), be(ctl[2]);
+            R1_CUDA(cudaMemcpy(al.data(), a.alpha, al.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            R1_CUDA(cudaMemcpy(be.data(), a.beta, be.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int k = 0; k < std::min(ctl[2], 24); ++k)
+                std::fprintf(stderr, "  T[%d] alpha=%.6e beta=%.6e\n", k, al[k], be[k]);
+        }
         std::fprintf(stderr,
                      "[r1 eig] n=%lld conv=%d pick=%d steps=%d restarts=%d breakdowns=%d "
                      "lo=%.17g hi=%.17g res_lo=%.3g res_hi=%.3g | us: A=%.1f syncA=%.1f B=%.1f "
