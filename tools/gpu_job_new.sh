@@ -1,4 +1,5 @@
-for G in 1 148; do
-R1_EIG_GRID=$G R1_DEBUG_EIG=1 timeout 120 python tools/eig_dense_probe.py 120 129 131 140 2>&1 | grep -E "r1 eig" | awk '{print $3, $6, $7, $8, $9}'
+export PATH=/usr/local/cuda/bin:$PATH
+for tool in memcheck synccheck racecheck; do
+echo "== $tool"
+timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_probe.py 2>&1 | grep -vE "^(hoscf|ihoscf|asvd|eig|rqi|greedy) " | tail -25
 done
-timeout 900 python -m pytest tests/test_nepv_props_gpu.py tests/test_solver_gpu.py tests/test_solver_props_gpu.py tests/test_baselines_gpu.py -q 2>&1 | tail -2
