@@ -19,6 +19,9 @@ SHAPES = [
     (40, 12, 6, 2), (100, 4, 2, 2, 2),
     # small single-tile faces: KO o-panels per box (KO = 2 and 4)
     (30, 20, 6), (64, 60, 12), (8, 6, 4, 2, 3),
+    # extreme aspect ratios: a long fastest mode, a tiny face with a long
+    # outer mode, unit modes
+    (100000, 3, 2), (2, 2, 50000), (1, 1, 1, 1, 1000), (5000, 1, 7), (1, 4000, 3),
 ]
 
 
