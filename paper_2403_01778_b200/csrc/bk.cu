@@ -308,10 +308,6 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_kernel(const BkArgs a) {
 // costs two cluster barriers (three on the imax path) and no global re-reads
 // of the updated columns.  W rows exchanged by an interchange move through
 // DSMEM and land at the top of the next column.
-constexpr int kPubS = 3 * 16;  // per-CTA (|v|, index, signed v) for <= 16 CTAs
-constexpr int kPubScal = kPubS;      // 8 published scalars
-constexpr int kPubRow = kPubS + 8;   // per-CTA rowmax partials
-
 __device__ void block_argmax3(double& v, int64_t& i, double& sgn, double* sv, int64_t* si,
                               double* ss) {
 #pragma unroll

@@ -19,14 +19,17 @@
 //   I0x) smaller, handled by recursion (the reference's reuse_intermediates
 //   idea, nepv.cpp:174-195, applied to the fused pass).
 //
-// Kernel: persistent, one CTA per SM; the CTA owns a face tile (r0 x t1 of
-// (i0,i1)) and a contiguous run of o.  A producer warp streams the tile's
-// column runs HBM -> shared memory with cp.async.bulk (TMA bulk copies,
-// L2 evict_first) into a STAGES-deep ring guarded by mbarriers; 8 consumer
-// warps keep the B01 face tile in registers, reduce C1 with a transposing warp
-// butterfly and C0 through shared memory.  C0/C1 partials over face tiles go
-// to a workspace and are summed in a fixed order by a second kernel: no
-// atomics anywhere, so results are bit-reproducible run to run.
+// Kernels: sweep3_box_kernel — persistent, one CTA per SM, one
+// producer warp streaming (tile, o) panels HBM -> shared memory with 3-D TMA
+// tensor-map loads (cp.async.bulk.tensor, L2 evict_first) into a byte-budgeted
+// mbarrier ring, 15 consumer warps keeping the B01 face tile in registers,
+// reducing C1 with a transposing warp butterfly and C0 through shared memory;
+// tiles are cut in whole 128-B lines (alignment classes), small faces put KO
+// o-panels in one box, the last 25% of the panels are scheduled dynamically.
+// sweep3_kernel — the 1-D cp.async.bulk variant for odd I0 (no 16-B TMA
+// stride).  C0/C1/B01 partials over tiles / segments go to a workspace and are
+// summed in a fixed order by finish_kernel: no atomics anywhere, so results are
+// bit-reproducible run to run.
 #include "common.cuh"
 
 #include <cuda.h>
@@ -144,14 +147,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)),
         "l"(pol)
         : "memory");
-}
-
-// L2 prefetch of a 3-D box (no smem, no completion tracking).
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
 }
 
 __device__ __forceinline__ void consumer_bar() {
@@ -418,7 +413,6 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     static_assert(KO * NCB <= 32, "C1 reduction holds KO * NCB values per lane");
     static_assert(NRA % 2 == 0, "rows are read in pairs");
     constexpr int RMAX = 32 * NRA;
-    constexpr int CMAX = NWC * NCB;
     constexpr int NP = NRA / 2;
     extern __shared__ __align__(1024) double smem[];
     double* ring = smem;

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_sweep_gpu.py -q 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
