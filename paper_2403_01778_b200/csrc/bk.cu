@@ -58,7 +58,15 @@ struct BkLayout {
     double *Wp, *Ck, *Ci, *red, *part, *z;
     int *ctl, *ipiv, *perm;
     char* ps;
+    int* pperm;  // per panel: composed interchanges for the cluster solve
 };
+
+// Per-panel record of the cluster solve: [0] number of rows >= the panel end
+// touched by its interchanges, [1] / [2] bit mask (low / high word) of the
+// panel's first-of-2x2 columns, then those rows, then the slot permutations
+// of the forward (P) and backward (P^T) application.
+constexpr int kPermStride = 4 + kBkW + 4 * kBkW;
+inline int64_t max_panels(int64_t n) { return n / kBkNb + 2; }
 
 BkLayout bk_layout(void* ws, int64_t n, int num_sms) {
     BkLayout L;
@@ -79,6 +87,7 @@ BkLayout bk_layout(void* ws, int64_t n, int num_sms) {
     L.ipiv = i + 16;
     L.perm = L.ipiv + n + 16;
     L.ps = reinterpret_cast<char*>(L.perm + n + 16);
+    L.pperm = reinterpret_cast<int*>(L.ps + ((n + 64 + 15) & ~int64_t(15)));
     return L;
 }
 
@@ -301,42 +310,32 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_kernel(const BkArgs a) {
     }
 }
 
-// Panel kernel with the CTA's rows of W and of the two updated columns held
-// in shared memory (used when they fit).  The few scalars other CTAs need —
-// c_k(k), c_k(k+1), the signed arg-max entry, c_imax(imax), c_imax(k),
-// c_imax(k+1) — are published beside the reduction partials, so a column
-// costs two cluster barriers (three on the imax path) and no global re-reads
-// of the updated columns.  W rows exchanged by an interchange move through
-// DSMEM and land at the top of the next column.
-__device__ void block_argmax3(double& v, int64_t& i, double& sgn, double* sv, int64_t* si,
-                              double* ss) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, v, off);
-        const int64_t i2 = __shfl_xor_sync(0xffffffffu, i, off);
-        const double s2 = __shfl_xor_sync(0xffffffffu, sgn, off);
-        if (v2 > v || (v2 == v && i2 < i)) {
-            v = v2;
-            i = i2;
-            sgn = s2;
-        }
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) {
-        sv[warp] = v;
-        si[warp] = i;
-        ss[warp] = sgn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
-            if (sv[w] > v || (sv[w] == v && si[w] < i)) {
-                v = sv[w];
-                i = si[w];
-                sgn = ss[w];
-            }
-}
+// Panel kernel with the CTA's rows of W, of the two updated columns and of the
+// raw stored columns k, k+1 held in shared memory (used when they fit).
+//
+// No cluster barrier inside the column loop: every value another CTA needs is
+// PUSHED into that CTA's shared memory with st.async, which counts the bytes
+// on the receiver's mbarrier (transaction count), and the receiver waits for
+// exactly the bytes it expects.  Three messages per column:
+//   CAND  (all -> all) each CTA's arg-max of column k (index, signed value) and,
+//         from the owners, c_k(k), c_k(k+1);
+//   RMAX  (all -> all, imax path) row-max partial of column imax, c_imax(imax),
+//         c_imax(k), c_imax(k+1);
+//   NEXT  (owners -> all) the final W rows of the next pivot rows k', k'+1, and
+//         to kp's owner the raw entries the interchange moves into columns
+//         k', k'+1.
+// A cluster barrier's release waits for every outstanding global store of the
+// CTA; a message's release (the complete_tx) is performed by the memory
+// system, so the L / interchange stores of a column stream out behind the NEXT
+// message instead of in front of it.  They are ordered before the next CAND
+// message, which every reader of A inside the panel waits for first.
+// The W row of imax is read from its owner's shared memory after CAND (one
+// DSMEM round trip); the raw columns k', k'+1 are prefetched with cp.async
+// while a column eliminates and the entries its interchange rewrites are
+// patched in; interchanged rows of the panel's earlier L columns are rebuilt
+// from the W rows (stores only).
+constexpr size_t kBkPanelSmemMax = 200 * 1024;
+constexpr int kBkMsg = 4;  // doubles per CAND / RMAX record
 
 // Pivot coefficients of one panel step, kept by every CTA so a row of the
 // panel's L can be rebuilt from the same row of W (bit-identical to the stored
@@ -347,207 +346,307 @@ struct StepCoef {
     double c0, c1, c2;
 };
 
-__device__ __forceinline__ void l_row(const double* wrow, const StepCoef* cf, int jp, double* out) {
-    for (int t = threadIdx.x; t < jp; t += blockDim.x) {
-        const StepCoef c = cf[t];
-        double v = 0.0;
-        if (c.type == 1) v = wrow[t] * c.c0;
-        else if (c.type == 2) v = c.c0 * (c.c1 * wrow[t] - wrow[t + 1]);
-        else if (c.type == 3) v = c.c0 * (c.c2 * wrow[t] - wrow[t - 1]);
-        out[t] = v;
+__device__ __forceinline__ double l_1x1(double w, double r1) { return __dmul_rn(w, r1); }
+__device__ __forceinline__ double l_2x2(double d21t, double dii, double wi, double wo) {
+    return __dmul_rn(d21t, __fma_rn(dii, wi, -wo));
+}
+
+__device__ __forceinline__ double l_entry(const double* wrow, const StepCoef* cf, int t) {
+    const StepCoef c = cf[t];
+    if (c.type == 1) return l_1x1(wrow[t], c.c0);
+    if (c.type == 2) return l_2x2(c.c0, c.c1, wrow[t], wrow[t + 1]);
+    if (c.type == 3) return l_2x2(c.c0, c.c2, wrow[t], wrow[t - 1]);
+    return 0.0;
+}
+
+// (|v|, index) arg-max, first index on ties; v < 0 marks "no candidate"
+__device__ __forceinline__ void amax_merge(double& v, int& i, double& s, double v2, int i2, double s2) {
+    if (v2 > v || (v2 == v && i2 < i)) {
+        v = v2;
+        i = i2;
+        s = s2;
     }
 }
 
+__device__ __forceinline__ void warp_amax(double& v, int& i, double& s) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+        amax_merge(v, i, s, __shfl_xor_sync(0xffffffffu, v, off), __shfl_xor_sync(0xffffffffu, i, off),
+                   __shfl_xor_sync(0xffffffffu, s, off));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+// v -> the same shared-memory slot of CTA `rank`, counted on its mbarrier `bar`
+__device__ __forceinline__ void send8(const void* slot, double v, const uint64_t* bar, int rank) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(slot)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(v),
+                 "r"(rb)
+                 : "memory");
+}
+
+__device__ __forceinline__ void expect_bytes(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "BK_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra BK_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs a, int rcap) {
+    static_assert((kBkThreads & (kBkThreads - 1)) == 0, "row mapping uses a mask");
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double dsm[];
     double* Ws = dsm;                 // [rcap][kBkW] this CTA's rows of W
     double* Cs = Ws + rcap * kBkW;    // [rcap] updated column k
     double* Cis = Cs + rcap;          // [rcap] updated column imax
-    __shared__ double sv[32], ss[32];
-    __shared__ int64_t si[32];
-    __shared__ double Lr[kBkW];
+    double* Raw = Cis + rcap;         // [2 pairs][2][rcap] raw stored columns (k, k+1)
+    __shared__ double sv[8], ss[8];
+    __shared__ int si[8];
+    __shared__ double Lr[kBkW], Wim[kBkW];  // L row being applied; W row of imax
     __shared__ double pend[2][kBkW];
     __shared__ int pend_row[2], pend_n[2];
     __shared__ StepCoef coef[kBkW + 1];
-    // published for the other CTAs (read through DSMEM after a cluster barrier)
-    __shared__ double pub_v, pub_s, pub_rv;
-    __shared__ int64_t pub_i;
-    __shared__ double scal[8];  // [0] c_k(k) [1] c_k(k+1) [2] c_i(imax) [3] c_i(k) [4] c_i(k+1)
-    // this CTA's copy of the cluster-wide decision inputs
-    __shared__ double g_colmax, g_ckimax, g_rowmax, g_sc[5];
-    __shared__ int64_t g_imax;
-    const int64_t n = a.n;
-    const int64_t k0 = a.ctl[0];
+    __shared__ double own[5];  // this CTA's c_k(k), c_k(k+1), c_i(imax), c_i(k), c_i(k+1)
+    // message buffers (written by the other CTAs), double-buffered by step parity
+    __shared__ __align__(16) double candm[2][16][kBkMsg];
+    __shared__ __align__(16) double rmaxm[2][16][kBkMsg];
+    __shared__ __align__(16) double nextm[2][2 * kBkW + 2];  // rows k', k'+1, 2 patches
+    __shared__ __align__(8) uint64_t bars[6];                 // CAND[2], RMAX[2], NEXT[2]
+    const int n = static_cast<int>(a.n);
+    const int k0 = a.ctl[0];
     if (k0 >= n) return;
     const int G = gridDim.x;
-    const int64_t chunk = (n - k0 + G - 1) / G;
-    const int64_t lo = k0 + chunk * blockIdx.x, hi = min(n, lo + chunk);
-    const int R = static_cast<int>(hi > lo ? hi - lo : 0);
-    const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    const int64_t gthreads = static_cast<int64_t>(G) * blockDim.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int me = static_cast<int>(blockIdx.x);
+    const int tid = static_cast<int>(threadIdx.x);
+    const int chunk = (n - k0 + G - 1) / G;
+    const int lo = k0 + chunk * me, hi = min(n, lo + chunk);
+    const int R = hi > lo ? hi - lo : 0;
+    const int gtid = me * kBkThreads + tid;
     double* A = a.A;
-    auto owner = [&](int64_t i) { return static_cast<int>((i - k0) / chunk); };
-    auto local = [&](int64_t i) { return i - (k0 + chunk * owner(i)); };
-    // row q of the panel's L (columns k0 .. k0+jp-1) from the owner's W row; a
-    // row moved by the previous interchange is read from the owner's pending
-    // copy (its W row is rewritten at the top of this column, concurrently)
-    int64_t last_kk = -1, last_kp = -1;
-    auto load_lrow = [&](int64_t q, int jp) {
-        const double* w;
-        if (q == last_kk) w = cl.map_shared_rank(&pend[0][0], owner(q));
-        else if (q == last_kp) w = cl.map_shared_rank(&pend[1][0], owner(q));
-        else w = cl.map_shared_rank(Ws, owner(q)) + local(q) * kBkW;
-        l_row(w, coef, jp, Lr);
+    auto col = [&](int c) { return A + static_cast<size_t>(c) * static_cast<size_t>(n); };
+    auto owner = [&](int i) { return (i - k0) / chunk; };
+    // local row r is always handled by thread r % kBkThreads (the thread that
+    // prefetched / patched a raw entry is the one that reads it)
+    auto first_row = [&](int grow) {
+        const int r0 = grow > lo ? min(grow - lo, R) : 0;
+        return r0 + ((tid - r0) & (kBkThreads - 1));
     };
-    const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long tprev = 0, tnow = 0;
+    auto raw = [&](int pair, int slot) { return Raw + (2 * pair + slot) * rcap; };
+    const bool tr = a.trace && me == 0 && tid == 0;
+    long long tprev = 0;
     auto mark = [&](int ph) {
         if (!tr) return;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-        if (ph >= 0) a.trace[ph] += tnow - tprev;
-        tprev = tnow;
+        const long long t = clock64();
+        if (ph >= 0) a.trace[ph] += static_cast<unsigned long long>(t - tprev);
+        tprev = t;
     };
-    mark(-1);
-    if (threadIdx.x < 2) pend_row[threadIdx.x] = -1;
+    if (tid < 2) pend_row[tid] = -1;
+    if (tid == 0) {
+        for (int b = 0; b < 6; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[b])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // raw columns k0, k0+1 of this panel
+    for (int s = 0; s < 2; ++s) {
+        const int c = k0 + s;
+        if (c >= n) break;
+        const double* src = col(c);
+        for (int r = first_row(c); r < R; r += kBkThreads) cp_async8(raw(0, s) + r, src + lo + r);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     __syncthreads();
-    cl.sync();  // every CTA's shared memory is live before DSMEM use
+    cl.sync();  // barriers initialised and shared memory live everywhere
+    mark(-1);
 
-    int64_t k = k0;
-    int jp = 0;
+    int k = k0, jp = 0, cp = 0, step = 0, rstep = 0;
+    // the previous step's interchange and NEXT message
+    bool p_swap = false;
+    int p_kp = 0, p_kks = 0;
+    uint32_t p_next_bytes = 0;
     while (k < n && jp < kBkNb) {
+        const int b = step & 1;
+        const double* nx = nextm[b ^ 1];  // NEXT of the previous step
+        if (step > 0) {
+            if (tid == 0) expect_bytes(&bars[4 + (b ^ 1)], p_next_bytes);
+            wait_parity(&bars[4 + (b ^ 1)], ((step - 1) >> 1) & 1);
+        }
+        mark(0);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        if (p_swap) {
+            for (int s = 0; s < 2; ++s) {
+                const int c = k + s;
+                if (c >= n || c > p_kp) continue;
+                double* dst = raw(cp, s);
+                if (c == p_kp) {  // column kp <- raw column kk below kp
+                    const double* src = raw(cp ^ 1, p_kks);
+                    for (int r = first_row(p_kp + 1); r < R; r += kBkThreads) dst[r] = src[r];
+                }
+                if (p_kp >= lo && p_kp < hi && ((p_kp - lo) & (kBkThreads - 1)) == tid)
+                    dst[p_kp - lo] = nx[2 * kBkW + s];
+            }
+        }
         for (int p = 0; p < 2; ++p)
             if (pend_row[p] >= 0)
-                for (int t = threadIdx.x; t < pend_n[p]; t += blockDim.x) Ws[pend_row[p] * kBkW + t] = pend[p][t];
+                for (int t = tid; t < pend_n[p]; t += kBkThreads) Ws[pend_row[p] * kBkW + t] = pend[p][t];
+        if (tid < jp) Lr[tid] = l_entry(nx, coef, tid);
         __syncthreads();
-        if (threadIdx.x < 2) pend_row[threadIdx.x] = -1;
-        load_lrow(k, jp);
-        last_kk = last_kp = -1;
-        __syncthreads();
-        mark(0);
-        // ---- updated column k on the CTA's rows
-        double bv = -1.0, bs = 0.0;
-        int64_t bi = n;
-        for (int r = static_cast<int>(k > lo ? k - lo : 0) + threadIdx.x; r < R; r += blockDim.x) {
-            const int64_t i = lo + r;
-            double sacc = A[i + k * n];
-            for (int t = 0; t < jp; ++t) sacc -= Ws[r * kBkW + t] * Lr[t];
-            Cs[r] = sacc;
-            if (i > k && (fabs(sacc) > bv || (fabs(sacc) == bv && i < bi))) {
-                bv = fabs(sacc);
-                bi = i;
-                bs = sacc;
-            }
-            if (i == k) scal[0] = sacc;
-            if (i == k + 1) scal[1] = sacc;
-        }
-        block_argmax3(bv, bi, bs, sv, si, ss);
-        if (threadIdx.x == 0) {
-            pub_v = bv;
-            pub_i = bi;
-            pub_s = bs;
-        }
+        if (tid < 2) pend_row[tid] = -1;
         mark(1);
-        cl.sync();
-        mark(2);
-        if (warp == 0) {
-            // all remote reads issued together: lanes < G the partials, lanes
-            // 16 / 17 the scalars c_k(k), c_k(k+1)
-            double v = -1.0, sg = 0.0;
-            int64_t ii = n;
-            if (lane < G) {
-                v = *cl.map_shared_rank(&pub_v, lane);
-                ii = *cl.map_shared_rank(&pub_i, lane);
-                sg = *cl.map_shared_rank(&pub_s, lane);
-            } else if (lane == 16) {
-                g_sc[0] = *cl.map_shared_rank(&scal[0], owner(k));
-            } else if (lane == 17) {
-                g_sc[1] = k + 1 < n ? *cl.map_shared_rank(&scal[1], owner(k + 1)) : 0.0;
-            }
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                const double v2 = __shfl_xor_sync(0xffffffffu, v, off);
-                const int64_t i2 = __shfl_xor_sync(0xffffffffu, ii, off);
-                const double s2 = __shfl_xor_sync(0xffffffffu, sg, off);
-                if (v2 > v || (v2 == v && i2 < ii)) {
-                    v = v2;
-                    ii = i2;
-                    sg = s2;
+        // ---- updated column k on the CTA's rows, its arg-max below the diagonal
+        double bv = -1.0, bs = 0.0;
+        int bi = n;
+        {
+            const double* rk = raw(cp, 0);
+            for (int r = first_row(k); r < R; r += kBkThreads) {
+                const int i = lo + r;
+                const double* w = Ws + r * kBkW;
+                double s0 = rk[r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int t = 0;
+                for (; t + 4 <= jp; t += 4) {
+                    s0 -= w[t] * Lr[t];
+                    s1 -= w[t + 1] * Lr[t + 1];
+                    s2 -= w[t + 2] * Lr[t + 2];
+                    s3 -= w[t + 3] * Lr[t + 3];
                 }
-            }
-            if (lane == 0) {
-                g_colmax = v;
-                g_imax = ii;
-                g_ckimax = sg;
+                for (; t < jp; ++t) s0 -= w[t] * Lr[t];
+                const double sacc = (s0 + s1) + (s2 + s3);
+                Cs[r] = sacc;
+                if (i > k && (fabs(sacc) > bv || (fabs(sacc) == bv && i < bi))) {
+                    bv = fabs(sacc);
+                    bi = i;
+                    bs = sacc;
+                }
+                if (i == k) own[0] = sacc;
+                if (i == k + 1) own[1] = sacc;
             }
         }
+        warp_amax(bv, bi, bs);
+        if ((tid & 31) == 0) {
+            sv[tid >> 5] = bv;
+            si[tid >> 5] = bi;
+            ss[tid >> 5] = bs;
+        }
         __syncthreads();
-        double colmax = g_colmax;
-        int64_t imax = g_imax;
-        const double ckimax = g_ckimax;
+        if (tid < kBkMsg * G) {
+            // CAND record of this CTA -> CTA tid / 4
+            const int f = tid & 3;
+            double v = 0.0;
+            if (f < 2) {
+                double cv = -1.0, cs = 0.0;
+                int ci = n;
+                for (int w = 0; w < kBkThreads / 32; ++w) amax_merge(cv, ci, cs, sv[w], si[w], ss[w]);
+                v = f == 0 ? static_cast<double>(ci) : cs;
+            } else {
+                v = own[f - 2];
+            }
+            send8(&candm[b][me][f], v, &bars[b], tid >> 2);
+        }
+        mark(2);
+        if (tid == 0) expect_bytes(&bars[b], static_cast<uint32_t>(G * kBkMsg * 8));
+        wait_parity(&bars[b], (step >> 1) & 1);
+        mark(3);
+        double colmax, ckimax;
+        int imax;
+        {
+            const int lane = tid & 31;
+            int ii = lane < G ? static_cast<int>(candm[b][lane][0]) : n;
+            double sg = lane < G ? candm[b][lane][1] : 0.0;
+            double v = ii < n ? fabs(sg) : -1.0;
+            warp_amax(v, ii, sg);
+            colmax = v;
+            imax = ii;
+            ckimax = sg;
+        }
         if (colmax < 0.0) {
             colmax = 0.0;
             imax = k;
         }
-        const double ckk = g_sc[0], ckk1 = g_sc[1];
+        const double ckk = candm[b][owner(k)][2];
+        const double ckk1 = k + 1 < n ? candm[b][owner(k + 1)][3] : 0.0;
         const double absakk = fabs(ckk);
-        int kstep = 1;
-        int64_t kp = k;
+        int kstep = 1, kp = k;
         double cimax = 0.0, cik = 0.0, cik1 = 0.0;
-        mark(3);
-        if (fmax(absakk, colmax) == 0.0) {
-            for (int r = static_cast<int>(k > lo ? k - lo : 0) + threadIdx.x; r < R; r += blockDim.x) {
-                A[(lo + r) + k * n] = Cs[r];
-                Ws[r * kBkW + jp] = 0.0;
+        const bool imax_path = !(absakk >= kBkAlpha * colmax);
+        if (imax_path) {
+            const int oi = owner(imax);
+            const int lo_i = k0 + chunk * oi;
+            const double* wrem = cl.map_shared_rank(Ws, oi) + (imax - lo_i) * kBkW;
+            if (tid < jp) {
+                const double w0 = wrem[tid];
+                const StepCoef c = coef[tid];
+                double lv = 0.0;
+                if (c.type == 1) lv = l_1x1(w0, c.c0);
+                else if (c.type == 2) lv = l_2x2(c.c0, c.c1, w0, wrem[tid + 1]);
+                else if (c.type == 3) lv = l_2x2(c.c0, c.c2, w0, wrem[tid - 1]);
+                Wim[tid] = w0;
+                Lr[tid] = lv;
             }
-            if (threadIdx.x == 0) coef[jp] = StepCoef{0, 0.0, 0.0, 0.0};
-            if (gtid == 0) {
-                a.ipiv[k] = static_cast<int>(k);
-                a.ps[k] = 0;
-                a.ctl[1] = 1;
-            }
-            k += 1;
-            jp += 1;
-            __syncthreads();
-            cl.sync();
-            continue;
-        }
-        if (!(absakk >= kBkAlpha * colmax)) {
-            load_lrow(imax, jp);
             __syncthreads();
             double rv = -1.0;
-            for (int r = static_cast<int>(k > lo ? k - lo : 0) + threadIdx.x; r < R; r += blockDim.x) {
-                const int64_t i = lo + r;
-                double sacc = i >= imax ? A[i + imax * n] : A[imax + i * n];
-                for (int t = 0; t < jp; ++t) sacc -= Ws[r * kBkW + t] * Lr[t];
+            const double* ci = col(imax);
+            for (int r = first_row(k); r < R; r += kBkThreads) {
+                const int i = lo + r;
+                const double* w = Ws + r * kBkW;
+                double s0 = i >= imax ? ci[i] : col(i)[imax], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int t = 0;
+                for (; t + 4 <= jp; t += 4) {
+                    s0 -= w[t] * Lr[t];
+                    s1 -= w[t + 1] * Lr[t + 1];
+                    s2 -= w[t + 2] * Lr[t + 2];
+                    s3 -= w[t + 3] * Lr[t + 3];
+                }
+                for (; t < jp; ++t) s0 -= w[t] * Lr[t];
+                const double sacc = (s0 + s1) + (s2 + s3);
                 Cis[r] = sacc;
                 if (i != imax) rv = fmax(rv, fabs(sacc));
-                if (i == imax) scal[2] = sacc;
-                if (i == k) scal[3] = sacc;
-                if (i == k + 1) scal[4] = sacc;
+                if (i == imax) own[2] = sacc;
+                if (i == k) own[3] = sacc;
+                if (i == k + 1) own[4] = sacc;
             }
-            int64_t dummy = 0;
-            double dd = 0.0;
-            block_argmax3(rv, dummy, dd, sv, si, ss);
-            if (threadIdx.x == 0) pub_rv = rv;
-            mark(4);
-            cl.sync();
-            if (warp == 0) {
-                double v = 0.0;
-                if (lane < G) v = *cl.map_shared_rank(&pub_rv, lane);
-                else if (lane == 16) g_sc[2] = *cl.map_shared_rank(&scal[2], owner(imax));
-                else if (lane == 17) g_sc[3] = *cl.map_shared_rank(&scal[3], owner(k));
-                else if (lane == 18) g_sc[4] = k + 1 < n ? *cl.map_shared_rank(&scal[4], owner(k + 1)) : 0.0;
 #pragma unroll
-                for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
-                if (lane == 0) g_rowmax = v;
-            }
+            for (int off = 16; off >= 1; off >>= 1) rv = fmax(rv, __shfl_xor_sync(0xffffffffu, rv, off));
+            if ((tid & 31) == 0) sv[tid >> 5] = rv;
             __syncthreads();
-            const double rowmax = fmax(g_rowmax, 0.0);
-            cimax = g_sc[2];
-            cik = g_sc[3];
-            cik1 = g_sc[4];
+            const int rb = 2 + (rstep & 1);
+            if (tid < kBkMsg * G) {
+                const int f = tid & 3;
+                double v;
+                if (f == 0) {
+                    v = -1.0;
+                    for (int w = 0; w < kBkThreads / 32; ++w) v = fmax(v, sv[w]);
+                } else {
+                    v = own[f + 1];
+                }
+                send8(&rmaxm[rstep & 1][me][f], v, &bars[rb], tid >> 2);
+            }
+            mark(4);
+            if (tid == 0) expect_bytes(&bars[rb], static_cast<uint32_t>(G * kBkMsg * 8));
+            wait_parity(&bars[rb], (rstep >> 1) & 1);
+            mark(5);
+            double v = (tid & 31) < G ? rmaxm[rstep & 1][tid & 31][0] : 0.0;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+            const double rowmax = fmax(v, 0.0);
+            cimax = rmaxm[rstep & 1][oi][1];
+            cik = rmaxm[rstep & 1][owner(k)][2];
+            cik1 = k + 1 < n ? rmaxm[rstep & 1][owner(k + 1)][3] : 0.0;
+            ++rstep;
             if (tr) a.trace[8] += 1;
             if (absakk * rowmax >= kBkAlpha * colmax * colmax) {
                 kp = k;
@@ -558,127 +657,180 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 kstep = 2;
             }
         }
-        const int64_t kk = k + kstep - 1;
+        const int kk = k + kstep - 1;
+        const int kks = kstep - 1;  // slot of column kk in the raw pair
         const bool swap = kp != kk;
-        if (swap) {
-            // rows of this panel's L columns (earlier panels keep their order:
-            // the solve applies the interchanges panel by panel)
-            for (int64_t t = k0 + gtid; t < k; t += gthreads) {
-                const double u = A[kk + t * n];
-                A[kk + t * n] = A[kp + t * n];
-                A[kp + t * n] = u;
+        const int kn = k + kstep, jn = jp + kstep;
+        const bool more = kn < n && jn < kBkNb;
+        const double* rkk = raw(cp, kks);
+        const double* w_kk = nx + kks * kBkW;  // W row kk (NEXT of the previous step)
+        // prefetch the raw columns kn, kn+1 (patched at the top of the next step)
+        if (more) {
+            for (int s = 0; s < 2; ++s) {
+                const int c = kn + s;
+                if (c >= n) break;
+                const double* src = col(c);
+                for (int r = first_row(c); r < R; r += kBkThreads) cp_async8(raw(cp ^ 1, s) + r, src + lo + r);
             }
-            // W rows kk <-> kp through DSMEM; applied at the top of the next column
-            const int okk = owner(kk), okp = owner(kp);
-            for (int side = 0; side < 2; ++side) {
-                const int me = side == 0 ? okk : okp;
-                if (static_cast<int>(blockIdx.x) != me) continue;
-                const int64_t dst = side == 0 ? kk : kp, src = side == 0 ? kp : kk;
-                const double* remote = cl.map_shared_rank(Ws, owner(src)) + local(src) * kBkW;
-                for (int t = threadIdx.x; t < jp; t += blockDim.x) pend[side][t] = remote[t];
-                if (threadIdx.x == 0) {
-                    pend_row[side] = static_cast<int>(dst - lo);
-                    pend_n[side] = jp + kstep;  // + the new column(s), stored below
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // ---- pivot coefficients (every CTA), new W column(s), pending W rows
+        double d = 0.0, r1 = 0.0, d11 = 0.0, d22 = 0.0, d21t = 0.0;
+        bool zero = false;
+        const bool same = kp == k + 1;
+        if (kstep == 1) {
+            d = kp == k ? ckk : cimax;
+            zero = d == 0.0;
+            r1 = zero ? 0.0 : 1.0 / d;
+        } else {
+            const double d21 = same ? ckk1 : ckimax;
+            d11 = cimax / d21;
+            d22 = ckk / d21;
+            const double tt = 1.0 / (d11 * d22 - 1.0);
+            d21t = tt / d21;
+        }
+        auto new_w = [&](int r, int i, double& x0, double& x1) {
+            if (kstep == 1) {
+                const double v = kp == k ? Cs[r] : (i == k ? cimax : (i == kp ? cik : Cis[r]));
+                x0 = zero ? 0.0 : (i == k ? d : v);
+                x1 = v;  // unscaled, for the L store
+            } else {
+                x0 = same ? Cs[r] : (i == k + 1 ? ckimax : (i == kp ? ckk1 : Cs[r]));
+                x1 = same ? Cis[r] : (i == k + 1 ? cimax : (i == kp ? cik1 : Cis[r]));
+            }
+        };
+        if (swap) {
+            if (kk >= lo && kk < hi && tid < jp) pend[0][tid] = Wim[tid];
+            if (kp >= lo && kp < hi && tid < jp) pend[1][tid] = w_kk[tid];
+            if (tid == 0) {
+                if (kk >= lo && kk < hi) {
+                    pend_row[0] = kk - lo;
+                    pend_n[0] = jn;
+                }
+                if (kp >= lo && kp < hi) {
+                    pend_row[1] = kp - lo;
+                    pend_n[1] = jn;
                 }
             }
         }
-        auto move_out = [&](int64_t i) {
-            if (!swap) return;
-            if (i > kp) A[i + kp * n] = A[i + kk * n];
-            else if (i > kk && i < kp) A[kp + i * n] = A[i + kk * n];
-            else if (i == kk) A[kp + kp * n] = A[kk + kk * n];
-        };
-        if (kstep == 1) {
-            const double d = kp == k ? ckk : cimax;
-            const bool zero = d == 0.0;
-            const double r1 = zero ? 0.0 : 1.0 / d;
-            for (int r = static_cast<int>(k > lo ? k - lo : 0) + threadIdx.x; r < R; r += blockDim.x) {
-                const int64_t i = lo + r;
-                const double v = kp == k ? Cs[r] : (i == k ? cimax : (i == kp ? cik : Cis[r]));
-                move_out(i);
-                const double wv = zero ? 0.0 : (i == k ? d : v);
-                Ws[r * kBkW + jp] = wv;
-                if (swap && i == kk) pend[0][jp] = wv;
-                if (swap && i == kp) pend[1][jp] = wv;
-                if (i == k) A[k + k * n] = d;
-                else A[i + k * n] = zero ? v : v * r1;
+        for (int r = first_row(k); r < R; r += kBkThreads) {
+            const int i = lo + r;
+            double x0, x1;
+            new_w(r, i, x0, x1);
+            Ws[r * kBkW + jp] = x0;
+            if (kstep == 2) Ws[r * kBkW + jp + 1] = x1;
+            if (swap && (i == kk || i == kp)) {
+                double* pr = pend[i == kk ? 0 : 1];
+                pr[jp] = x0;
+                if (kstep == 2) pr[jp + 1] = x1;
             }
-            if (threadIdx.x == 0) coef[jp] = StepCoef{zero ? 0 : 1, r1, 0.0, 0.0};
-            if (gtid == 0) {
-                a.ipiv[k] = static_cast<int>(kp);
-                a.ps[k] = 0;
-                if (zero) a.ctl[1] = 1;
-            }
-        } else {
-            const bool same = kp == k + 1;
-            const double nk_k = ckk, nk_k1 = same ? ckk1 : ckimax;
-            const double nk1_k1 = cimax;
-            const double d21 = nk_k1;
-            const double d11 = nk1_k1 / d21;
-            const double d22 = nk_k / d21;
-            const double tt = 1.0 / (d11 * d22 - 1.0);
-            const double d21t = tt / d21;
-            for (int r = static_cast<int>(k > lo ? k - lo : 0) + threadIdx.x; r < R; r += blockDim.x) {
-                const int64_t i = lo + r;
-                const double x0 = same ? Cs[r] : (i == k + 1 ? ckimax : (i == kp ? ckk1 : Cs[r]));
-                const double x1 = same ? Cis[r] : (i == k + 1 ? cimax : (i == kp ? cik1 : Cis[r]));
-                move_out(i);
-                Ws[r * kBkW + jp] = x0;
-                Ws[r * kBkW + jp + 1] = x1;
-                if (swap && i == kk) {
-                    pend[0][jp] = x0;
-                    pend[0][jp + 1] = x1;
-                }
-                if (swap && i == kp) {
-                    pend[1][jp] = x0;
-                    pend[1][jp + 1] = x1;
-                }
-                if (i == k) {
-                    A[k + k * n] = x0;
-                } else if (i == k + 1) {
-                    A[k + 1 + k * n] = x0;
-                    A[k + 1 + (k + 1) * n] = x1;
-                } else {
-                    A[i + k * n] = d21t * (d11 * x0 - x1);
-                    A[i + (k + 1) * n] = d21t * (d22 * x1 - x0);
-                }
-            }
-            if (threadIdx.x == 0) {
+        }
+        if (tid == 0) {
+            if (kstep == 1) {
+                coef[jp] = StepCoef{zero ? 0 : 1, r1, 0.0, 0.0};
+            } else {
                 coef[jp] = StepCoef{2, d21t, d11, d22};
                 coef[jp + 1] = StepCoef{3, d21t, d11, d22};
             }
-            if (gtid == 0) {
-                a.ipiv[k] = static_cast<int>(-kp - 1);
-                a.ipiv[k + 1] = static_cast<int>(-kp - 1);
+        }
+        __syncthreads();
+        uint32_t next_bytes = 0;
+        if (more) {
+            // NEXT: final W rows of kn, kn+1 -> every CTA (kp's row is the pending
+            // copy); raw entries moved into columns kn, kn+1 -> kp's owner
+            const int okp = owner(kp);
+            for (int s = 0; s < 2; ++s) {
+                const int q = kn + s;
+                if (q >= n) break;
+                next_bytes += 8u * jn;
+                if (q >= lo && q < hi) {
+                    const double* src = swap && q == kp ? pend[1] : Ws + (q - lo) * kBkW;
+                    for (int e = tid; e < G * jn; e += kBkThreads) {
+                        const int dst = e / jn, t = e - dst * jn;
+                        send8(&nextm[b][s * kBkW + t], src[t], &bars[4 + b], dst);
+                    }
+                }
+                if (swap && q <= kp) {
+                    if (okp == me) next_bytes += 8u;
+                    const int srow = q < kp ? q : kk;  // the raw entry's row in column kk
+                    if (srow >= lo && srow < hi && ((srow - lo) & (kBkThreads - 1)) == tid)
+                        send8(&nextm[b][2 * kBkW + s], rkk[srow - lo], &bars[4 + b], okp);
+                }
+            }
+        }
+        mark(6);
+        // ---- global stores (stream out behind NEXT): L / D of the new
+        // column(s), interchange moves, interchanged rows of earlier L columns
+        if (swap) {
+            for (int e = gtid; e < 2 * jp; e += G * kBkThreads) {
+                const int t = e >> 1;
+                if (e & 1) col(k0 + t)[kp] = l_entry(w_kk, coef, t);
+                else col(k0 + t)[kk] = l_entry(Wim, coef, t);
+            }
+        }
+        double* ck = col(k);
+        double* ck1 = col(k + 1 < n ? k + 1 : k);
+        double* ckp = col(kp);
+        for (int r = first_row(k); r < R; r += kBkThreads) {
+            const int i = lo + r;
+            double x0, x1;
+            new_w(r, i, x0, x1);
+            if (swap && i >= kk) {
+                const double rv = rkk[r];
+                if (i > kp) ckp[i] = rv;
+                else if (i > kk && i < kp) col(i)[kp] = rv;
+                else if (i == kk) ckp[kp] = rv;
+            }
+            if (kstep == 1) {
+                if (i == k) ck[k] = d;
+                else ck[i] = zero ? x1 : l_1x1(x1, r1);
+            } else if (i == k) {
+                ck[k] = x0;
+            } else if (i == k + 1) {
+                ck[k + 1] = x0;
+                ck1[k + 1] = x1;
+            } else {
+                ck[i] = l_2x2(d21t, d11, x0, x1);
+                ck1[i] = l_2x2(d21t, d22, x1, x0);
+            }
+        }
+        if (gtid == 0) {
+            if (kstep == 1) {
+                a.ipiv[k] = kp;
+                a.ps[k] = 0;
+                if (zero) a.ctl[1] = 1;
+            } else {
+                a.ipiv[k] = -kp - 1;
+                a.ipiv[k + 1] = -kp - 1;
                 a.ps[k] = 1;
                 a.ps[k + 1] = 2;
             }
         }
-        if (swap) {
-            last_kk = kk;
-            last_kp = kp;
-        }
-        k += kstep;
-        jp += kstep;
-        mark(5);
-        __syncthreads();
-        cl.sync();
-        mark(6);
+        p_swap = swap;
+        p_kp = kp;
+        p_kks = kks;
+        p_next_bytes = next_bytes;
+        k = kn;
+        jp = jn;
+        cp ^= 1;
+        ++step;
+        mark(7);
         if (tr) a.trace[9] += 1;
     }
+    __syncthreads();
     for (int p = 0; p < 2; ++p)
         if (pend_row[p] >= 0)
-            for (int t = threadIdx.x; t < pend_n[p]; t += blockDim.x) Ws[pend_row[p] * kBkW + t] = pend[p][t];
+            for (int t = tid; t < pend_n[p]; t += kBkThreads) Ws[pend_row[p] * kBkW + t] = pend[p][t];
     __syncthreads();
     // the panel's W rows of this CTA -> global, for the trailing update
     for (int t = 0; t < jp; ++t)
-        for (int r = threadIdx.x; r < R; r += blockDim.x) a.Wp[(lo + r) + t * n] = Ws[r * kBkW + t];
+        for (int r = tid; r < R; r += kBkThreads) a.Wp[(lo + r) + static_cast<size_t>(t) * n] = Ws[r * kBkW + t];
     if (gtid == 0) {
-        a.perm[a.ctl[4]] = static_cast<int>(k0);  // panel starts, for the solve
+        a.perm[a.ctl[4]] = k0;  // panel starts, for the solve
         a.ctl[4] += 1;
-        a.ctl[2] = static_cast<int>(k0);
+        a.ctl[2] = k0;
         a.ctl[3] = jp;
-        a.ctl[0] = static_cast<int>(k);
+        a.ctl[0] = k;
     }
     cl.sync();  // no CTA exits while others may still read its shared memory
 }
@@ -690,12 +842,6 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
 constexpr int kBkT2 = 128;
 constexpr size_t kBkUpdSmem = (2 * kBkW * kBkT2 + kBkT2 * kBkT2) * sizeof(double);
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-                 "l"(gmem)
-                 : "memory");
-}
 
 __global__ void __launch_bounds__(kBkThreads, 1) bk_update2_kernel(const BkArgs a) {
     extern __shared__ __align__(16) double usm[];
@@ -958,6 +1104,258 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_kernel(const SolveArgs s)
     }
 }
 
+// Composed interchanges of each panel (one thread per panel): the rows a
+// panel's interchanges touch are its own columns' rows plus a few rows below
+// it ("outside" rows); applying the interchanges in order (forward) or in
+// reverse (backward) is a fixed permutation of those slots.
+__global__ void bk_perm_kernel(const int* __restrict__ ipiv, const char* __restrict__ ps,
+                               const int* __restrict__ pstart, const int* __restrict__ ctl, int n,
+                               int* __restrict__ pperm) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int np = ctl[4];
+    if (p >= np) return;
+    const int c0 = pstart[p], c1 = p + 1 < np ? pstart[p + 1] : n, w = c1 - c0;
+    int* P = pperm + static_cast<size_t>(p) * kPermStride;
+    int* out = P + 4;
+    int* fwd = out + kBkW;
+    int* bwd = fwd + 2 * kBkW;
+    int nout = 0;
+    unsigned long long first2 = 0;
+    auto slot = [&](int row) {
+        if (row < c1) return row - c0;
+        for (int j = 0; j < nout; ++j)
+            if (out[j] == row) return w + j;
+        out[nout] = row;
+        return w + nout++;
+    };
+    for (int j = 0; j < 2 * kBkW; ++j) fwd[j] = bwd[j] = j;
+    for (int k = c0; k < c1; ++k) {
+        if (ps[k] == 1) first2 |= 1ull << (k - c0);
+        if (ps[k] == 2) continue;
+        const int kk = ps[k] == 1 ? k + 1 : k;
+        const int kp = ps[k] == 1 ? -ipiv[k] - 1 : ipiv[k];
+        if (kp == kk) continue;
+        const int a = slot(kk), b = slot(kp);
+        const int t = fwd[a];
+        fwd[a] = fwd[b];
+        fwd[b] = t;
+    }
+    for (int k = c1 - 1; k >= c0; --k) {
+        if (ps[k] == 2) continue;
+        const int kk = ps[k] == 1 ? k + 1 : k;
+        const int kp = ps[k] == 1 ? -ipiv[k] - 1 : ipiv[k];
+        if (kp == kk) continue;
+        const int a = slot(kk), b = slot(kp);
+        const int t = bwd[a];
+        bwd[a] = bwd[b];
+        bwd[b] = t;
+    }
+    P[0] = nout;
+    P[1] = static_cast<int>(first2 & 0xffffffffu);
+    P[2] = static_cast<int>(first2 >> 32);
+}
+
+// A x = b on ONE thread-block cluster (<= 16 CTAs): z lives in shared memory,
+// CTA c owning rows [c chunk, (c+1) chunk).  Per panel (forward: P_p, L_p^-1;
+// backward: L_p^-T, P_p^T, same algebra as bk_solve_kernel) every CTA
+// redundantly solves the panel's diagonal block on the panel's rows plus the
+// outside rows its interchanges touch (slots), and updates its own rows below
+// the panel; the slot values a panel needs are pushed to every CTA by their
+// owners at the end of the previous panel, so one cluster barrier per panel
+// orders everything.  Fixed partitions and summation orders: deterministic.
+__global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const SolveArgs s, const int* pperm) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double zs[];                    // own rows of z
+    __shared__ double Lb[2][kBkW][kBkW + 1];          // panel diagonal block (see below)
+    __shared__ double gsl[2][2 * kBkW];               // pushed slot values, by panel parity
+    __shared__ double part[2][16][kBkW];              // pushed backward partials, by parity
+    __shared__ double zp[2 * kBkW];
+    __shared__ double nrm2[16];
+    const int n = static_cast<int>(s.n);
+    const int G = gridDim.x, me = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int chunk = (n + G - 1) / G;
+    const int lo = chunk * me, hi = min(n, lo + chunk), R = hi > lo ? hi - lo : 0;
+    const int np = s.ctl[4];
+    const double* A = s.A;
+    auto colp = [&](int c) { return A + static_cast<size_t>(c) * static_cast<size_t>(n); };
+    auto rec = [&](int p) { return pperm + static_cast<size_t>(p) * kPermStride; };
+    auto pbounds = [&](int p, int& c0, int& c1) {
+        c0 = s.pstart[p];
+        c1 = p + 1 < np ? s.pstart[p + 1] : n;
+    };
+    auto slot_row = [&](const int* P, int c0, int w, int j) { return j < w ? c0 + j : P[4 + j - w]; };
+    auto is_first2 = [&](const int* P, int t) {
+        return ((t < 32 ? static_cast<unsigned>(P[1]) >> t : static_cast<unsigned>(P[2]) >> (t - 32)) & 1u) != 0;
+    };
+    // every CTA's slot values of panel p (rows owned here) -> gsl[par] everywhere
+    auto push_slots = [&](int p, int par) {
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int* P = rec(p);
+        const int w = c1 - c0, m = w + P[0];
+        for (int e = tid; e < m * G; e += kBkThreads) {
+            const int j = e % m, d = e / m;
+            const int row = slot_row(P, c0, w, j);
+            if (row >= lo && row < hi) *cl.map_shared_rank(&gsl[par][j], d) = zs[row - lo];
+        }
+    };
+    // forward: Lb[par][t][i] = L(c0+i, c0+t), i > t (column t contiguous)
+    auto load_fwd_block = [&](int p, int par) {
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int* P = rec(p);
+        const int w = c1 - c0;
+        for (int e = tid; e < w * w; e += kBkThreads) {
+            const int t = e / w, i = e - t * w;
+            const bool z = i <= t || (i == t + 1 && is_first2(P, t));
+            Lb[par][t][i] = z ? 0.0 : colp(c0 + t)[c0 + i];
+        }
+    };
+    for (int r = tid; r < R; r += kBkThreads) zs[r] = s.x[lo + r];
+    __syncthreads();
+    if (np > 0) {
+        push_slots(0, 0);
+        load_fwd_block(0, 0);
+    }
+    cl.sync();
+    // ---- forward
+    for (int p = 0; p < np; ++p) {
+        const int par = p & 1;
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int* P = rec(p);
+        const int w = c1 - c0, m = w + P[0];
+        if (tid < m) zp[tid] = gsl[par][P[4 + kBkW + tid]];
+        __syncthreads();
+        if (warp == 0) {
+            double a0 = lane < w ? zp[lane] : 0.0, a1 = lane + 32 < w ? zp[lane + 32] : 0.0;
+            for (int t = 0; t < w; ++t) {
+                const double zt = __shfl_sync(0xffffffffu, t < 32 ? a0 : a1, t & 31);
+                a0 -= Lb[par][t][lane] * zt;  // zero for lane <= t
+                if (lane + 32 < w) a1 -= Lb[par][t][lane + 32] * zt;
+            }
+            if (lane < w) zp[lane] = a0;
+            if (lane + 32 < w) zp[lane + 32] = a1;
+        }
+        if (p + 1 < np) load_fwd_block(p + 1, par ^ 1);
+        __syncthreads();
+        if (tid < m) {
+            const int row = slot_row(P, c0, w, tid);
+            if (row >= lo && row < hi) zs[row - lo] = zp[tid];
+        }
+        __syncthreads();
+        {
+            const int r0 = c1 > lo ? min(c1 - lo, R) : 0;
+            for (int r = r0 + tid; r < R; r += kBkThreads) {
+                const int i = lo + r;
+                double acc = 0.0;
+                for (int t = 0; t < w; ++t) acc += colp(c0 + t)[i] * zp[t];
+                zs[r] -= acc;
+            }
+        }
+        __syncthreads();
+        if (p + 1 < np) push_slots(p + 1, par ^ 1);
+        cl.sync();
+    }
+    // ---- D^-1 (sym_eig.cpp:338-352); a 2x2 pair is solved by its first row's owner
+    for (int r = tid; r < R; r += kBkThreads) {
+        const int k = lo + r;
+        if (s.ps[k] == 0) {
+            zs[r] /= A[k + static_cast<size_t>(k) * n];
+        } else if (s.ps[k] == 1) {
+            double* zk1 = k + 1 < hi ? &zs[r + 1] : cl.map_shared_rank(zs, me + 1);
+            const double akm1k = A[(k + 1) + static_cast<size_t>(k) * n];
+            const double akm1 = A[k + static_cast<size_t>(k) * n] / akm1k;
+            const double ak = A[(k + 1) + static_cast<size_t>(k + 1) * n] / akm1k;
+            const double denom = akm1 * ak - 1.0;
+            const double bkm1 = zs[r] / akm1k;
+            const double bk = *zk1 / akm1k;
+            zs[r] = (ak * bkm1 - bk) / denom;
+            *zk1 = (akm1 * bk - bkm1) / denom;
+        }
+    }
+    cl.sync();
+    // ---- backward: per panel, partials of L21^T z over own rows + own slot
+    // values -> every CTA; barrier; sum (fixed order), L11^-T, P^T, write back
+    auto push_back = [&](int p, int par) {
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int w = c1 - c0;
+        const int r0 = c1 > lo ? min(c1 - lo, R) : 0;
+        for (int t = warp; t < w; t += kBkThreads / 32) {
+            const double* ct = colp(c0 + t);
+            double acc = 0.0;
+            for (int r = r0 + lane; r < R; r += 32) acc += ct[lo + r] * zs[r];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane < G) *cl.map_shared_rank(&part[par][me][t], lane) = acc;
+        }
+        push_slots(p, par);
+    };
+    if (np > 0) push_back(np - 1, (np - 1) & 1);
+    cl.sync();
+    for (int p = np - 1; p >= 0; --p) {
+        const int par = p & 1;
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int* P = rec(p);
+        const int w = c1 - c0, m = w + P[0];
+        // backward block: Lb[par][i][t] = L(c0+i, c0+t), i > t (row i contiguous)
+        for (int e = tid; e < w * w; e += kBkThreads) {
+            const int i = e / w, t = e - i * w;
+            const bool z = i <= t || (i == t + 1 && is_first2(P, t));
+            Lb[par][i][t] = z ? 0.0 : colp(c0 + t)[c0 + i];
+        }
+        if (tid < m) {
+            double v = gsl[par][tid];
+            if (tid < w)
+                for (int c = 0; c < G; ++c) v -= part[par][c][tid];
+            zp[tid] = v;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double a0 = lane < w ? zp[lane] : 0.0, a1 = lane + 32 < w ? zp[lane + 32] : 0.0;
+            for (int i = w - 1; i >= 1; --i) {
+                const double zi = __shfl_sync(0xffffffffu, i < 32 ? a0 : a1, i & 31);
+                a0 -= Lb[par][i][lane] * zi;  // zero for lane >= i
+            }
+            if (lane < w) zp[lane] = a0;
+            if (lane + 32 < w) zp[lane + 32] = a1;
+        }
+        __syncthreads();
+        if (tid < m) {
+            const int row = slot_row(P, c0, w, tid);
+            if (row >= lo && row < hi) zs[row - lo] = zp[P[4 + 3 * kBkW + tid]];
+        }
+        __syncthreads();
+        if (p > 0) push_back(p - 1, par ^ 1);
+        cl.sync();
+    }
+    // ---- normalise (sym_eig.cpp:425-431)
+    {
+        double acc = 0.0;
+        for (int r = tid; r < R; r += kBkThreads) acc = fma(zs[r], zs[r], acc);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) zp[warp] = acc;
+        __syncthreads();
+        if (tid < G) {
+            double tot = 0.0;
+            for (int w = 0; w < kBkThreads / 32; ++w) tot += zp[w];
+            *cl.map_shared_rank(&nrm2[me], tid) = tot;
+        }
+        cl.sync();
+        double tot = 0.0;
+        for (int c = 0; c < G; ++c) tot += nrm2[c];
+        const double nrm = sqrt(tot);
+        const bool good = isfinite(nrm) && nrm != 0.0;
+        for (int r = tid; r < R; r += kBkThreads) s.y[lo + r] = good ? zs[r] / nrm : zs[r];
+        if (me == 0 && tid == 0) s.ok[0] = good ? 1 : 0;
+    }
+    cl.sync();  // no CTA exits while others may still access its shared memory
+}
+
 // Largest cluster (<= 16, <= one CTA per 256 rows) the device can schedule.
 int panel_cluster_size(r1_context* ctx, int64_t n) {
     static int max16 = -1;
@@ -1001,7 +1399,8 @@ int coop_grid(const void* fn, int want, int num_sms) {
 size_t bk_workspace_bytes(int64_t n, int num_sms) {
     return (static_cast<size_t>(n) * kBkW + 3 * static_cast<size_t>(n) + 64 * 8 +
             static_cast<size_t>(num_sms) * kBkSolveB + 96) * sizeof(double) +
-           (2 * static_cast<size_t>(n) + 64) * sizeof(int) + static_cast<size_t>(n) + 64;
+           (2 * static_cast<size_t>(n) + 64) * sizeof(int) + static_cast<size_t>(n) + 64 + 16 +
+           static_cast<size_t>(max_panels(n)) * kPermStride * sizeof(int);
 }
 
 // Factor A (n x n, device, lower triangle; overwritten) and write the D-block
@@ -1037,12 +1436,12 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     cfg.numAttrs = 1;
     // CTA rows of W + the two updated columns in shared memory when they fit
     const int rcap = static_cast<int>((n + gp - 1) / gp);
-    const size_t psmem = static_cast<size_t>(rcap) * (kBkW + 2) * sizeof(double);
-    const bool smem_panel = psmem <= 160 * 1024 && gp <= 16;
+    const size_t psmem = static_cast<size_t>(rcap) * (kBkW + 6) * sizeof(double);
+    const bool smem_panel = psmem <= kBkPanelSmemMax && gp <= 16;
     static int configured = -1;
     if (configured != ctx->device) {
         R1_CUDA(cudaFuncSetAttribute(bk_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     160 * 1024));
+                                     static_cast<int>(kBkPanelSmemMax)));
         R1_CUDA(cudaFuncSetAttribute(bk_panel_smem_kernel,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         R1_CUDA(cudaFuncSetAttribute(bk_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1069,10 +1468,10 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
         const double c = h[9] ? static_cast<double>(h[9]) : 1.0;
         std::fprintf(stderr,
-                     "[r1 bk] n=%lld cols=%llu imax-path=%llu us/col: top %.2f step1 %.2f sync1 %.2f "
-                     "decide %.2f imax %.2f elim %.2f sync_end %.2f\n",
-                     static_cast<long long>(n), h[9], h[8], h[0] / c * 1e-3, h[1] / c * 1e-3,
-                     h[2] / c * 1e-3, h[3] / c * 1e-3, h[4] / c * 1e-3, h[5] / c * 1e-3, h[6] / c * 1e-3);
+                     "[r1 bk] n=%lld cols=%llu imax-path=%llu cycles/col: wait_next %.0f top %.0f step1 %.0f "
+                     "wait_cand %.0f imax %.0f wait_rmax %.0f elim %.0f stores %.0f\n",
+                     static_cast<long long>(n), h[9], h[8], h[0] / c, h[1] / c, h[2] / c, h[3] / c,
+                     h[4] / c, h[5] / c, h[6] / c, h[7] / c);
     }
 }
 
@@ -1081,6 +1480,40 @@ void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const doubl
               int* ok_dev) {
     const BkLayout L = bk_layout(ws, n, ctx->num_sms);
     SolveArgs s{n, A, L.ipiv, L.ps, L.perm, L.ctl, x, L.z, y, L.part, ok_dev};
+    static const char* gsolve = std::getenv("R1_BK_GRID_SOLVE");
+    const int gp = panel_cluster_size(ctx, n);
+    if (!(gsolve && std::atoi(gsolve)) && n < (int64_t(1) << 30)) {
+        // cluster solve: interchanges composed per panel, z in shared memory
+        const int64_t mp = max_panels(n);
+        bk_perm_kernel<<<static_cast<int>((mp + 127) / 128), 128, 0, ctx->stream>>>(
+            L.ipiv, L.ps, L.perm, L.ctl, static_cast<int>(n), L.pperm);
+        check_launch(ctx, "bk_perm_kernel");
+        static int configured = -1;
+        if (configured != ctx->device) {
+            R1_CUDA(cudaFuncSetAttribute(bk_solve_cluster_kernel,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            R1_CUDA(cudaFuncSetAttribute(bk_solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         160 * 1024));
+            configured = ctx->device;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(gp);
+        cfg.blockDim = dim3(kBkThreads);
+        cfg.dynamicSmemBytes = static_cast<size_t>((n + gp - 1) / gp) * sizeof(double);
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = gp;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cfg.dynamicSmemBytes <= 160 * 1024) {
+            R1_CUDA(cudaLaunchKernelEx(&cfg, bk_solve_cluster_kernel, s, static_cast<const int*>(L.pperm)));
+            check_launch(ctx, "bk_solve_cluster_kernel");
+            return;
+        }
+    }
     const int g = coop_grid(reinterpret_cast<const void*>(bk_solve_kernel),
                             static_cast<int>(std::min<int64_t>(ctx->num_sms, (n + 255) / 256 + 1)),
                             ctx->num_sms);

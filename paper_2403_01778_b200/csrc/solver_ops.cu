@@ -216,14 +216,30 @@ __global__ void shift_copy_kernel(const double* __restrict__ S, double* __restri
 }
 
 // (Sx)_i, thread per row (column-major S: coalesced across threads).
+// y = S x for symmetric S (column-major): y_j = S(:, j) . x, one warp per
+// column (coalesced column reads, fixed-order lane sums: deterministic).
 __global__ void dense_matvec_kernel(const double* __restrict__ S, const double* __restrict__ x,
                                     int64_t n, double* __restrict__ y) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int64_t j = 0; j < n; ++j) s = fma(S[i + j * n], x[j], s);
-        y[i] = s;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += warps) {
+        const double* c = S + j * n;
+        double s0 = 0.0, s1 = 0.0;
+        int64_t i = lane;
+        for (; i + 32 < n; i += 64) {
+            s0 = fma(c[i], x[i], s0);
+            s1 = fma(c[i + 32], x[i + 32], s1);
+        }
+        if (i < n) s0 = fma(c[i], x[i], s0);
+        double s = s0 + s1;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) y[j] = s;
     }
+}
+
+inline int dense_matvec_grid(int64_t n, int num_sms) {
+    return std::max(1, static_cast<int>(std::min<int64_t>((n + 7) / 8, 8 * static_cast<int64_t>(num_sms))));
 }
 
 // shifts[1] = bumped shift (sym_eig.cpp:435-436) from rho = shifts[0].
@@ -409,8 +425,7 @@ bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, doub
     ipiv64.ensure(std::max<int64_t>(n, 1) * sizeof(int64_t));
     // rho = x'Sx (sym_eig.cpp:417-418); ||S||_F only matters when rho == 0
     double* sx = scal + 16 + (n + 16) / 2 + 8;  // after ipiv/info (ints)
-    dense_matvec_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms))),
-                          256, 0, ctx->stream>>>(S, x, n, sx);
+    dense_matvec_kernel<<<dense_matvec_grid(n, ctx->num_sms), 256, 0, ctx->stream>>>(S, x, n, sx);
     check_launch(ctx, "dense_matvec_kernel");
     dot_device(ctx, x, sx, static_cast<uint64_t>(n), scal);
     sumsq_device(ctx, S, nn, scal + 3);
@@ -473,8 +488,7 @@ bool rqi_step_bk(r1_context* ctx, int64_t n, const double* S, const double* x, d
     double* sx = scal + 16;
     SolverHandle& H = handle_state(ctx);
     H.work.ensure(bk_workspace_bytes(n, ctx->num_sms));
-    dense_matvec_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms))),
-                          256, 0, ctx->stream>>>(S, x, n, sx);
+    dense_matvec_kernel<<<dense_matvec_grid(n, ctx->num_sms), 256, 0, ctx->stream>>>(S, x, n, sx);
     check_launch(ctx, "dense_matvec_kernel");
     dot_device(ctx, x, sx, static_cast<uint64_t>(n), scal);
     sumsq_device(ctx, S, nn, scal + 3);
