@@ -65,6 +65,11 @@ struct EigArgs {
     double* stats;   // [theta_lo, theta_hi, res_lo, res_hi, value]
     double* out_value;
     double* out_vec;
+    int cluster;     // 1: the grid is one thread-block cluster (hardware cluster barriers)
+    int* hint;       // steps the previous warm-started solve of this operator took
+    int warm;        // 1: x0 is the previous eigenvector (use and update *hint)
+    const double* x1;  // previous solve's other-end Ritz vector (start = x0 + x1), or null
+    double* other_out; // this solve's other-end Ritz vector (unit), or null
 };
 
 __device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
@@ -300,6 +305,8 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     auto gsync = [&]() {
         if (gridDim.x == 1)
             __syncthreads();
+        else if (a.cluster)
+            cg::this_cluster().sync();
         else
             grid.sync();
     };
@@ -417,12 +424,18 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     };
     for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
         const double r = hash_unit(static_cast<uint64_t>(t), 0x5eedull);
-        a.w[t] = a.x0 ? a.x0[t] + 1e-3 * r / sqrt(static_cast<double>(n)) : r;
+        a.w[t] = a.x0 ? a.x0[t] + (a.x1 ? a.x1[t] : 0.0) + 1e-3 * r / sqrt(static_cast<double>(n)) : r;
     }
     set_v0_from_w();
 
     int restarts = 0, breakdowns = 0;
     int j = 0;
+    // A warm-started solve (x0 = previous eigenvector) needs about as many
+    // steps as the previous one of the same operator: skip the convergence
+    // checks before that (each check is a sequential T-eigen solve on CTA 0).
+    // The hint is reset by every cold start, so a solve is reproducible.
+    int first_check = a.min_steps;
+    if (a.warm && a.hint) first_check = max(a.min_steps, (*a.hint / a.check_every - 1) * a.check_every);
     bool zero_op = false;
     double anorm = 0.0;
     double inv_beta = 1.0;  // V[:,j] = w * inv_beta for j > 0 (materialised in phase B)
@@ -490,7 +503,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         ++j;
         const bool size_limit = (j == a.maxm) || space_full;
         mark(4);
-        if (((j >= a.min_steps && j % a.check_every == 0) && !breakdown) || size_limit) {
+        if (((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit) {
             if (blockIdx.x == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts);
             mark(5);
             gsync();
@@ -500,6 +513,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
                 if (restarts >= a.max_restarts) break;  // best effort: ctl[0] stays 0
                 // restart from (x_lo + x_hi): both ends stay represented
                 ++restarts;
+                first_check = a.min_steps;
                 for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
                     double s0 = 0.0, s1 = 0.0;
                     for (int k = 0; k < j; ++k) {
@@ -533,14 +547,21 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     const int m = j;
     const int pick = a.ctl[1];
     const double* s = a.sT + (pick ? kMaxKrylov : 0);
+    const double* so = a.sT + (pick ? 0 : kMaxKrylov);
     double best = -1.0;
     int64_t besti = 0;
-    double ss = 0.0;
+    double ss = 0.0, sso = 0.0;
     for (int64_t i = gtid; i < n; i += gstride) {
-        double x = 0.0;
-        for (int k = 0; k < m; ++k) x = fma(a.V[i + static_cast<int64_t>(k) * n], s[k], x);
+        double x = 0.0, xo = 0.0;
+        for (int k = 0; k < m; ++k) {
+            const double v = a.V[i + static_cast<int64_t>(k) * n];
+            x = fma(v, s[k], x);
+            xo = fma(v, so[k], xo);
+        }
         a.out_vec[i] = x;
+        if (a.other_out) a.other_out[i] = xo;
         ss = fma(x, x, ss);
+        sso = fma(xo, xo, sso);
         if (fabs(x) > best) {
             best = fabs(x);
             besti = i;
@@ -564,7 +585,9 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         bi[warp] = besti;
     }
     ss = cta_sum(ss, red);
+    sso = cta_sum(sso, red);
     if (threadIdx.x == 0) {
+        a.part[3 * G + blockIdx.x] = sso;
         double b0 = bv[0];
         int64_t i0 = bi[0];
         for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k)
@@ -590,10 +613,17 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     const double nrm = sqrt(grid_total(a.part, 0));
     const double sgn = a.out_vec[i0] < 0.0 ? -1.0 : 1.0;
     gsync();
-    for (int64_t i = gtid; i < n; i += gstride) a.out_vec[i] = sgn * a.out_vec[i] / nrm;
+    double nrm_o = 0.0;
+    for (int b = 0; b < G; ++b) nrm_o += a.part[3 * G + b];
+    nrm_o = sqrt(nrm_o);
+    for (int64_t i = gtid; i < n; i += gstride) {
+        a.out_vec[i] = sgn * a.out_vec[i] / nrm;
+        if (a.other_out && nrm_o > 0.0) a.other_out[i] /= nrm_o;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         for (int k = 0; k < 8; ++k) a.stats[8 + k] = static_cast<double>(tacc[k]);
         *a.out_value = a.stats[4];
+        if (a.hint) *a.hint = restarts == 0 ? m : 0;
         a.ctl[2] = m;
         a.ctl[3] = restarts;
         a.ctl[4] = breakdowns;
@@ -603,6 +633,9 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
 struct EigPlan {
     BlockOp op;
     DescCache<BlockOp> dop;
+    DeviceBuffer hint;   // one int: steps of the last solve in the solver's chain
+    DeviceBuffer other;  // n: other-end Ritz vector of the last solve in the chain
+    bool other_valid = false;
     int64_t coldot_n = 0, rowpart_n = 0;
 };
 
@@ -611,7 +644,7 @@ struct EigPlan {
 namespace {
 
 void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_dev,
-                 double* vec_dev, int* info_host, double* stats_host) {
+                 double* vec_dev, int* info_host, double* stats_host, bool solver_chain = false) {
     const int64_t n = P.op.n;
     const int maxm = static_cast<int>(std::min<int64_t>(n, 320));
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
@@ -655,6 +688,18 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.op = P.dop.get(op, ctx->stream);
     a.out_value = value_dev;
     a.out_vec = vec_dev;
+    if (solver_chain) {
+        if (!P.hint.ptr) {
+            P.hint.ensure(sizeof(int));
+            R1_CUDA(cudaMemsetAsync(P.hint.ptr, 0, sizeof(int), ctx->stream));
+        }
+        a.hint = P.hint.as<int>();
+        a.warm = x0 != nullptr ? 1 : 0;
+        P.other.ensure(static_cast<size_t>(n) * sizeof(double));
+        a.x1 = x0 != nullptr && P.other_valid ? P.other.as<double>() : nullptr;
+        a.other_out = P.other.as<double>();
+        P.other_valid = true;
+    }
 
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
     static int configured = -1;
@@ -680,10 +725,36 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     const int auto_grid = (n <= 1024 && op_bytes <= (int64_t(2) << 20)) ? 1 : ctx->num_sms;
     (void)auto_grid;
     static const char* g1 = std::getenv("R1_EIG_SMALL_ONE_CTA");
-    const int grid = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs)))
-                        : (g1 && std::atoi(g1) ? auto_grid : ctx->num_sms);
-    R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel), dim3(grid),
-                                        dim3(kEigThreads), args, kEigDynSmem, ctx->stream));
+    static const char* gc = std::getenv("R1_EIG_CLUSTER");
+    const int cl_size = gc ? std::max(0, std::min(16, std::atoi(gc))) : 0;
+    if (cl_size > 1 && !gs) {
+        // the whole Lanczos run on ONE thread-block cluster: cluster barriers
+        // instead of cooperative grid syncs
+        static int cl_configured = -1;
+        if (cl_configured != ctx->device) {
+            R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cl_configured = ctx->device;
+        }
+        a.cluster = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cl_size);
+        cfg.blockDim = dim3(kEigThreads);
+        cfg.dynamicSmemBytes = kEigDynSmem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl_size;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        R1_CUDA(cudaLaunchKernelEx(&cfg, lanczos_kernel, a));
+    } else {
+        const int grid = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs)))
+                            : (g1 && std::atoi(g1) ? auto_grid : ctx->num_sms);
+        R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel), dim3(grid),
+                                            dim3(kEigThreads), args, kEigDynSmem, ctx->stream));
+    }
     check_launch(ctx, "lanczos_kernel");
     static const bool dbg = std::getenv("R1_DEBUG_EIG") != nullptr;
     if (dbg) {
@@ -744,7 +815,7 @@ void forget_eig_plans(r1_context* ctx) {
 // res_lo, res_hi, value].
 void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                 const double* x0, double* value_dev, double* vec_dev, int* info_host,
-                double* stats_host) {
+                double* stats_host, bool solver_chain) {
     if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "eig: unsupported order");
     auto& P = eig_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
     if (!P) {
@@ -753,7 +824,7 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
     }
     P->op.blocks = blocks;
     P->op.dense = nullptr;
-    run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host);
+    run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host, solver_chain);
 }
 
 // Same on a dense symmetric n x n matrix S (device, column-major).

@@ -230,7 +230,7 @@ RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
         Marks mk;
         mk.a = ev.rec(st);
         eig_blocks(w.ctx, w.dims.data(), d, w.J, have_prev ? w.Xprev : nullptr, w.mu, w.X, nullptr,
-                   nullptr);
+                   nullptr, true);
         mk.b = ev.rec(st);
         split_stack(w.ctx, w.dims.data(), d, w.X, w.Umid, w.Xhat, w.flags);
         mk.c = ev.rec(st);

@@ -24,9 +24,11 @@ void flip_first(r1_context* ctx, double* u0, int64_t n0, const double* lam_in, d
 void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                        double* S);
 bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, double* y);
+// solver_chain: x0 is the previous eigenvector of the same operator inside one
+// solve (nullptr on its first iteration): the step-count hint is used / reset.
 void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                 const double* x0, double* value_dev, double* vec_dev, int* info_host,
-                double* stats_host);
+                double* stats_host, bool solver_chain = false);
 void eig_dense(r1_context* ctx, int64_t n, const double* S, const double* x0, double* value_dev,
                double* vec_dev, int* info_host, double* stats_host);
 void dot_device(r1_context* ctx, const double* x, const double* y, uint64_t n, double* out_dev);
