@@ -181,15 +181,15 @@ __device__ void tri_eigvec(const double* a, const double* b, int m, double theta
 }
 
 // CTA 0: extremes of T_m, eigenvectors, bounds, convergence decision.
-__device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact, int restarts) {
+__device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact, int restarts,
+                           double* scratch, int stride) {
     // tridiagonal, two inverse-iteration workspaces and the two T-eigenvectors
-    // live in dynamic shared memory (kEigDynSmem bytes)
-    extern __shared__ double dsm[];
-    double* ta = dsm;
-    double* tb = ta + kMaxKrylov;
-    double* work = tb + kMaxKrylov;
-    double* work2 = work + 5 * kMaxKrylov;
-    double* sv[2] = {work2 + 5 * kMaxKrylov, work2 + 6 * kMaxKrylov};
+    // live in shared memory: 14 * stride doubles at scratch (stride >= m)
+    double* ta = scratch;
+    double* tb = ta + stride;
+    double* work = tb + stride;
+    double* work2 = work + 5 * stride;
+    double* sv[2] = {work2 + 5 * stride, work2 + 6 * stride};
     __shared__ double lohi[4];  // [a_lo, b_lo, a_hi, b_hi] intervals
     __shared__ int cnt[kEigThreads];
     __shared__ double theta[2];
@@ -504,7 +504,10 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         const bool size_limit = (j == a.maxm) || space_full;
         mark(4);
         if (((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit) {
-            if (blockIdx.x == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts);
+            if (blockIdx.x == 0) {
+                extern __shared__ double dsm[];
+                t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts, dsm, kMaxKrylov);
+            }
             mark(5);
             gsync();
             mark(6);
@@ -630,6 +633,291 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     }
 }
 
+// ---------------------------------------------------------------------------
+// Small operators (n <= kSmallN): the whole Lanczos run on ONE thread-block
+// cluster (<= 16 CTAs).  CTA c owns rows [c R, (c+1) R) of every length-n
+// vector; its rows of J (dense, built once per call from the blocks; shared
+// memory when they fit, else an L2-resident scratch), of the Krylov basis and
+// of w stay with it.  Three cluster barriers per step: after the partial dots
+// of each CGS2 pass and after publishing the next (unnormalised) vector with
+// the ||w||^2 partials; partials travel as DSMEM stores and every sum runs
+// over the G partials in CTA order (deterministic).  Same start vector,
+// convergence test (t_extremes), breakdown / restart handling and pick / sign
+// rules as lanczos_kernel; the lanczos_kernel's grid syncs and L2 round
+// trips cost ~20 us per step at n = 300..800, this ~4 us.
+constexpr int kSmallN = 1024;
+constexpr int kSmallMaxM = 192;
+
+__global__ void __launch_bounds__(kEigThreads, 1)
+    lanczos_cluster_kernel(const EigArgs a, double* __restrict__ Sg, int s_in_smem) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double dsm[];
+    const BlockOp& op = *a.op;
+    const int n = static_cast<int>(a.n);
+    const int G = gridDim.x, me = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = kEigThreads / 32;
+    const int R = (n + G - 1) / G;
+    const int r0 = min(n, me * R), r1 = min(n, r0 + R), Rm = r1 - r0;
+    const int ld = a.maxm + 1;
+    double* text = dsm;             // t_extremes scratch, 14 * ld
+    double* Vs = text + 14 * ld;    // own rows of V: Vs[k * R + r]
+    double* hp1 = Vs + ld * R;      // pushed pass-1 partials [16][ld]
+    double* hp2 = hp1 + 16 * ld;    // pushed pass-2 partials [16][ld]
+    double* wfull = hp2 + 16 * ld;  // pushed next vector (unnormalised), n
+    double* ws = wfull + n;         // own rows of w, R
+    double* Sown = s_in_smem ? ws + R : Sg + static_cast<size_t>(me) * R * n;  // own rows of J, [R][n]
+    __shared__ double hsh[kSmallMaxM + 1];
+    __shared__ double red[32];
+    __shared__ double nrmp[16];
+    __shared__ double fin[5][16];
+
+    // ---- own rows of J (row t = column t: symmetric)
+    for (int e = tid; e < Rm * n; e += kEigThreads) {
+        const int r = e / n, u = e - r * n, t = r0 + r;
+        double v;
+        if (op.dense) {
+            v = op.dense[t + static_cast<size_t>(u) * n];
+        } else {
+            int m = 0, q = 0;
+            while (t >= op.offs[m + 1]) ++m;
+            while (u >= op.offs[q + 1]) ++q;
+            const int64_t i = t - op.offs[m], jj = u - op.offs[q];
+            v = 0.0;
+            if (q > m) v = op.blocks[op.boff[pair_index(m, q, op.d)] + i + jj * op.dims[m]];
+            else if (q < m) v = op.blocks[op.boff[pair_index(q, m, op.d)] + jj + i * op.dims[q]];
+        }
+        Sown[static_cast<size_t>(r) * n + u] = v;
+    }
+    // publish own rows of w and the CTA's ||w||^2 partial to every CTA; after
+    // the barrier every CTA returns sqrt(sum of the partials in CTA order)
+    auto publish = [&]() {
+        double ss = 0.0;
+        for (int r = tid; r < Rm; r += kEigThreads) ss = fma(ws[r], ws[r], ss);
+        ss = cta_sum(ss, red);
+        if (tid < G) *cl.map_shared_rank(&nrmp[me], tid) = ss;
+        for (int e = tid; e < G * Rm; e += kEigThreads) {
+            const int c = e / Rm, r = e - c * Rm;
+            *cl.map_shared_rank(&wfull[r0 + r], c) = ws[r];
+        }
+        cl.sync();
+        double t = 0.0;
+        for (int c = 0; c < G; ++c) t += nrmp[c];
+        return sqrt(t);
+    };
+    // one classical Gram-Schmidt pass of w (own rows) against V[:, 0..j]
+    auto cgs_pass = [&](double* hp, int j) {
+        for (int k = warp; k <= j; k += nw) {
+            const double* vk = Vs + k * R;
+            double s = 0.0;
+            for (int r = lane; r < Rm; r += 32) s = fma(vk[r], ws[r], s);
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane < G) *cl.map_shared_rank(&hp[me * ld + k], lane) = s;
+        }
+        cl.sync();
+        for (int k = tid; k <= j; k += kEigThreads) {
+            double h = 0.0;
+            for (int c = 0; c < G; ++c) h += hp[c * ld + k];
+            hsh[k] = h;
+        }
+        __syncthreads();
+        for (int r = tid; r < Rm; r += kEigThreads) {
+            double s = 0.0;
+            for (int k = 0; k <= j; ++k) s = fma(Vs[k * R + r], hsh[k], s);
+            ws[r] -= s;
+        }
+        __syncthreads();
+    };
+
+    for (int r = tid; r < Rm; r += kEigThreads) {
+        const int t = r0 + r;
+        const double rr = hash_unit(static_cast<uint64_t>(t), 0x5eedull);
+        ws[r] = a.x0 ? a.x0[t] + (a.x1 ? a.x1[t] : 0.0) + 1e-3 * rr / sqrt(static_cast<double>(n)) : rr;
+    }
+    __syncthreads();
+    double inv_beta = 1.0 / publish();
+
+    int restarts = 0, breakdowns = 0;
+    int j = 0;
+    int first_check = a.min_steps;
+    if (a.warm && a.hint) first_check = max(a.min_steps, (*a.hint / a.check_every - 1) * a.check_every);
+    bool zero_op = false;
+    double anorm = 0.0;
+    for (;;) {
+        // v_j = w * inv_beta (own rows into V, all rows from wfull), w = J v_j
+        for (int r = tid; r < Rm; r += kEigThreads) Vs[j * R + r] = ws[r] * inv_beta;
+        for (int r = warp; r < Rm; r += nw) {
+            const double* sr = Sown + static_cast<size_t>(r) * n;
+            double s0 = 0.0, s1 = 0.0;
+            int u = lane;
+            for (; u + 32 < n; u += 64) {
+                s0 = fma(sr[u], wfull[u], s0);
+                s1 = fma(sr[u + 32], wfull[u + 32], s1);
+            }
+            if (u < n) s0 = fma(sr[u], wfull[u], s0);
+            double s = s0 + s1;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) ws[r] = s * inv_beta * op.scale;
+        }
+        __syncthreads();
+        cgs_pass(hp1, j);
+        const double h1j = hsh[j];
+        cgs_pass(hp2, j);
+        const double alpha = h1j + hsh[j];
+        double nrm = publish();
+        anorm = fmax(anorm, fabs(alpha) + nrm + (j > 0 ? a.beta[j - 1] : 0.0));
+        if (j == 0 && restarts == 0 && anorm == 0.0) {
+            zero_op = true;  // J v0 == 0 for a dense random v0: J == 0 (see lanczos_kernel)
+            break;
+        }
+        const bool space_full = (j + 1 == n);
+        const bool breakdown = !space_full && nrm <= 1e-13 * anorm;
+        if (me == 0 && tid == 0) {
+            a.alpha[j] = alpha;
+            a.beta[j] = breakdown ? 0.0 : nrm;
+        }
+        if (breakdown) {
+            ++breakdowns;
+            for (int r = tid; r < Rm; r += kEigThreads)
+                ws[r] = hash_unit(static_cast<uint64_t>(r0 + r), 0xb00ull + breakdowns);
+            __syncthreads();
+            cgs_pass(hp1, j);
+            cgs_pass(hp2, j);
+            nrm = publish();
+        }
+        inv_beta = 1.0 / nrm;
+        ++j;
+        const bool size_limit = (j == a.maxm) || space_full;
+        if (((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit) {
+            if (me == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts, text, ld);
+            cl.sync();
+            if (*reinterpret_cast<volatile int*>(a.ctl)) break;
+            if (size_limit) {
+                if (restarts >= a.max_restarts) break;  // best effort: ctl[0] stays 0
+                ++restarts;
+                first_check = a.min_steps;
+                for (int r = tid; r < Rm; r += kEigThreads) {
+                    double s0 = 0.0, s1 = 0.0;
+                    for (int k = 0; k < j; ++k) {
+                        const double v = Vs[k * R + r];
+                        s0 = fma(v, a.sT[k], s0);
+                        s1 = fma(v, a.sT[kMaxKrylov + k], s1);
+                    }
+                    ws[r] = s0 + s1;
+                }
+                __syncthreads();
+                inv_beta = 1.0 / publish();
+                j = 0;
+                anorm = 0.0;
+            }
+        }
+    }
+
+    if (zero_op) {
+        for (int r = tid; r < Rm; r += kEigThreads) a.out_vec[r0 + r] = r0 + r == n - 1 ? 1.0 : 0.0;
+        if (me == 0 && tid == 0) {
+            *a.out_value = 0.0;
+            a.ctl[0] = 1;
+            a.ctl[1] = 1;
+            a.ctl[2] = 1;
+            a.ctl[3] = 0;
+            a.ctl[4] = 0;
+        }
+        cl.sync();
+        return;
+    }
+    // ---- Ritz vectors of both ends (own rows); sign rule needs the global
+    // arg-max |x| (lowest index on ties) and both norms
+    const int m = j;
+    const int pick = *reinterpret_cast<volatile int*>(a.ctl + 1);
+    const double* s = a.sT + (pick ? kMaxKrylov : 0);
+    const double* so = a.sT + (pick ? 0 : kMaxKrylov);
+    double* xo_s = hp1;  // reuse: own rows of the other-end vector
+    double best = -1.0, bsg = 0.0, ss = 0.0, sso = 0.0;
+    int besti = n;
+    for (int r = tid; r < Rm; r += kEigThreads) {
+        double x = 0.0, xo = 0.0;
+        for (int k = 0; k < m; ++k) {
+            const double v = Vs[k * R + r];
+            x = fma(v, s[k], x);
+            xo = fma(v, so[k], xo);
+        }
+        ws[r] = x;
+        xo_s[r] = xo;
+        ss = fma(x, x, ss);
+        sso = fma(xo, xo, sso);
+        if (fabs(x) > best) {
+            best = fabs(x);
+            besti = r0 + r;
+            bsg = x;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, besti, off);
+        const double os = __shfl_xor_sync(0xffffffffu, bsg, off);
+        if (ov > best || (ov == best && oi < besti)) {
+            best = ov;
+            besti = oi;
+            bsg = os;
+        }
+    }
+    __shared__ double bv[32], bs[32];
+    __shared__ int bi[32];
+    if (lane == 0) {
+        bv[warp] = best;
+        bi[warp] = besti;
+        bs[warp] = bsg;
+    }
+    ss = cta_sum(ss, red);
+    sso = cta_sum(sso, red);
+    if (tid < G) {
+        double b0 = bv[0], s0 = bs[0];
+        int i0 = bi[0];
+        for (int k = 1; k < nw; ++k)
+            if (bv[k] > b0 || (bv[k] == b0 && bi[k] < i0)) {
+                b0 = bv[k];
+                i0 = bi[k];
+                s0 = bs[k];
+            }
+        *cl.map_shared_rank(&fin[0][me], tid) = b0;
+        *cl.map_shared_rank(&fin[1][me], tid) = static_cast<double>(i0);
+        *cl.map_shared_rank(&fin[2][me], tid) = s0;
+        *cl.map_shared_rank(&fin[3][me], tid) = ss;
+        *cl.map_shared_rank(&fin[4][me], tid) = sso;
+    }
+    cl.sync();
+    double b0 = -1.0, s0 = 0.0, nrm2 = 0.0, nrm2o = 0.0;
+    int i0 = n;
+    for (int c = 0; c < G; ++c) {
+        const int ii = static_cast<int>(fin[1][c]);
+        if (fin[0][c] > b0 || (fin[0][c] == b0 && ii < i0)) {
+            b0 = fin[0][c];
+            i0 = ii;
+            s0 = fin[2][c];
+        }
+        nrm2 += fin[3][c];
+        nrm2o += fin[4][c];
+    }
+    const double nrm = sqrt(nrm2), nrm_o = sqrt(nrm2o);
+    const double sgn = s0 < 0.0 ? -1.0 : 1.0;
+    for (int r = tid; r < Rm; r += kEigThreads) {
+        a.out_vec[r0 + r] = sgn * ws[r] / nrm;
+        if (a.other_out && nrm_o > 0.0) a.other_out[r0 + r] = xo_s[r] / nrm_o;
+    }
+    if (me == 0 && tid == 0) {
+        for (int k = 0; k < 8; ++k) a.stats[8 + k] = 0.0;
+        *a.out_value = a.stats[4];
+        if (a.hint) *a.hint = restarts == 0 ? m : 0;
+        a.ctl[2] = m;
+        a.ctl[3] = restarts;
+        a.ctl[4] = breakdowns;
+    }
+    cl.sync();  // no CTA exits while others may still write its shared memory
+}
+
 struct EigPlan {
     BlockOp op;
     DescCache<BlockOp> dop;
@@ -643,13 +931,52 @@ struct EigPlan {
 
 namespace {
 
+void finish_lanczos(r1_context* ctx, const EigArgs& a, int* info_host, double* stats_host) {
+    const int64_t n = a.n;
+    static const bool dbg = std::getenv("R1_DEBUG_EIG") != nullptr;
+    if (dbg) {
+        int ctl[5];
+        double st[16];
+        R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        static const bool dbg_t = std::getenv("R1_DEBUG_EIG_T") != nullptr;
+        if (dbg_t) {
+            std::vector<double> al(ctl[2]), be(ctl[2]);
+            R1_CUDA(cudaMemcpy(al.data(), a.alpha, al.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            R1_CUDA(cudaMemcpy(be.data(), a.beta, be.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int k = 0; k < std::min(ctl[2], 24); ++k)
+                std::fprintf(stderr, "  T[%d] alpha=%.6e beta=%.6e\n", k, al[k], be[k]);
+        }
+        std::fprintf(stderr,
+                     "[r1 eig] n=%lld conv=%d pick=%d steps=%d restarts=%d breakdowns=%d "
+                     "lo=%.17g hi=%.17g res_lo=%.3g res_hi=%.3g | us: A=%.1f syncA=%.1f B=%.1f "
+                     "cgs2=%.1f tail=%.1f text=%.1f synct=%.1f other=%.1f\n",
+                     static_cast<long long>(n), ctl[0], ctl[1], ctl[2], ctl[3], ctl[4], st[0], st[1],
+                     st[2], st[3], st[8] * 1e-3, st[9] * 1e-3, st[10] * 1e-3, st[11] * 1e-3,
+                     st[12] * 1e-3, st[13] * 1e-3, st[14] * 1e-3, st[15] * 1e-3);
+    }
+    if (info_host || stats_host) {
+        int ctl[5];
+        double st[5];
+        R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (info_host)
+            for (int k = 0; k < 5; ++k) info_host[k] = ctl[k];
+        if (stats_host)
+            for (int k = 0; k < 5; ++k) stats_host[k] = st[k];
+    }
+}
+
 void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_dev,
                  double* vec_dev, int* info_host, double* stats_host, bool solver_chain = false) {
     const int64_t n = P.op.n;
     const int maxm = static_cast<int>(std::min<int64_t>(n, 320));
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
                          2 * static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 8) +
-                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 256;
+                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 256 +
+                         (n <= kSmallN ? (n + 16) * n : 0);
     ctx->ws_eig.ensure(need * sizeof(double));
     double* base = ctx->ws_eig.as<double>();
     int64_t off = 0;
@@ -702,6 +1029,65 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     }
 
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
+    static const char* gs = std::getenv("R1_EIG_GRID");
+    static const char* gc = std::getenv("R1_EIG_CLUSTER");
+    static const char* gsm = std::getenv("R1_EIG_SMALL");
+    if (n <= kSmallN && !gs && !gc && !(gsm && std::atoi(gsm) == 0)) {
+        // one thread-block cluster, rows of J / V / w on chip
+        const int G = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (n + 15) / 16)));
+        const int64_t R = (n + G - 1) / G;
+        const int mm = static_cast<int>(std::min<int64_t>(n, kSmallMaxM));
+        const int64_t ld = mm + 1;
+        const int64_t base_d = 14 * ld + ld * R + 32 * ld + n + R;
+        const int64_t with_s = base_d + R * n;
+        constexpr int64_t cap = 215 * 1024 / 8;
+        static int small_state = -1;  // -1 unknown, 0 unavailable, 1 configured
+        if (small_state < 0) {
+            small_state = 0;
+            if (cudaFuncSetAttribute(lanczos_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                    cudaSuccess &&
+                cudaFuncSetAttribute(lanczos_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(cap * 8)) == cudaSuccess) {
+                cudaLaunchConfig_t q{};
+                q.gridDim = dim3(16);
+                q.blockDim = dim3(kEigThreads);
+                q.dynamicSmemBytes = static_cast<size_t>(cap * 8);
+                cudaLaunchAttribute qa[1];
+                qa[0].id = cudaLaunchAttributeClusterDimension;
+                qa[0].val.clusterDim.x = 16;
+                qa[0].val.clusterDim.y = 1;
+                qa[0].val.clusterDim.z = 1;
+                q.attrs = qa;
+                q.numAttrs = 1;
+                int clusters = 0;
+                if (cudaOccupancyMaxActiveClusters(&clusters, lanczos_cluster_kernel, &q) == cudaSuccess &&
+                    clusters >= 1)
+                    small_state = 1;
+            }
+            cudaGetLastError();
+        }
+        if (small_state == 1 && base_d <= cap) {
+            const int s_in = with_s <= cap ? 1 : 0;
+            double* Sg = s_in ? nullptr : take(static_cast<int64_t>(G) * R * n);
+            a.maxm = mm;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(G);
+            cfg.blockDim = dim3(kEigThreads);
+            cfg.dynamicSmemBytes = static_cast<size_t>(s_in ? with_s : base_d) * sizeof(double);
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = G;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            R1_CUDA(cudaLaunchKernelEx(&cfg, lanczos_cluster_kernel, a, Sg, s_in));
+            check_launch(ctx, "lanczos_cluster_kernel");
+            finish_lanczos(ctx, a, info_host, stats_host);
+            return;
+        }
+    }
     static int configured = -1;
     if (configured != ctx->device) {
         R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -716,7 +1102,6 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     // Small operators (C1/C4-sized: n <= 1024 and <= 2 MB of blocks) run on one
     // CTA with CTA barriers: a cooperative grid sync costs ~5 us, more than
     // a whole Lanczos step's work there.
-    static const char* gs = std::getenv("R1_EIG_GRID");
     const int64_t op_bytes = 8 * (P.op.dense ? n * n : P.coldot_n * 0 + [&] {
         int64_t b = 0;
         for (int p = 0; p < P.op.npairs; ++p) b += P.op.dims[P.op.pm[p]] * P.op.dims[P.op.pn[p]];
@@ -725,7 +1110,6 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     const int auto_grid = (n <= 1024 && op_bytes <= (int64_t(2) << 20)) ? 1 : ctx->num_sms;
     (void)auto_grid;
     static const char* g1 = std::getenv("R1_EIG_SMALL_ONE_CTA");
-    static const char* gc = std::getenv("R1_EIG_CLUSTER");
     const int cl_size = gc ? std::max(0, std::min(16, std::atoi(gc))) : 0;
     if (cl_size > 1 && !gs) {
         // the whole Lanczos run on ONE thread-block cluster: cluster barriers
@@ -756,40 +1140,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
                                             dim3(kEigThreads), args, kEigDynSmem, ctx->stream));
     }
     check_launch(ctx, "lanczos_kernel");
-    static const bool dbg = std::getenv("R1_DEBUG_EIG") != nullptr;
-    if (dbg) {
-        int ctl[5];
-        double st[16];
-        R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
-        R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
-        R1_CUDA(cudaStreamSynchronize(ctx->stream));
-        static const bool dbg_t = std::getenv("R1_DEBUG_EIG_T") != nullptr;
-        if (dbg_t) {
-            std::vector<double> al(ctl[2]), be(ctl[2]);
-            R1_CUDA(cudaMemcpy(al.data(), a.alpha, al.size() * sizeof(double), cudaMemcpyDeviceToHost));
-            R1_CUDA(cudaMemcpy(be.data(), a.beta, be.size() * sizeof(double), cudaMemcpyDeviceToHost));
-            for (int k = 0; k < std::min(ctl[2], 24); ++k)
-                std::fprintf(stderr, "  T[%d] alpha=%.6e beta=%.6e\n", k, al[k], be[k]);
-        }
-        std::fprintf(stderr,
-                     "[r1 eig] n=%lld conv=%d pick=%d steps=%d restarts=%d breakdowns=%d "
-                     "lo=%.17g hi=%.17g res_lo=%.3g res_hi=%.3g | us: A=%.1f syncA=%.1f B=%.1f "
-                     "cgs2=%.1f tail=%.1f text=%.1f synct=%.1f other=%.1f\n",
-                     static_cast<long long>(n), ctl[0], ctl[1], ctl[2], ctl[3], ctl[4], st[0], st[1],
-                     st[2], st[3], st[8] * 1e-3, st[9] * 1e-3, st[10] * 1e-3, st[11] * 1e-3,
-                     st[12] * 1e-3, st[13] * 1e-3, st[14] * 1e-3, st[15] * 1e-3);
-    }
-    if (info_host || stats_host) {
-        int ctl[5];
-        double st[5];
-        R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
-        R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
-        R1_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (info_host)
-            for (int k = 0; k < 5; ++k) info_host[k] = ctl[k];
-        if (stats_host)
-            for (int k = 0; k < 5; ++k) stats_host[k] = st[k];
-    }
+    finish_lanczos(ctx, a, info_host, stats_host);
 }
 
 using PlanKey = std::pair<r1_context*, std::vector<uint64_t>>;
