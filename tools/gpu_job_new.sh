@@ -1,4 +1,2 @@
-timeout 120 python tools/c1_probe.py C1 2>&1 | tail -1
-timeout 120 python tools/c1_probe.py C4 2>&1 | tail -1
-timeout 200 python tools/solve_probe.py C3 --alg hoscf,ihoscf 2>&1 | grep rep1
-timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
+timeout 900 python bench.py > gpurun_out/r01_bench.json 2> gpurun_out/r01_bench.err; tail -c 400 gpurun_out/r01_bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bk_launches2.csv python tools/bk_probe.py 3000 6500 > gpurun_out/bk_ncu.log 2>&1; tail -1 gpurun_out/bk_ncu.log
