@@ -440,7 +440,15 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
     const int gtid = me * kBkThreads + tid;
     double* A = a.A;
     auto col = [&](int c) { return A + static_cast<size_t>(c) * static_cast<size_t>(n); };
-    auto owner = [&](int i) { return (i - k0) / chunk; };
+    // owner CTA of row i: (i - k0) / chunk by a float reciprocal and a +-1 fixup
+    const float inv_chunk = 1.0f / static_cast<float>(chunk);
+    auto owner = [&](int i) {
+        const int x = i - k0;
+        int q = static_cast<int>(static_cast<float>(x) * inv_chunk);
+        if (q * chunk > x) --q;
+        else if ((q + 1) * chunk <= x) ++q;
+        return q;
+    };
     // local row r is always handled by thread r % kBkThreads (the thread that
     // prefetched / patched a raw entry is the one that reads it)
     auto first_row = [&](int grow) {
