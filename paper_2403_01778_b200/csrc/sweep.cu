@@ -1400,8 +1400,13 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         }
         oa.O = L.O;
         oa.W = resolve(L.w);
-        outer_weights_kernel<<<grid_for(L.O, 256, ctx->num_sms), 256, 0, ctx->stream>>>(oa);
-        check_launch(ctx, "outer_weights_kernel");
+        const double* Wsrc = oa.W;
+        if (oa.nout == 1) {
+            Wsrc = oa.u[0];  // order 3: the outer weights are u_2 itself
+        } else {
+            outer_weights_kernel<<<grid_for(L.O, 256, ctx->num_sms), 256, 0, ctx->stream>>>(oa);
+            check_launch(ctx, "outer_weights_kernel");
+        }
 
         SweepArgs s{};
         s.A = resolve(L.input);
@@ -1413,7 +1418,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.MI1 = L.MI1;
         s.u0 = factors_dev + foff[L.modes[0]];
         s.u1 = factors_dev + foff[L.modes[1]];
-        s.W = oa.W;
+        s.W = Wsrc;
         s.r0 = L.r0;
         s.t1 = L.t1;
         s.G0 = L.G0;
