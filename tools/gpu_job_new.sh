@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests/test_sweep_gpu.py tests/test_fullsize_gpu.py tests/test_solver_gpu.py -q 2>&1 | tail -2
-for i in 1 2; do timeout 300 python bench.py --skip-solve --skip-cpu --skip-configs --e2e-steps 2 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['roofline']['kernel_ms_per_launch'], d['roofline']['frac'], d['gpu_launches'], d['clocks'])"; done
+timeout 900 python -m pytest tests/test_fullsize_gpu.py -q -k "c3_fixed" 2>&1 | tail -3
