@@ -70,6 +70,7 @@ struct EigArgs {
     int warm;        // 1: x0 is the previous eigenvector (use and update *hint)
     const double* x1;  // previous solve's other-end Ritz vector (start = x0 + x1), or null
     double* other_out; // this solve's other-end Ritz vector (unit), or null
+    int debug_text;    // development: print the phase split of t_extremes
 };
 
 __device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
@@ -103,80 +104,137 @@ __device__ double grid_total(const double* part, int slot) {
     return s;
 }
 
-// Number of eigenvalues of the symmetric tridiagonal (a, b) that are < x.
-__device__ int sturm_count(const double* a, const double* b, int m, double x, double pivmin) {
+// Number of eigenvalues of the symmetric tridiagonal (a, b) that are < x:
+// sign changes of the leading principal minors p_k(x) = (a_k - x) p_{k-1} -
+// b_{k-1}^2 p_{k-2} (Sturm).  No division on the chain (a division per step
+// made this ~160 cycles per row); the pair (p_{k-1}, p_k) is rescaled by an
+// exact power of two every 8 rows, which keeps the signs.  A zero minor
+// counts as a sign change (the pivmin convention of the LDL^T form: d_k =
+// p_k / p_{k-1} = 0 is replaced by a tiny negative pivot).
+__device__ int sturm_count(const double* a, const double* b2, int m, double x) {
     int c = 0;
-    double q = a[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    if (q < 0) ++c;
-    for (int i = 1; i < m; ++i) {
-        q = (a[i] - x) - b[i - 1] * b[i - 1] / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        if (q < 0) ++c;
+    double pm = 1.0, p = a[0] - x;
+    bool neg = !(p > 0.0);  // sign of the last minor as used for counting
+    c += neg;
+    auto step = [&](int i) {
+        const double pn = fma(a[i] - x, p, -b2[i - 1] * pm);
+        pm = p;
+        p = pn;
+        // sign / zero tests on the bits (integer pipe, not the FP64 pipe)
+        const long long bits = __double_as_longlong(p);
+        const bool ng = (bits << 1) == 0 ? !neg : bits < 0;
+        c += ng != neg;
+        neg = ng;
+    };
+    auto rescale = [&]() {
+        const double mx = fmax(fabs(p), fabs(pm));
+        const int e = mx > 0.0 && mx < INFINITY ? ilogb(mx) : 0;
+        if (e > 512 || e < -512) {
+            p = scalbn(p, -e);
+            pm = scalbn(pm, -e);
+        }
+    };
+    // blocks of 8 rows: the loads and a_i - x hoist off the chain, which is
+    // then one FMA per row
+    int i = 1;
+    for (; i + 8 <= m; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) step(i + u);
+        rescale();
     }
+    for (; i < m; ++i) step(i);
     return c;
 }
 
 // Inverse iteration for the eigenvector of T (size m) at shift theta; s unit.
 __device__ void tri_eigvec(const double* a, const double* b, int m, double theta, double tnorm,
                            double* s, double* work) {
-    // work: d[m], du[m], du2[m], dl[m], piv flags in ipiv (as doubles)
+    // work: d[m] (then 1 / d), du[m], du2[m], l[m], row-swap flags[m].  One
+    // thread; the recurrences carry their running values in registers so a
+    // step's chain is one or two FMAs (shared-memory round trips on the chain
+    // made the three passes ~40 us at m = 64).
     double* d = work;
     double* du = work + m;
     double* du2 = work + 2 * m;
     double* l = work + 3 * m;
     double* sw = work + 4 * m;  // 1.0 if rows i,i+1 were swapped
     const double tiny = 1e-300 + 2.2e-16 * tnorm;
-    for (int i = 0; i < m; ++i) {
-        d[i] = a[i] - theta;
-        du[i] = i + 1 < m ? b[i] : 0.0;
-        du2[i] = 0.0;
-    }
-    // LU with partial pivoting of the tridiagonal (LAPACK dgttrf pattern)
+    // LU with partial pivoting of the tridiagonal (LAPACK dgttrf pattern); at
+    // step i only d[i] / du[i] may differ from T's (changed by step i-1)
+    double di = a[0] - theta, dui = m > 1 ? b[0] : 0.0;
     for (int i = 0; i + 1 < m; ++i) {
         const double sub = b[i];  // T(i+1, i)
-        if (fabs(d[i]) >= fabs(sub)) {
+        const double dn = a[i + 1] - theta;
+        const double dun = i + 2 < m ? b[i + 1] : 0.0;
+        if (fabs(di) >= fabs(sub)) {
+            const double f = di != 0.0 ? sub / di : 0.0;
             sw[i] = 0.0;
-            const double f = d[i] != 0.0 ? sub / d[i] : 0.0;
             l[i] = f;
-            d[i + 1] -= f * du[i];
+            d[i] = di;
+            du[i] = dui;
+            du2[i] = 0.0;
+            di = dn - f * dui;
+            dui = dun;
         } else {
+            const double f = di / sub;
             sw[i] = 1.0;
-            const double f = d[i] / sub;
             l[i] = f;
             d[i] = sub;
-            const double t = du[i];
-            du[i] = d[i + 1];
-            d[i + 1] = t - f * d[i + 1];
-            if (i + 2 < m) {
-                du2[i] = du[i + 1];
-                du[i + 1] = -f * du[i + 1];
-            }
+            du[i] = dn;
+            du2[i] = dun;
+            di = dui - f * dn;
+            dui = -f * dun;
         }
     }
-    for (int i = 0; i < m; ++i)
-        if (fabs(d[i]) < tiny) d[i] = d[i] < 0 ? -tiny : tiny;
+    d[m - 1] = di;
+    du[m - 1] = 0.0;
+    du2[m - 1] = 0.0;
+    // reciprocals of U's diagonal (independent of each other), then the three
+    // substitution passes multiply
+    for (int i = 0; i < m; ++i) {
+        double v = d[i];
+        if (fabs(v) < tiny) v = v < 0 ? -tiny : tiny;
+        d[i] = 1.0 / v;
+    }
     for (int i = 0; i < m; ++i) s[i] = 1.0;
     for (int it = 0; it < 3; ++it) {
         // forward: apply L^-1 P
+        double prev = s[0];
+#pragma unroll 4
         for (int i = 0; i + 1 < m; ++i) {
+            const double nxt = s[i + 1], li = l[i];
             if (sw[i] == 0.0) {
-                s[i + 1] -= l[i] * s[i];
+                s[i] = prev;
+                prev = nxt - li * prev;
             } else {
-                const double t = s[i];
-                s[i] = s[i + 1];
-                s[i + 1] = t - l[i] * s[i];
+                s[i] = nxt;
+                prev = prev - li * nxt;
             }
         }
-        // back: U^-1
-        s[m - 1] /= d[m - 1];
-        if (m > 1) s[m - 2] = (s[m - 2] - du[m - 2] * s[m - 1]) / d[m - 2];
-        for (int i = m - 3; i >= 0; --i)
-            s[i] = (s[i] - du[i] * s[i + 1] - du2[i] * s[i + 2]) / d[i];
-        double nrm = 0.0;
-        for (int i = 0; i < m; ++i) nrm += s[i] * s[i];
-        nrm = sqrt(nrm);
-        for (int i = 0; i < m; ++i) s[i] /= nrm;
+        s[m - 1] = prev;
+        // back: U^-1 (d holds 1 / U(i,i))
+        double n1 = s[m - 1] * d[m - 1], n0 = 0.0;
+        s[m - 1] = n1;
+        if (m > 1) {
+            n0 = (s[m - 2] - du[m - 2] * n1) * d[m - 2];
+            s[m - 2] = n0;
+        }
+#pragma unroll 4
+        for (int i = m - 3; i >= 0; --i) {
+            const double v = (s[i] - du[i] * n0 - du2[i] * n1) * d[i];
+            s[i] = v;
+            n1 = n0;
+            n0 = v;
+        }
+        double q0 = 0.0, q1 = 0.0;
+        int i = 0;
+        for (; i + 1 < m; i += 2) {
+            q0 = fma(s[i], s[i], q0);
+            q1 = fma(s[i + 1], s[i + 1], q1);
+        }
+        if (i < m) q0 = fma(s[i], s[i], q0);
+        const double inv = 1.0 / sqrt(q0 + q1);
+        for (int k = 0; k < m; ++k) s[k] *= inv;
     }
 }
 
@@ -196,10 +254,14 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
     // alpha/beta[m-1] were stored by thread 0 of this CTA: order them before the reads
     __threadfence_block();
     __syncthreads();
+    unsigned long long t_dbg0 = 0, t_dbg1 = 0, t_dbg2 = 0, t_dbg3 = 0;
+    if (a.debug_text && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_dbg0));
 
+    double* b2 = work;  // squared off-diagonal for the Sturm counts (work is free until the eigvecs)
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         ta[i] = a.alpha[i];
         tb[i] = i + 1 < m ? a.beta[i] : 0.0;
+        b2[i] = tb[i] * tb[i];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -218,27 +280,33 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
         theta[0] = tn;  // temp: T norm
     }
     __syncthreads();
+    unsigned long long t_dbgA = 0;
+    int rounds_dbg = 0;
+    if (a.debug_text && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_dbgA));
     const double tnorm = theta[0];
-    const double pivmin = 1e-300 + 1e-30 * tnorm * tnorm;
+    // 0: lowest, 1: highest; NP points per side and round (more points per
+    // round only add FP64-pipe pressure: 128 -> 8 rounds to full precision)
     const int half = blockDim.x / 2;
-    const int side = threadIdx.x < half ? 0 : 1;  // 0: lowest, 1: highest
+    const int side = threadIdx.x < half ? 0 : 1;
     const int k = threadIdx.x - side * half;
+    const int NP = min(half, 128);
     __shared__ int found[2];
     auto narrow = [&](int sd) {
         const double lo = lohi[2 * sd], hi = lohi[2 * sd + 1];
         return !(hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300);
     };
-    for (int round = 0; round < 10; ++round) {
+    for (int round = 0; round < 12; ++round) {
         // every thread takes every barrier: the two halves may finish in
         // different rounds, so a finished half idles instead of leaving
         if (!narrow(0) && !narrow(1)) break;  // uniform: read after a barrier
-        const bool active = narrow(side);
+        ++rounds_dbg;
+        const bool active = narrow(side) && k < NP;
         const double lo = lohi[2 * side], hi = lohi[2 * side + 1];
         if (active) {
-            const double x = lo + (hi - lo) * static_cast<double>(k + 1) / static_cast<double>(half + 1);
-            cnt[threadIdx.x] = sturm_count(ta, tb, m, x, pivmin);
+            const double x = lo + (hi - lo) * static_cast<double>(k + 1) / static_cast<double>(NP + 1);
+            cnt[threadIdx.x] = sturm_count(ta, b2, m, x);
         }
-        if (k == 0) found[side] = half;
+        if (k == 0) found[side] = NP;
         __syncthreads();
         // lowest: first point with count >= 1; highest: first with count >= m
         const int target = side == 0 ? 1 : m;
@@ -248,22 +316,23 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
             if (hit && !prev) found[side] = k;  // counts are monotone: one writer
         }
         __syncthreads();
-        if (k == 0 && active) {
+        if (k == 0 && narrow(side)) {
             const int f = found[side];
-            const double nlo = f == 0 ? lo : lo + (hi - lo) * static_cast<double>(f) / (half + 1);
-            const double nhi =
-                f == half ? hi : lo + (hi - lo) * static_cast<double>(f + 1) / (half + 1);
+            const double nlo = f == 0 ? lo : lo + (hi - lo) * static_cast<double>(f) / (NP + 1);
+            const double nhi = f == NP ? hi : lo + (hi - lo) * static_cast<double>(f + 1) / (NP + 1);
             lohi[2 * side] = nlo;
             lohi[2 * side + 1] = nhi;
         }
         __syncthreads();
     }
+    if (a.debug_text && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_dbg1));
     if (threadIdx.x == 0 || threadIdx.x == half) {
         const double th = 0.5 * (lohi[2 * side] + lohi[2 * side + 1]);
         theta[side] = th;
         tri_eigvec(ta, tb, m, th, tnorm, sv[side], side == 0 ? work : work2);
     }
     __syncthreads();
+    if (a.debug_text && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_dbg2));
     if (threadIdx.x == 0) {
         const double res_lo = fabs(beta_last * sv[0][m - 1]);
         const double res_hi = fabs(beta_last * sv[1][m - 1]);
@@ -290,6 +359,12 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         a.sT[i] = sv[0][i];
         a.sT[kMaxKrylov + i] = sv[1][i];
+    }
+    if (a.debug_text && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_dbg3));
+        printf("[t_extremes] m=%d load+gersh %.1f us multisection %.1f us (%d rounds) eigvec %.1f us tail %.1f us\n",
+               m, (t_dbgA - t_dbg0) * 1e-3, (t_dbg1 - t_dbgA) * 1e-3, rounds_dbg, (t_dbg2 - t_dbg1) * 1e-3,
+               (t_dbg3 - t_dbg2) * 1e-3);
     }
 }
 
@@ -670,6 +745,14 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     __shared__ double red[32];
     __shared__ double nrmp[16];
     __shared__ double fin[5][16];
+    // diagnostics (R1_DEBUG_EIG): per-phase ns of CTA 0 thread 0 -> stats[8..15]
+    unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tlast = gtimer();
+    auto mark = [&](int ph) {
+        const unsigned long long t = gtimer();
+        tacc[ph] += t - tlast;
+        tlast = t;
+    };
 
     // ---- own rows of J (row t = column t: symmetric)
     for (int e = tid; e < Rm * n; e += kEigThreads) {
@@ -736,6 +819,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     }
     __syncthreads();
     double inv_beta = 1.0 / publish();
+    mark(0);
 
     int restarts = 0, breakdowns = 0;
     int j = 0;
@@ -761,11 +845,15 @@ __global__ void __launch_bounds__(kEigThreads, 1)
             if (lane == 0) ws[r] = s * inv_beta * op.scale;
         }
         __syncthreads();
+        mark(1);
         cgs_pass(hp1, j);
         const double h1j = hsh[j];
+        mark(2);
         cgs_pass(hp2, j);
         const double alpha = h1j + hsh[j];
+        mark(3);
         double nrm = publish();
+        mark(4);
         anorm = fmax(anorm, fabs(alpha) + nrm + (j > 0 ? a.beta[j - 1] : 0.0));
         if (j == 0 && restarts == 0 && anorm == 0.0) {
             zero_op = true;  // J v0 == 0 for a dense random v0: J == 0 (see lanczos_kernel)
@@ -792,6 +880,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         if (((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit) {
             if (me == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts, text, ld);
             cl.sync();
+            mark(5);
             if (*reinterpret_cast<volatile int*>(a.ctl)) break;
             if (size_limit) {
                 if (restarts >= a.max_restarts) break;  // best effort: ctl[0] stays 0
@@ -908,7 +997,8 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         if (a.other_out && nrm_o > 0.0) a.other_out[r0 + r] = xo_s[r] / nrm_o;
     }
     if (me == 0 && tid == 0) {
-        for (int k = 0; k < 8; ++k) a.stats[8 + k] = 0.0;
+        mark(6);
+        for (int k = 0; k < 8; ++k) a.stats[8 + k] = static_cast<double>(tacc[k]);
         *a.out_value = a.stats[4];
         if (a.hint) *a.hint = restarts == 0 ? m : 0;
         a.ctl[2] = m;
@@ -1015,6 +1105,8 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.op = P.dop.get(op, ctx->stream);
     a.out_value = value_dev;
     a.out_vec = vec_dev;
+    static const bool dbg_text = std::getenv("R1_DEBUG_EIG_TEXT") != nullptr;
+    a.debug_text = dbg_text ? 1 : 0;
     if (solver_chain) {
         if (!P.hint.ptr) {
             P.hint.ensure(sizeof(int));
