@@ -456,12 +456,15 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         return r0 + ((tid - r0) & (kBkThreads - 1));
     };
     auto raw = [&](int pair, int slot) { return Raw + (2 * pair + slot) * rcap; };
+    // diagnostics (R1_BK_TRACE): per-phase cycles of CTA 0 thread 0, kept in
+    // registers (constant indices after inlining) and written once at the end
     const bool tr = a.trace && me == 0 && tid == 0;
     long long tprev = 0;
+    unsigned long long tacc[16] = {};
     auto mark = [&](int ph) {
         if (!tr) return;
         const long long t = clock64();
-        if (ph >= 0) a.trace[ph] += static_cast<unsigned long long>(t - tprev);
+        if (ph >= 0) tacc[ph] += static_cast<unsigned long long>(t - tprev);
         tprev = t;
     };
     if (tid < 2) pend_row[tid] = -1;
@@ -655,7 +658,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
             cik = rmaxm[rstep & 1][owner(k)][2];
             cik1 = k + 1 < n ? rmaxm[rstep & 1][owner(k + 1)][3] : 0.0;
             ++rstep;
-            if (tr) a.trace[8] += 1;
+            if (tr) tacc[8] += 1;
             if (absakk * rowmax >= kBkAlpha * colmax * colmax) {
                 kp = k;
             } else if (fabs(cimax) >= kBkAlpha * rowmax) {
@@ -672,16 +675,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         const bool more = kn < n && jn < kBkNb;
         const double* rkk = raw(cp, kks);
         const double* w_kk = nx + kks * kBkW;  // W row kk (NEXT of the previous step)
-        // prefetch the raw columns kn, kn+1 (patched at the top of the next step)
-        if (more) {
-            for (int s = 0; s < 2; ++s) {
-                const int c = kn + s;
-                if (c >= n) break;
-                const double* src = col(c);
-                for (int r = first_row(c); r < R; r += kBkThreads) cp_async8(raw(cp ^ 1, s) + r, src + lo + r);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
+        mark(10);
         // ---- pivot coefficients (every CTA), new W column(s), pending W rows
         double d = 0.0, r1 = 0.0, d11 = 0.0, d22 = 0.0, d21t = 0.0;
         bool zero = false;
@@ -697,6 +691,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
             const double tt = 1.0 / (d11 * d22 - 1.0);
             d21t = tt / d21;
         }
+        mark(12);
         auto new_w = [&](int r, int i, double& x0, double& x1) {
             if (kstep == 1) {
                 const double v = kp == k ? Cs[r] : (i == k ? cimax : (i == kp ? cik : Cis[r]));
@@ -741,7 +736,9 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 coef[jp + 1] = StepCoef{3, d21t, d11, d22};
             }
         }
+        mark(13);
         __syncthreads();
+        mark(14);
         uint32_t next_bytes = 0;
         if (more) {
             // NEXT: final W rows of kn, kn+1 -> every CTA (kp's row is the pending
@@ -767,6 +764,18 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
             }
         }
         mark(6);
+        // prefetch the raw columns kn, kn+1 (patched at the top of the next
+        // step), issued after NEXT so they stream during the stores
+        if (more) {
+            for (int s = 0; s < 2; ++s) {
+                const int c = kn + s;
+                if (c >= n) break;
+                const double* src = col(c);
+                for (int r = first_row(c); r < R; r += kBkThreads) cp_async8(raw(cp ^ 1, s) + r, src + lo + r);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        mark(11);
         // ---- global stores (stream out behind NEXT): L / D of the new
         // column(s), interchange moves, interchanged rows of earlier L columns
         if (swap) {
@@ -823,7 +832,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         cp ^= 1;
         ++step;
         mark(7);
-        if (tr) a.trace[9] += 1;
+        if (tr) tacc[9] += 1;
     }
     __syncthreads();
     for (int p = 0; p < 2; ++p)
@@ -833,6 +842,8 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
     // the panel's W rows of this CTA -> global, for the trailing update
     for (int t = 0; t < jp; ++t)
         for (int r = tid; r < R; r += kBkThreads) a.Wp[(lo + r) + static_cast<size_t>(t) * n] = Ws[r * kBkW + t];
+    if (tr)
+        for (int q = 0; q < 16; ++q) a.trace[q] += tacc[q];
     if (gtid == 0) {
         a.perm[a.ctl[4]] = k0;  // panel starts, for the solve
         a.ctl[4] += 1;
@@ -1477,9 +1488,11 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         const double c = h[9] ? static_cast<double>(h[9]) : 1.0;
         std::fprintf(stderr,
                      "[r1 bk] n=%lld cols=%llu imax-path=%llu cycles/col: wait_next %.0f top %.0f step1 %.0f "
-                     "wait_cand %.0f imax %.0f wait_rmax %.0f elim %.0f stores %.0f\n",
+                     "wait_cand %.0f imax %.0f wait_rmax %.0f elim %.0f (decide %.0f prefetch %.0f coef %.0f "
+                     "neww %.0f bar %.0f sends %.0f) stores %.0f\n",
                      static_cast<long long>(n), h[9], h[8], h[0] / c, h[1] / c, h[2] / c, h[3] / c,
-                     h[4] / c, h[5] / c, h[6] / c, h[7] / c);
+                     h[4] / c, h[5] / c, (h[10] + h[11] + h[12] + h[13] + h[14] + h[6]) / c, h[10] / c,
+                     h[11] / c, h[12] / c, h[13] / c, h[14] / c, h[6] / c, h[7] / c);
     }
 }
 
