@@ -935,6 +935,108 @@ __global__ void __launch_bounds__(kBkThreads, 1) bk_update2_kernel(const BkArgs 
     }
 }
 
+// A22 -= W L^T on the FP64 tensor cores (mma.sync m8n8k4 f64): 128 x 64
+// tiles of the trailing lower triangle (each 128 x 128 block of the triangle
+// as two column halves), 8 warps of 32 x 32, two CTAs per SM so one CTA's
+// memory phases overlap the other's.  The A tile goes straight into the
+// accumulator fragments (negated: acc = W L^T - A, stored back negated, which
+// is exact), so only the W / L panels are staged in shared memory (cp.async,
+// row stride kBkUpdLd: conflict-free fragment loads).  One mma replaces 8 DFMA
+// issue slots per lane; the DFMA kernel ran its FP64 pipe at ~31%.
+constexpr int kBkUpdLd = kBkT2 + 8;                  // 136: t-rows 16 banks apart
+constexpr int kBkUpdK = (kBkW + 3) / 4 * 4;          // 36: panel width rounded to k = 4
+constexpr int kBkUpdCols = 64;                       // tile columns
+constexpr size_t kBkUpdTcSmem =
+    static_cast<size_t>(kBkUpdK) * (kBkUpdLd + kBkUpdCols + 8) * sizeof(double);
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kBkThreads, 2) bk_update_tc_kernel(const BkArgs a) {
+    constexpr int kLdL = kBkUpdCols + 8;  // 72
+    extern __shared__ __align__(16) double usm[];
+    double* Ws = usm;                      // [kBkUpdK][kBkUpdLd]  W(i0 + r, t)
+    double* Ls = usm + kBkUpdK * kBkUpdLd;  // [kBkUpdK][kLdL]      L(j0 + c, t)
+    const int64_t n = a.n;
+    const int64_t k0 = a.ctl[2];
+    const int jp = a.ctl[3];
+    const int64_t kend = k0 + jp;
+    const int64_t m = n - kend;
+    if (m <= 0 || jp == 0) return;
+    const int kp4 = (jp + 3) / 4;
+    const int64_t T = (m + kBkT2 - 1) / kBkT2;
+    const int64_t ntiles = T * (T + 1);  // two column halves per 128 x 128 block
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp tile origin in the CTA tile
+    const int fr = lane >> 2, fc = (lane & 3) * 2;            // accumulator fragment row / col pair
+    for (int64_t xx = blockIdx.x; xx < ntiles; xx += gridDim.x) {
+        const int64_t x = xx >> 1;
+        int64_t bi = static_cast<int64_t>((sqrt(8.0 * static_cast<double>(x) + 1.0) - 1.0) * 0.5);
+        while (bi * (bi + 1) / 2 > x) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= x) ++bi;
+        const int64_t bj = x - bi * (bi + 1) / 2;
+        const int64_t i0 = kend + bi * kBkT2, j0 = kend + bj * kBkT2 + (xx & 1) * kBkUpdCols;
+        if (j0 >= n) continue;
+        const int rows = static_cast<int>(n - i0 < kBkT2 ? n - i0 : kBkT2);
+        const int cols = static_cast<int>(n - j0 < kBkUpdCols ? n - j0 : kBkUpdCols);
+        __syncthreads();  // the previous tile's fragment loads are done
+        // W / L panels -> shared (zero outside the tile and for t >= jp)
+        for (int e = threadIdx.x; e < kBkT2 * kp4 * 4; e += blockDim.x) {
+            const int r = e % kBkT2, t = e / kBkT2;
+            double* wd = &Ws[t * kBkUpdLd + r];
+            if (t < jp && r < rows) cp_async8(wd, a.Wp + (i0 + r) + t * n);
+            else *wd = 0.0;
+        }
+        for (int e = threadIdx.x; e < kBkUpdCols * kp4 * 4; e += blockDim.x) {
+            const int r = e % kBkUpdCols, t = e / kBkUpdCols;
+            double* ld = &Ls[t * kLdL + r];
+            if (t < jp && r < cols) cp_async8(ld, a.A + (j0 + r) + (k0 + t) * n);
+            else *ld = 0.0;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // accumulators <- -A (the loads overlap the panel copies)
+        double acc[4][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int rr = wm + mi * 8 + fr, cc = wn + ni * 8 + fc + q;
+                    acc[mi][ni][q] = rr < rows && cc < cols ? -a.A[(i0 + rr) + (j0 + cc) * n] : 0.0;
+                }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        for (int k4 = 0; k4 < kp4; ++k4) {
+            const int t = k4 * 4 + (lane & 3);
+            double fa[4], fb[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) fa[mi] = Ws[t * kBkUpdLd + wm + mi * 8 + fr];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) fb[ni] = Ls[t * kLdL + wn + ni * 8 + fr];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], fa[mi], fb[ni]);
+        }
+        // A <- -(W L^T - A), lower triangle only where the tile meets the diagonal
+        const bool diag = j0 + kBkUpdCols > i0;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int rr = wm + mi * 8 + fr, cc = wn + ni * 8 + fc + q;
+                    const int64_t i = i0 + rr, j = j0 + cc;
+                    if (rr < rows && cc < cols && (!diag || i >= j)) a.A[i + j * n] = -acc[mi][ni][q];
+                }
+    }
+}
+
 // The reference's D-block condition
 // (ldlt_diag_condition, sym_eig.cpp:381-407); one CTA.
 __global__ void bk_condition_kernel(const double* __restrict__ A, int64_t n,
@@ -1465,9 +1567,14 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         R1_CUDA(cudaFuncSetAttribute(bk_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kBkUpdSmem)));
+        R1_CUDA(cudaFuncSetAttribute(bk_update_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kBkUpdTcSmem)));
         configured = ctx->device;
     }
     if (smem_panel) cfg.dynamicSmemBytes = psmem;
+    // trailing update on the FP64 tensor cores (R1_BK_UPDATE_DFMA=1: the DFMA kernel)
+    static const char* ud = std::getenv("R1_BK_UPDATE_DFMA");
+    const bool upd_tc = !(ud && std::atoi(ud));
     // each panel factors >= kBkNb columns (or the rest); extra launches exit at once
     const int64_t panels = (n + kBkNb - 1) / kBkNb;
     for (int64_t p = 0; p < panels; ++p) {
@@ -1476,7 +1583,10 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         else
             R1_CUDA(cudaLaunchKernelEx(&cfg, bk_panel_kernel, a));
         check_launch(ctx, "bk_panel_kernel");
-        bk_update2_kernel<<<ctx->num_sms, kBkThreads, kBkUpdSmem, ctx->stream>>>(a);
+        if (upd_tc)
+            bk_update_tc_kernel<<<2 * ctx->num_sms, kBkThreads, kBkUpdTcSmem, ctx->stream>>>(a);
+        else
+            bk_update2_kernel<<<ctx->num_sms, kBkThreads, kBkUpdSmem, ctx->stream>>>(a);
         check_launch(ctx, "bk_update2_kernel");
     }
     bk_condition_kernel<<<1, 1024, 0, ctx->stream>>>(A, n, L.ctl, L.ps, cond_dev);
