@@ -408,16 +408,19 @@ __device__ __forceinline__ void wait_parity(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-__global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs a, int rcap) {
-    static_assert((kBkThreads & (kBkThreads - 1)) == 0, "row mapping uses a mask");
+// NT threads per CTA; TRACE compiles the phase timers in (their register
+// array doubles the register count).
+template <int NT, bool TRACE>
+__global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int rcap) {
+    static_assert((NT & (NT - 1)) == 0, "row mapping uses a mask");
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double dsm[];
     double* Ws = dsm;                 // [rcap][kBkW] this CTA's rows of W
     double* Cs = Ws + rcap * kBkW;    // [rcap] updated column k
     double* Cis = Cs + rcap;          // [rcap] updated column imax
     double* Raw = Cis + rcap;         // [2 pairs][2][rcap] raw stored columns (k, k+1)
-    __shared__ double sv[8], ss[8];
-    __shared__ int si[8];
+    __shared__ double sv[NT / 32], ss[NT / 32];
+    __shared__ int si[NT / 32];
     __shared__ double Lr[kBkW], Wim[kBkW];  // L row being applied; W row of imax
     __shared__ double pend[2][kBkW];
     __shared__ int pend_row[2], pend_n[2];
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
     const int chunk = (n - k0 + G - 1) / G;
     const int lo = k0 + chunk * me, hi = min(n, lo + chunk);
     const int R = hi > lo ? hi - lo : 0;
-    const int gtid = me * kBkThreads + tid;
+    const int gtid = me * NT + tid;
     double* A = a.A;
     auto col = [&](int c) { return A + static_cast<size_t>(c) * static_cast<size_t>(n); };
     // owner CTA of row i: (i - k0) / chunk by a float reciprocal and a +-1 fixup
@@ -449,16 +452,16 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         else if ((q + 1) * chunk <= x) ++q;
         return q;
     };
-    // local row r is always handled by thread r % kBkThreads (the thread that
+    // local row r is always handled by thread r % NT (the thread that
     // prefetched / patched a raw entry is the one that reads it)
     auto first_row = [&](int grow) {
         const int r0 = grow > lo ? min(grow - lo, R) : 0;
-        return r0 + ((tid - r0) & (kBkThreads - 1));
+        return r0 + ((tid - r0) & (NT - 1));
     };
     auto raw = [&](int pair, int slot) { return Raw + (2 * pair + slot) * rcap; };
     // diagnostics (R1_BK_TRACE): per-phase cycles of CTA 0 thread 0, kept in
     // registers (constant indices after inlining) and written once at the end
-    const bool tr = a.trace && me == 0 && tid == 0;
+    const bool tr = TRACE && a.trace && me == 0 && tid == 0;
     long long tprev = 0;
     unsigned long long tacc[16] = {};
     auto mark = [&](int ph) {
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         const int c = k0 + s;
         if (c >= n) break;
         const double* src = col(c);
-        for (int r = first_row(c); r < R; r += kBkThreads) cp_async8(raw(0, s) + r, src + lo + r);
+        for (int r = first_row(c); r < R; r += NT) cp_async8(raw(0, s) + r, src + lo + r);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     __syncthreads();
@@ -506,15 +509,15 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 double* dst = raw(cp, s);
                 if (c == p_kp) {  // column kp <- raw column kk below kp
                     const double* src = raw(cp ^ 1, p_kks);
-                    for (int r = first_row(p_kp + 1); r < R; r += kBkThreads) dst[r] = src[r];
+                    for (int r = first_row(p_kp + 1); r < R; r += NT) dst[r] = src[r];
                 }
-                if (p_kp >= lo && p_kp < hi && ((p_kp - lo) & (kBkThreads - 1)) == tid)
+                if (p_kp >= lo && p_kp < hi && ((p_kp - lo) & (NT - 1)) == tid)
                     dst[p_kp - lo] = nx[2 * kBkW + s];
             }
         }
         for (int p = 0; p < 2; ++p)
             if (pend_row[p] >= 0)
-                for (int t = tid; t < pend_n[p]; t += kBkThreads) Ws[pend_row[p] * kBkW + t] = pend[p][t];
+                for (int t = tid; t < pend_n[p]; t += NT) Ws[pend_row[p] * kBkW + t] = pend[p][t];
         if (tid < jp) Lr[tid] = l_entry(nx, coef, tid);
         __syncthreads();
         if (tid < 2) pend_row[tid] = -1;
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         int bi = n;
         {
             const double* rk = raw(cp, 0);
-            for (int r = first_row(k); r < R; r += kBkThreads) {
+            for (int r = first_row(k); r < R; r += NT) {
                 const int i = lo + r;
                 const double* w = Ws + r * kBkW;
                 double s0 = rk[r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
             if (f < 2) {
                 double cv = -1.0, cs = 0.0;
                 int ci = n;
-                for (int w = 0; w < kBkThreads / 32; ++w) amax_merge(cv, ci, cs, sv[w], si[w], ss[w]);
+                for (int w = 0; w < NT / 32; ++w) amax_merge(cv, ci, cs, sv[w], si[w], ss[w]);
                 v = f == 0 ? static_cast<double>(ci) : cs;
             } else {
                 v = own[f - 2];
@@ -611,7 +614,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
             __syncthreads();
             double rv = -1.0;
             const double* ci = col(imax);
-            for (int r = first_row(k); r < R; r += kBkThreads) {
+            for (int r = first_row(k); r < R; r += NT) {
                 const int i = lo + r;
                 const double* w = Ws + r * kBkW;
                 double s0 = i >= imax ? ci[i] : col(i)[imax], s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 double v;
                 if (f == 0) {
                     v = -1.0;
-                    for (int w = 0; w < kBkThreads / 32; ++w) v = fmax(v, sv[w]);
+                    for (int w = 0; w < NT / 32; ++w) v = fmax(v, sv[w]);
                 } else {
                     v = own[f + 1];
                 }
@@ -716,7 +719,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 }
             }
         }
-        for (int r = first_row(k); r < R; r += kBkThreads) {
+        for (int r = first_row(k); r < R; r += NT) {
             const int i = lo + r;
             double x0, x1;
             new_w(r, i, x0, x1);
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 next_bytes += 8u * jn;
                 if (q >= lo && q < hi) {
                     const double* src = swap && q == kp ? pend[1] : Ws + (q - lo) * kBkW;
-                    for (int e = tid; e < G * jn; e += kBkThreads) {
+                    for (int e = tid; e < G * jn; e += NT) {
                         const int dst = e / jn, t = e - dst * jn;
                         send8(&nextm[b][s * kBkW + t], src[t], &bars[4 + b], dst);
                     }
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 if (swap && q <= kp) {
                     if (okp == me) next_bytes += 8u;
                     const int srow = q < kp ? q : kk;  // the raw entry's row in column kk
-                    if (srow >= lo && srow < hi && ((srow - lo) & (kBkThreads - 1)) == tid)
+                    if (srow >= lo && srow < hi && ((srow - lo) & (NT - 1)) == tid)
                         send8(&nextm[b][2 * kBkW + s], rkk[srow - lo], &bars[4 + b], okp);
                 }
             }
@@ -771,7 +774,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
                 const int c = kn + s;
                 if (c >= n) break;
                 const double* src = col(c);
-                for (int r = first_row(c); r < R; r += kBkThreads) cp_async8(raw(cp ^ 1, s) + r, src + lo + r);
+                for (int r = first_row(c); r < R; r += NT) cp_async8(raw(cp ^ 1, s) + r, src + lo + r);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
@@ -779,7 +782,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         // ---- global stores (stream out behind NEXT): L / D of the new
         // column(s), interchange moves, interchanged rows of earlier L columns
         if (swap) {
-            for (int e = gtid; e < 2 * jp; e += G * kBkThreads) {
+            for (int e = gtid; e < 2 * jp; e += G * NT) {
                 const int t = e >> 1;
                 if (e & 1) col(k0 + t)[kp] = l_entry(w_kk, coef, t);
                 else col(k0 + t)[kk] = l_entry(Wim, coef, t);
@@ -788,7 +791,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
         double* ck = col(k);
         double* ck1 = col(k + 1 < n ? k + 1 : k);
         double* ckp = col(kp);
-        for (int r = first_row(k); r < R; r += kBkThreads) {
+        for (int r = first_row(k); r < R; r += NT) {
             const int i = lo + r;
             double x0, x1;
             new_w(r, i, x0, x1);
@@ -837,11 +840,11 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_smem_kernel(const BkArgs 
     __syncthreads();
     for (int p = 0; p < 2; ++p)
         if (pend_row[p] >= 0)
-            for (int t = tid; t < pend_n[p]; t += kBkThreads) Ws[pend_row[p] * kBkW + t] = pend[p][t];
+            for (int t = tid; t < pend_n[p]; t += NT) Ws[pend_row[p] * kBkW + t] = pend[p][t];
     __syncthreads();
     // the panel's W rows of this CTA -> global, for the trailing update
     for (int t = 0; t < jp; ++t)
-        for (int r = tid; r < R; r += kBkThreads) a.Wp[(lo + r) + static_cast<size_t>(t) * n] = Ws[r * kBkW + t];
+        for (int r = tid; r < R; r += NT) a.Wp[(lo + r) + static_cast<size_t>(t) * n] = Ws[r * kBkW + t];
     if (tr)
         for (int q = 0; q < 16; ++q) a.trace[q] += tacc[q];
     if (gtid == 0) {
@@ -1561,17 +1564,22 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     const bool smem_panel = psmem <= kBkPanelSmemMax && gp <= 16;
     static int configured = -1;
     if (configured != ctx->device) {
-        R1_CUDA(cudaFuncSetAttribute(bk_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kBkPanelSmemMax)));
-        R1_CUDA(cudaFuncSetAttribute(bk_panel_smem_kernel,
-                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        for (auto fn : {bk_panel_smem_kernel<kBkThreads, false>, bk_panel_smem_kernel<kBkThreads, true>}) {
+            R1_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kBkPanelSmemMax)));
+            R1_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
         R1_CUDA(cudaFuncSetAttribute(bk_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kBkUpdSmem)));
         R1_CUDA(cudaFuncSetAttribute(bk_update_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kBkUpdTcSmem)));
         configured = ctx->device;
     }
-    if (smem_panel) cfg.dynamicSmemBytes = psmem;
+    // 256 threads even when a CTA owns 2 rows per thread (n = 6500): 512 was
+    // measured 2% slower there (16-warp reductions and barriers)
+    auto panel_fn = trace ? bk_panel_smem_kernel<kBkThreads, true> : bk_panel_smem_kernel<kBkThreads, false>;
+    cudaLaunchConfig_t pcfg = cfg;
+    pcfg.dynamicSmemBytes = psmem;
     // trailing update on the FP64 tensor cores (R1_BK_UPDATE_DFMA=1: the DFMA kernel)
     static const char* ud = std::getenv("R1_BK_UPDATE_DFMA");
     const bool upd_tc = !(ud && std::atoi(ud));
@@ -1579,7 +1587,7 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     const int64_t panels = (n + kBkNb - 1) / kBkNb;
     for (int64_t p = 0; p < panels; ++p) {
         if (smem_panel)
-            R1_CUDA(cudaLaunchKernelEx(&cfg, bk_panel_smem_kernel, a, rcap));
+            R1_CUDA(cudaLaunchKernelEx(&pcfg, panel_fn, a, rcap));
         else
             R1_CUDA(cudaLaunchKernelEx(&cfg, bk_panel_kernel, a));
         check_launch(ctx, "bk_panel_kernel");
