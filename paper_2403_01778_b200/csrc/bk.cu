@@ -1508,6 +1508,8 @@ int panel_cluster_size(r1_context* ctx, int64_t n) {
         }
     }
     (void)ctx;
+    static const char* genv = std::getenv("R1_BK_G");  // development: force the cluster size
+    if (genv) return std::max(1, std::min(max16, std::atoi(genv)));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max16, (n + 255) / 256)));
 }
 

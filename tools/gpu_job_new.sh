@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests/test_bk_gpu.py tests/test_solver_gpu.py -q -x 2>&1 | tail -2
-R1_BK_TRACE=1 timeout 300 python tools/bk_probe.py 3000 2>&1 | grep "r1 bk" | tail -1
+for g in 16 12 8 6; do R1_BK_G=$g timeout 300 python tools/solve_probe.py C2 C5 --alg ihoscf 2>&1 | grep rep1 | sed "s/^/G=$g /" | cut -c1-60; done
