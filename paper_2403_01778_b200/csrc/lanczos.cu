@@ -1113,7 +1113,8 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
             R1_CUDA(cudaMemsetAsync(P.hint.ptr, 0, sizeof(int), ctx->stream));
         }
         a.hint = P.hint.as<int>();
-        a.warm = x0 != nullptr ? 1 : 0;
+        static const char* he = std::getenv("R1_EIG_HINT");  // development: 0 disables the hint
+        a.warm = x0 != nullptr && !(he && std::atoi(he) == 0) ? 1 : 0;
         P.other.ensure(static_cast<size_t>(n) * sizeof(double));
         a.x1 = x0 != nullptr && P.other_valid ? P.other.as<double>() : nullptr;
         a.other_out = P.other.as<double>();

@@ -1,1 +1,4 @@
-for g in 16 12 8 6; do R1_BK_G=$g timeout 300 python tools/solve_probe.py C2 C5 --alg ihoscf 2>&1 | grep rep1 | sed "s/^/G=$g /" | cut -c1-60; done
+timeout 60 python tools/c1_probe.py C1 2>&1 | tail -1
+R1_DEBUG_EIG=1 timeout 60 python tools/c1_probe.py C1 2>&1 | grep "r1 eig" > gpurun_out/c1_eig_dbg.txt
+timeout 120 python tools/solve_probe.py C3 --alg hoscf --reps 2 2>&1 | grep rep1 | cut -c1-150
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
