@@ -1289,7 +1289,7 @@ __global__ void bk_perm_kernel(const int* __restrict__ ipiv, const char* __restr
 // orders everything.  Fixed partitions and summation orders: deterministic.
 __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const SolveArgs s, const int* pperm) {
     cg::cluster_group cl = cg::this_cluster();
-    extern __shared__ double zs[];                    // own rows of z
+    extern __shared__ __align__(16) double zs[];      // own rows of z, then Lr
     __shared__ double Lb[2][kBkW][kBkW + 1];          // panel diagonal block (see below)
     __shared__ double gsl[2][2 * kBkW];               // pushed slot values, by panel parity
     __shared__ double part[2][16][kBkW];              // pushed backward partials, by parity
@@ -1303,6 +1303,9 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
     const int np = s.ctl[4];
     const double* A = s.A;
     auto colp = [&](int c) { return A + static_cast<size_t>(c) * static_cast<size_t>(n); };
+    // Lr[t * chunk + r] = L(lo + r, c0 + t): this CTA's rows of a panel's L21,
+    // staged with cp.async one panel ahead (the update / partials read it)
+    double* Lr = zs + ((chunk + 1) & ~1);
     auto rec = [&](int p) { return pperm + static_cast<size_t>(p) * kPermStride; };
     auto pbounds = [&](int p, int& c0, int& c1) {
         c0 = s.pstart[p];
@@ -1336,9 +1339,22 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
             Lb[par][t][i] = z ? 0.0 : colp(c0 + t)[c0 + i];
         }
     };
+    auto prefetch_rows = [&](int p) {
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int w = c1 - c0;
+        const int r0 = c1 > lo ? min(c1 - lo, R) : 0;
+        const int nr = R - r0;
+        for (int e = tid; e < w * nr; e += kBkThreads) {
+            const int t = e / nr, r = r0 + (e - t * nr);
+            cp_async8(&Lr[t * chunk + r], colp(c0 + t) + lo + r);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     for (int r = tid; r < R; r += kBkThreads) zs[r] = s.x[lo + r];
     __syncthreads();
     if (np > 0) {
+        prefetch_rows(0);
         push_slots(0, 0);
         load_fwd_block(0, 0);
     }
@@ -1368,17 +1384,18 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
             const int row = slot_row(P, c0, w, tid);
             if (row >= lo && row < hi) zs[row - lo] = zp[tid];
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         {
             const int r0 = c1 > lo ? min(c1 - lo, R) : 0;
             for (int r = r0 + tid; r < R; r += kBkThreads) {
-                const int i = lo + r;
                 double acc = 0.0;
-                for (int t = 0; t < w; ++t) acc += colp(c0 + t)[i] * zp[t];
+                for (int t = 0; t < w; ++t) acc += Lr[t * chunk + r] * zp[t];
                 zs[r] -= acc;
             }
         }
         __syncthreads();
+        if (p + 1 < np) prefetch_rows(p + 1);
         if (p + 1 < np) push_slots(p + 1, par ^ 1);
         cl.sync();
     }
@@ -1408,16 +1425,21 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         const int w = c1 - c0;
         const int r0 = c1 > lo ? min(c1 - lo, R) : 0;
         for (int t = warp; t < w; t += kBkThreads / 32) {
-            const double* ct = colp(c0 + t);
+            const double* ct = Lr + t * chunk;
             double acc = 0.0;
-            for (int r = r0 + lane; r < R; r += 32) acc += ct[lo + r] * zs[r];
+            for (int r = r0 + lane; r < R; r += 32) acc += ct[r] * zs[r];
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
             if (lane < G) *cl.map_shared_rank(&part[par][me][t], lane) = acc;
         }
         push_slots(p, par);
     };
-    if (np > 0) push_back(np - 1, (np - 1) & 1);
+    if (np > 0) {
+        prefetch_rows(np - 1);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        push_back(np - 1, (np - 1) & 1);
+    }
     cl.sync();
     for (int p = np - 1; p >= 0; --p) {
         const int par = p & 1;
@@ -1425,6 +1447,8 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         pbounds(p, c0, c1);
         const int* P = rec(p);
         const int w = c1 - c0, m = w + P[0];
+        __syncthreads();  // push_back(p) finished reading Lr
+        if (p > 0) prefetch_rows(p - 1);
         // backward block: Lb[par][i][t] = L(c0+i, c0+t), i > t (row i contiguous)
         for (int e = tid; e < w * w; e += kBkThreads) {
             const int i = e / w, t = e - i * w;
@@ -1452,6 +1476,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
             const int row = slot_row(P, c0, w, tid);
             if (row >= lo && row < hi) zs[row - lo] = zp[P[4 + 3 * kBkW + tid]];
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (p > 0) push_back(p - 1, par ^ 1);
         cl.sync();
@@ -1634,13 +1659,14 @@ void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const doubl
             R1_CUDA(cudaFuncSetAttribute(bk_solve_cluster_kernel,
                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             R1_CUDA(cudaFuncSetAttribute(bk_solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         160 * 1024));
+                                         190 * 1024));
             configured = ctx->device;
         }
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(gp);
         cfg.blockDim = dim3(kBkThreads);
-        cfg.dynamicSmemBytes = static_cast<size_t>((n + gp - 1) / gp) * sizeof(double);
+        const int64_t chunk = (n + gp - 1) / gp;
+        cfg.dynamicSmemBytes = static_cast<size_t>(((chunk + 1) & ~int64_t(1)) + kBkW * chunk) * sizeof(double);
         cfg.stream = ctx->stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1649,7 +1675,7 @@ void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const doubl
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cfg.dynamicSmemBytes <= 160 * 1024) {
+        if (cfg.dynamicSmemBytes <= 190 * 1024) {
             R1_CUDA(cudaLaunchKernelEx(&cfg, bk_solve_cluster_kernel, s, static_cast<const int*>(L.pperm)));
             check_launch(ctx, "bk_solve_cluster_kernel");
             return;
