@@ -117,3 +117,25 @@ def test_rqi_rejects_near_singular_shift(gpu_ctx, ref):
     s = 0.5 * (s + s.T)
     x = q[:, 7].copy()
     assert (r1.rayleigh_quotient_step(s, x) is None) == (ref.rayleigh_quotient_step(s, x) is None)
+
+
+def test_rqi_large_n_fallback_paths(gpu_ctx):
+    """n = 12000: the panel no longer fits in shared memory (global-memory
+    panel kernel) and the cluster solve's rows exceed its shared-memory cap
+    (cooperative grid solve).  y = normalised (S - rho I)^-1 x, so
+    (S - rho I) y must be parallel to x (backward-stable LDL^T: tiny residual)."""
+    import paper_2403_01778_b200 as r1
+    n = 12000
+    rng = np.random.default_rng(12000)
+    m = rng.standard_normal((n, n))
+    s = m + m.T
+    del m
+    x = rng.standard_normal(n)
+    x /= np.linalg.norm(x)
+    y = r1.rayleigh_quotient_step(s, x)
+    assert y is not None
+    assert abs(np.linalg.norm(y) - 1.0) <= 1e-12
+    rho = float(x @ (s @ x))
+    r = s @ y - rho * y
+    c = float(x @ r)
+    assert np.linalg.norm(r - c * x) <= 1e-9 * np.linalg.norm(r)
