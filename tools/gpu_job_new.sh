@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_bk_gpu.py -q -x -k large_n 2>&1 | tail -3
+R1_DEBUG_EIG=1 timeout 120 python tools/solve_probe.py C2 C5 --alg hoscf --reps 1 2>&1 | grep "r1 eig" | sed 's/lo=.*res_hi=[^ ]* //' | head -12
