@@ -1192,17 +1192,8 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
                                                           kEigDynSmem));
     if (per_sm < 1) fail(R1_ERR_CUDA, "lanczos kernel cannot be resident");
     void* args[] = {&a};
-    // Small operators (C1/C4-sized: n <= 1024 and <= 2 MB of blocks) run on one
-    // CTA with CTA barriers: a cooperative grid sync costs ~5 us, more than
-    // a whole Lanczos step's work there.
-    const int64_t op_bytes = 8 * (P.op.dense ? n * n : P.coldot_n * 0 + [&] {
-        int64_t b = 0;
-        for (int p = 0; p < P.op.npairs; ++p) b += P.op.dims[P.op.pm[p]] * P.op.dims[P.op.pn[p]];
-        return b;
-    }());
-    const int auto_grid = (n <= 1024 && op_bytes <= (int64_t(2) << 20)) ? 1 : ctx->num_sms;
-    (void)auto_grid;
-    static const char* g1 = std::getenv("R1_EIG_SMALL_ONE_CTA");
+    // (small operators took the cluster kernel above; R1_EIG_CLUSTER / R1_EIG_GRID
+    // are development overrides for this grid kernel)
     const int cl_size = gc ? std::max(0, std::min(16, std::atoi(gc))) : 0;
     if (cl_size > 1 && !gs) {
         // the whole Lanczos run on ONE thread-block cluster: cluster barriers
@@ -1227,8 +1218,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
         cfg.numAttrs = 1;
         R1_CUDA(cudaLaunchKernelEx(&cfg, lanczos_kernel, a));
     } else {
-        const int grid = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs)))
-                            : (g1 && std::atoi(g1) ? auto_grid : ctx->num_sms);
+        const int grid = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs))) : ctx->num_sms;
         R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel), dim3(grid),
                                             dim3(kEigThreads), args, kEigDynSmem, ctx->stream));
     }

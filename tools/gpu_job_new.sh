@@ -1,1 +1,2 @@
-R1_DEBUG_EIG=1 timeout 120 python tools/solve_probe.py C2 C5 --alg hoscf --reps 1 2>&1 | grep "r1 eig" | sed 's/lo=.*res_hi=[^ ]* //' | head -12
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 2>&1 | tail -1 | cut -c1-600
