@@ -518,9 +518,9 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         // [A] matvec partials of v_j
         mark(7);
         if (j == 0)
-            blockop_phase_a(op, a.V);
+            blockop_phase_a<false>(op, a.V);
         else
-            blockop_phase_a(op, a.w, inv_beta);
+            blockop_phase_a<false>(op, a.w, inv_beta);
         mark(0);
         gsync();
         mark(1);
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
             for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) vj[t] = a.w[t] * inv_beta;
             __syncthreads();
         }
-        blockop_phase_b(op, a.w, r0 + threadIdx.x, blockDim.x, r1);
+        blockop_phase_b<false>(op, a.w, r0 + threadIdx.x, blockDim.x, r1);
         __syncthreads();
         mark(2);
         cgs2(j);
@@ -1254,7 +1254,7 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
     auto& P = eig_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
     if (!P) {
         P = std::make_shared<EigPlan>();
-        blockop_layout(P->op, dims, order, &P->coldot_n, &P->rowpart_n);
+        blockop_layout(P->op, dims, order, &P->coldot_n, &P->rowpart_n, int64_t(1) << 40);
     }
     P->op.blocks = blocks;
     P->op.dense = nullptr;

@@ -1,2 +1,2 @@
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 2>&1 | tail -1 | cut -c1-600
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+for v in old new old new; do R1_LIB_PATH=$PWD/abtest/$v.so timeout 120 python tools/solve_probe.py C2 C5 --alg hoscf,ihoscf --reps 3 2>&1 | grep rep2 | sed "s/^/$v /" | cut -c1-140; done
