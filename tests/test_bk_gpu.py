@@ -44,7 +44,8 @@ def sym(rng, n):
     return m + m.T
 
 
-CASES = ["rand5", "rand33", "rand100", "rand257", "zero_diag", "tiny_diag", "rank_def", "blockJ"]
+CASES = ["rand1", "rand2", "rand5", "rand33", "rand100", "rand257", "rand1000", "rand2050", "zero_diag",
+         "tiny_diag", "rank_def", "blockJ"]  # rand1000 / rand2050: 4- / 9-CTA panel clusters
 
 
 def make(case, oracle):
