@@ -705,6 +705,35 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
                 x1 = same ? Cis[r] : (i == k + 1 ? cimax : (i == kp ? cik1 : Cis[r]));
             }
         };
+        // NEXT first (everyone waits for it): the final W rows of kn, kn+1 are
+        // their old part (the row itself, or the interchange partner kk's for
+        // kp) and the new column value(s) of that row -> every CTA; the raw
+        // entries an interchange moves into columns kn, kn+1 -> kp's owner
+        uint32_t next_bytes = 0;
+        if (more) {
+            const int okp = owner(kp);
+            for (int s = 0; s < 2; ++s) {
+                const int q = kn + s;
+                if (q >= n) break;
+                next_bytes += 8u * jn;
+                if (q >= lo && q < hi) {
+                    const double* old = swap && q == kp ? w_kk : Ws + (q - lo) * kBkW;
+                    double x0, x1;
+                    new_w(q - lo, q, x0, x1);
+                    for (int e = tid; e < G * jn; e += NT) {
+                        const int dst = e / jn, t = e - dst * jn;
+                        const double v = t < jp ? old[t] : (t == jp ? x0 : x1);
+                        send8(&nextm[b][s * kBkW + t], v, &bars[4 + b], dst);
+                    }
+                }
+                if (swap && q <= kp) {
+                    if (okp == me) next_bytes += 8u;
+                    const int srow = q < kp ? q : kk;  // the raw entry's row in column kk
+                    if (srow >= lo && srow < hi && ((srow - lo) & (NT - 1)) == tid)
+                        send8(&nextm[b][2 * kBkW + s], rkk[srow - lo], &bars[4 + b], okp);
+                }
+            }
+        }
         if (swap) {
             if (kk >= lo && kk < hi && tid < jp) pend[0][tid] = Wim[tid];
             if (kp >= lo && kp < hi && tid < jp) pend[1][tid] = w_kk[tid];
@@ -742,30 +771,6 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         mark(13);
         __syncthreads();
         mark(14);
-        uint32_t next_bytes = 0;
-        if (more) {
-            // NEXT: final W rows of kn, kn+1 -> every CTA (kp's row is the pending
-            // copy); raw entries moved into columns kn, kn+1 -> kp's owner
-            const int okp = owner(kp);
-            for (int s = 0; s < 2; ++s) {
-                const int q = kn + s;
-                if (q >= n) break;
-                next_bytes += 8u * jn;
-                if (q >= lo && q < hi) {
-                    const double* src = swap && q == kp ? pend[1] : Ws + (q - lo) * kBkW;
-                    for (int e = tid; e < G * jn; e += NT) {
-                        const int dst = e / jn, t = e - dst * jn;
-                        send8(&nextm[b][s * kBkW + t], src[t], &bars[4 + b], dst);
-                    }
-                }
-                if (swap && q <= kp) {
-                    if (okp == me) next_bytes += 8u;
-                    const int srow = q < kp ? q : kk;  // the raw entry's row in column kk
-                    if (srow >= lo && srow < hi && ((srow - lo) & (NT - 1)) == tid)
-                        send8(&nextm[b][2 * kBkW + s], rkk[srow - lo], &bars[4 + b], okp);
-                }
-            }
-        }
         mark(6);
         // prefetch the raw columns kn, kn+1 (patched at the top of the next
         // step), issued after NEXT so they stream during the stores
