@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_kernel(const BkArgs a) {
 // patched in; interchanged rows of the panel's earlier L columns are rebuilt
 // from the W rows (stores only).
 constexpr size_t kBkPanelSmemMax = 200 * 1024;
+constexpr int kBkMaxRowsPerThread = 3;  // rows of a CTA per thread when the panel fits (rcap <= 656)
 constexpr int kBkMsg = 4;  // doubles per CAND / RMAX record
 
 // Pivot coefficients of one panel step, kept by every CTA so a row of the
@@ -598,6 +599,18 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         double cimax = 0.0, cik = 0.0, cik1 = 0.0;
         const bool imax_path = !(absakk >= kBkAlpha * colmax);
         if (imax_path) {
+            // the column imax of the stored matrix (own rows), loaded first: its
+            // L2 latency overlaps the remote W-row read and the L-row build
+            double araw[kBkMaxRowsPerThread];
+            const int rfirst = first_row(k);
+            {
+                const double* ci = col(imax);
+#pragma unroll
+                for (int q = 0; q < kBkMaxRowsPerThread; ++q) {
+                    const int r = rfirst + q * NT, i = lo + r;
+                    araw[q] = r < R ? (i >= imax ? ci[i] : col(i)[imax]) : 0.0;
+                }
+            }
             const int oi = owner(imax);
             const int lo_i = k0 + chunk * oi;
             const double* wrem = cl.map_shared_rank(Ws, oi) + (imax - lo_i) * kBkW;
@@ -613,11 +626,13 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
             }
             __syncthreads();
             double rv = -1.0;
-            const double* ci = col(imax);
-            for (int r = first_row(k); r < R; r += NT) {
+#pragma unroll
+            for (int q = 0; q < kBkMaxRowsPerThread; ++q) {
+                const int r = rfirst + q * NT;
+                if (r >= R) break;
                 const int i = lo + r;
                 const double* w = Ws + r * kBkW;
-                double s0 = i >= imax ? ci[i] : col(i)[imax], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                double s0 = araw[q], s1 = 0.0, s2 = 0.0, s3 = 0.0;
                 int t = 0;
                 for (; t + 4 <= jp; t += 4) {
                     s0 -= w[t] * Lr[t];
@@ -1593,7 +1608,7 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     // CTA rows of W + the two updated columns in shared memory when they fit
     const int rcap = static_cast<int>((n + gp - 1) / gp);
     const size_t psmem = static_cast<size_t>(rcap) * (kBkW + 6) * sizeof(double);
-    const bool smem_panel = psmem <= kBkPanelSmemMax && gp <= 16;
+    const bool smem_panel = psmem <= kBkPanelSmemMax && gp <= 16 && rcap <= kBkMaxRowsPerThread * kBkThreads;
     static int configured = -1;
     if (configured != ctx->device) {
         for (auto fn : {bk_panel_smem_kernel<kBkThreads, false>, bk_panel_smem_kernel<kBkThreads, true>}) {
