@@ -6,18 +6,27 @@
 // (1+sqrt17)/8; 1x1 without interchange, 1x1 with k <-> imax, 2x2 with
 // k+1 <-> imax; ties to the first index; zero column -> singular), blocked the
 // LAPACK dlasyf way so the O(n^3) work runs on all SMs:
-//   * panel kernel (cooperative, a few dozen CTAs): for each of <= 32 (+1 when
-//     a 2x2 pivot straddles the edge) columns, form the updated column from
-//     the stored matrix minus the panel's delayed update (W = unscaled pivot
-//     columns, L), reduce colmax / rowmax over the grid, pick the pivot, apply
-//     the symmetric interchange, eliminate.  2-4 grid barriers per column.
-//   * trailing update kernel (all SMs): A22 -= W L^T on the lower triangle,
-//     128x128 tiles, W / L panels and the A tile staged with cp.async.
+//   * panel kernel (ONE thread-block cluster of <= 16 CTAs, rows split across
+//     the CTAs, W / updated columns / raw columns in shared memory): for each
+//     of <= 32 (+1 when a 2x2 pivot straddles the edge) columns, form the
+//     updated column from the stored matrix minus the panel's delayed update
+//     (W = unscaled pivot columns, L), find colmax / rowmax across the
+//     cluster, pick the pivot, apply the symmetric interchange, eliminate.
+//     Cross-CTA data moves as st.async messages counted on mbarriers (no
+//     cluster barrier inside the column loop; bk_panel_smem_kernel);
+//     bk_panel_kernel is the global-memory fallback for panels that do not
+//     fit in shared memory;
+//   * trailing update (all SMs): A22 -= W L^T on the lower triangle on the
+//     FP64 tensor cores (bk_update_tc_kernel; bk_update2_kernel is the DFMA
+//     version);
+//   * solve (bk_solve_cluster_kernel: one cluster, z in shared memory, each
+//     panel's interchanges composed once by bk_perm_kernel; bk_solve_kernel
+//     is the cooperative-grid fallback).
 // D, the pivot sequence and the solution are the reference's (its accept test
 // only reads D).  Interchanges are applied to the rows of the CURRENT panel's
 // L only, so each panel's L is stored in the row order at the end of that
-// panel (the blocked LAPACK convention); the solve (one cooperative kernel)
-// applies them panel by panel: forward (P_p, L_p), D^-1, backward (L_p^T, P_p^T).
+// panel (the blocked LAPACK convention); the solve applies them panel by
+// panel: forward (P_p, L_p), D^-1, backward (L_p^T, P_p^T).
 #include "common.cuh"
 
 #include <cooperative_groups.h>

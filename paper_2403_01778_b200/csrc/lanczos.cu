@@ -2,17 +2,22 @@
 //
 // Replaces rank1::largest_magnitude_eigenpair(J.dense()) (reference
 // proj/src/sym_eig.cpp:206-229: tred2 + implicit QL on the dense sum(I) x
-// sum(I) matrix, O(n^3) per HOSCF iteration) by Lanczos on the block operator:
+// sum(I) matrix, O(n^3) per HOSCF iteration) by Lanczos:
 //
-//   * one persistent cooperative kernel (grid = #SMs, grid.sync between
-//     phases) runs the whole solve; the host launches once and reads nothing;
-//   * matvec through the blocks (blockmv.cuh), never forming dense J;
+//   * lanczos_kernel: one persistent cooperative kernel (grid = #SMs,
+//     grid.sync between phases) runs the whole solve, the matvec through the
+//     blocks (blockmv.cuh, never forming dense J); lanczos_cluster_kernel
+//     (n <= 1024): the same algorithm on ONE thread-block cluster with the
+//     rows of J, V and w in shared memory and DSMEM partial sums;
 //   * full reorthogonalisation, classical Gram-Schmidt applied twice;
 //   * every `check_every` steps CTA 0 computes BOTH extreme eigenvalues of
 //     the tridiagonal T by Sturm-count multisection, their T-eigenvectors by
-//     inverse iteration and the Ritz residual bounds |beta_m s_m|; the solve
-//     stops when both ends satisfy bound <= tol * max(|theta_lo|,|theta_hi|)
+//     inverse iteration and the Ritz residual bounds |beta_m s_m|; the picked
+//     end must reach tol, the other end only as far as the pick rule needs
 //     (or the Krylov space is the whole space, then T's spectrum is exact);
+//   * inside a solve the start vector is the previous eigenvector plus the
+//     previous other-end Ritz vector, and the first check follows the
+//     previous step count (both reset by the solve's cold first call);
 //   * the reference's pick rule (lo iff |lo| > |hi| (1 + 1e-12),
 //     sym_eig.cpp:214-216) and sign rule (largest-|entry| positive, first
 //     index on ties, :223-227) are applied to the Ritz pair;
