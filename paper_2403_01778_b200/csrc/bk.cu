@@ -17,8 +17,7 @@
 //     bk_panel_kernel is the global-memory fallback for panels that do not
 //     fit in shared memory;
 //   * trailing update (all SMs): A22 -= W L^T on the lower triangle on the
-//     FP64 tensor cores (bk_update_tc_kernel; bk_update2_kernel is the DFMA
-//     version);
+//     FP64 tensor cores (bk_update_tc_kernel);
 //   * solve (bk_solve_cluster_kernel: one cluster, z in shared memory, each
 //     panel's interchanges composed once by bk_perm_kernel; bk_solve_kernel
 //     is the cooperative-grid fallback).
@@ -886,86 +885,7 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
     cl.sync();  // no CTA exits while others may still read its shared memory
 }
 
-// A22 -= W L^T, 128 x 128 tiles, 8 x 8 per thread (rows tx + 16 r, cols ty + 16 c:
-// coalesced A traffic, conflict-free / broadcast shared loads).  The A tile is
-// staged into shared memory with cp.async while the W L^T product is formed,
-// so its HBM read overlaps the FP64 work.
-constexpr int kBkT2 = 128;
-constexpr size_t kBkUpdSmem = (2 * kBkW * kBkT2 + kBkT2 * kBkT2) * sizeof(double);
-
-
-__global__ void __launch_bounds__(kBkThreads, 1) bk_update2_kernel(const BkArgs a) {
-    extern __shared__ __align__(16) double usm[];
-    double* Wt = usm;                  // [kBkW][kBkT2]
-    double* Lt = usm + kBkW * kBkT2;   // [kBkW][kBkT2]
-    double* At = Lt + kBkW * kBkT2;    // [kBkT2 cols][kBkT2 rows]
-    const int64_t n = a.n;
-    const int64_t k0 = a.ctl[2];
-    const int jp = a.ctl[3];
-    const int64_t kend = k0 + jp;
-    const int64_t m = n - kend;
-    if (m <= 0 || jp == 0) return;
-    const int64_t T = (m + kBkT2 - 1) / kBkT2;
-    const int64_t ntiles = T * (T + 1) / 2;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    for (int64_t x = blockIdx.x; x < ntiles; x += gridDim.x) {
-        int64_t bi = static_cast<int64_t>((sqrt(8.0 * static_cast<double>(x) + 1.0) - 1.0) * 0.5);
-        while (bi * (bi + 1) / 2 > x) --bi;
-        while ((bi + 1) * (bi + 2) / 2 <= x) ++bi;
-        const int64_t bj = x - bi * (bi + 1) / 2;
-        const int64_t i0 = kend + bi * kBkT2, j0 = kend + bj * kBkT2;
-        const int rows = static_cast<int>(n - i0 < kBkT2 ? n - i0 : kBkT2);
-        const int cols = static_cast<int>(n - j0 < kBkT2 ? n - j0 : kBkT2);
-        __syncthreads();
-        // W / L panels (needed first), then the A tile (needed last)
-        for (int e = threadIdx.x; e < kBkT2 * jp; e += blockDim.x) {
-            const int r = e % kBkT2, t = e / kBkT2;
-            if (r < rows) cp_async8(&Wt[t * kBkT2 + r], a.Wp + (i0 + r) + t * n);
-            else Wt[t * kBkT2 + r] = 0.0;
-            if (r < cols) cp_async8(&Lt[t * kBkT2 + r], a.A + (j0 + r) + (k0 + t) * n);
-            else Lt[t * kBkT2 + r] = 0.0;
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        for (int e = threadIdx.x; e < kBkT2 * cols; e += blockDim.x) {
-            const int r = e % kBkT2, c = e / kBkT2;
-            if (r < rows) cp_async8(&At[c * kBkT2 + r], a.A + (i0 + r) + (j0 + c) * n);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-        double acc[8][8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
-        for (int t = 0; t < jp; ++t) {
-            double w[8], l[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) w[r] = Wt[t * kBkT2 + tx + 16 * r];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) l[c] = Lt[t * kBkT2 + ty + 16 * c];
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-#pragma unroll
-                for (int c = 0; c < 8; ++c) acc[r][c] = fma(w[r], l[c], acc[r][c]);
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        const bool diag = bi == bj;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const int cc = ty + 16 * c;
-            if (cc >= cols) continue;
-            const int64_t j = j0 + cc;
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int rr = tx + 16 * r;
-                const int64_t i = i0 + rr;
-                if (rr < rows && (!diag || i >= j)) a.A[i + j * n] = At[cc * kBkT2 + rr] - acc[r][c];
-            }
-        }
-    }
-}
+constexpr int kBkT2 = 128;  // trailing-update tile rows
 
 // A22 -= W L^T on the FP64 tensor cores (mma.sync m8n8k4 f64): 128 x 64
 // tiles of the trailing lower triangle (each 128 x 128 block of the triangle
@@ -974,7 +894,8 @@ __global__ void __launch_bounds__(kBkThreads, 1) bk_update2_kernel(const BkArgs 
 // accumulator fragments (negated: acc = W L^T - A, stored back negated, which
 // is exact), so only the W / L panels are staged in shared memory (cp.async,
 // row stride kBkUpdLd: conflict-free fragment loads).  One mma replaces 8 DFMA
-// issue slots per lane; the DFMA kernel ran its FP64 pipe at ~31%.
+// issue slots per lane; a DFMA version of this kernel ran its FP64 pipe at
+// ~31% (2 warps per scheduler) and was 18% slower end to end.
 constexpr int kBkUpdLd = kBkT2 + 8;                  // 136: t-rows 16 banks apart
 constexpr int kBkUpdK = (kBkW + 3) / 4 * 4;          // 36: panel width rounded to k = 4
 constexpr int kBkUpdCols = 64;                       // tile columns
@@ -1625,8 +1546,6 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
                                          static_cast<int>(kBkPanelSmemMax)));
             R1_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         }
-        R1_CUDA(cudaFuncSetAttribute(bk_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kBkUpdSmem)));
         R1_CUDA(cudaFuncSetAttribute(bk_update_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kBkUpdTcSmem)));
         configured = ctx->device;
@@ -1636,9 +1555,6 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     auto panel_fn = trace ? bk_panel_smem_kernel<kBkThreads, true> : bk_panel_smem_kernel<kBkThreads, false>;
     cudaLaunchConfig_t pcfg = cfg;
     pcfg.dynamicSmemBytes = psmem;
-    // trailing update on the FP64 tensor cores (R1_BK_UPDATE_DFMA=1: the DFMA kernel)
-    static const char* ud = std::getenv("R1_BK_UPDATE_DFMA");
-    const bool upd_tc = !(ud && std::atoi(ud));
     // each panel factors >= kBkNb columns (or the rest); extra launches exit at once
     const int64_t panels = (n + kBkNb - 1) / kBkNb;
     for (int64_t p = 0; p < panels; ++p) {
@@ -1647,11 +1563,8 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         else
             R1_CUDA(cudaLaunchKernelEx(&cfg, bk_panel_kernel, a));
         check_launch(ctx, "bk_panel_kernel");
-        if (upd_tc)
-            bk_update_tc_kernel<<<2 * ctx->num_sms, kBkThreads, kBkUpdTcSmem, ctx->stream>>>(a);
-        else
-            bk_update2_kernel<<<ctx->num_sms, kBkThreads, kBkUpdSmem, ctx->stream>>>(a);
-        check_launch(ctx, "bk_update2_kernel");
+        bk_update_tc_kernel<<<2 * ctx->num_sms, kBkThreads, kBkUpdTcSmem, ctx->stream>>>(a);
+        check_launch(ctx, "bk_update_tc_kernel");
     }
     bk_condition_kernel<<<1, 1024, 0, ctx->stream>>>(A, n, L.ctl, L.ps, cond_dev);
     check_launch(ctx, "bk_condition_kernel");
