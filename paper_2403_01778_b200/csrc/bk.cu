@@ -27,6 +27,7 @@
 // panel (the blocked LAPACK convention); the solve applies them panel by
 // panel: forward (P_p, L_p), D^-1, backward (L_p^T, P_p^T).
 #include "common.cuh"
+#include "dsmem.cuh"
 
 #include <cooperative_groups.h>
 
@@ -384,37 +385,8 @@ __device__ __forceinline__ void warp_amax(double& v, int& i, double& s) {
                    __shfl_xor_sync(0xffffffffu, s, off));
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-
-// v -> the same shared-memory slot of CTA `rank`, counted on its mbarrier `bar`
-__device__ __forceinline__ void send8(const void* slot, double v, const uint64_t* bar, int rank) {
-    uint32_t ra, rb;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(slot)), "r"(rank));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(v),
-                 "r"(rb)
-                 : "memory");
-}
-
-__device__ __forceinline__ void expect_bytes(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void wait_parity(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "BK_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra BK_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
 }
 
 // NT threads per CTA; TRACE compiles the phase timers in (their register
@@ -481,9 +453,8 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
     };
     if (tid < 2) pend_row[tid] = -1;
     if (tid == 0) {
-        for (int b = 0; b < 6; ++b)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[b])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b < 6; ++b) mbar_init1(&bars[b]);
+        mbar_init_fence();
     }
     // raw columns k0, k0+1 of this panel
     for (int s = 0; s < 2; ++s) {

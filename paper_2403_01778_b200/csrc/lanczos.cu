@@ -27,6 +27,7 @@
 // All reductions have a fixed order over a fixed grid: deterministic.
 #include "common.cuh"
 #include "blockmv.cuh"
+#include "dsmem.cuh"
 
 #include <cooperative_groups.h>
 
@@ -750,6 +751,16 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     __shared__ double red[32];
     __shared__ double nrmp[16];
     __shared__ double fin[5][16];
+    // message barriers (dsmem.cuh): 0 CGS pass 1, 1 CGS pass 2, 2 publish;
+    // their phases advance identically in every CTA (uniform control flow)
+    __shared__ __align__(8) uint64_t mbar[3];
+    uint32_t ph1 = 0, ph2 = 0, php = 0;
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) mbar_init1(&mbar[b]);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    cl.sync();  // barriers initialised, every CTA running, before any DSMEM store
     // diagnostics (R1_DEBUG_EIG): per-phase ns of CTA 0 thread 0 -> stats[8..15]
     unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tlast = gtimer();
@@ -776,33 +787,39 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         }
         Sown[static_cast<size_t>(r) * n + u] = v;
     }
-    // publish own rows of w and the CTA's ||w||^2 partial to every CTA; after
-    // the barrier every CTA returns sqrt(sum of the partials in CTA order)
+    // publish own rows of w and the CTA's ||w||^2 partial to every CTA (st.async
+    // messages); once all (G + n) values have arrived every CTA returns
+    // sqrt(sum of the partials in CTA order).  Buffers are reused safely: a CTA
+    // sends a phase's data only after receiving the previous phase from all.
     auto publish = [&]() {
         double ss = 0.0;
         for (int r = tid; r < Rm; r += kEigThreads) ss = fma(ws[r], ws[r], ss);
         ss = cta_sum(ss, red);
-        if (tid < G) *cl.map_shared_rank(&nrmp[me], tid) = ss;
+        if (tid < G) send8(&nrmp[me], ss, &mbar[2], tid);
         for (int e = tid; e < G * Rm; e += kEigThreads) {
             const int c = e / Rm, r = e - c * Rm;
-            *cl.map_shared_rank(&wfull[r0 + r], c) = ws[r];
+            send8(&wfull[r0 + r], ws[r], &mbar[2], c);
         }
-        cl.sync();
+        if (tid == 0) expect_bytes(&mbar[2], static_cast<uint32_t>((G + n) * 8));
+        wait_parity(&mbar[2], php & 1);
+        ++php;
         double t = 0.0;
         for (int c = 0; c < G; ++c) t += nrmp[c];
         return sqrt(t);
     };
     // one classical Gram-Schmidt pass of w (own rows) against V[:, 0..j]
-    auto cgs_pass = [&](double* hp, int j) {
+    auto cgs_pass = [&](double* hp, int j, uint64_t* bar, uint32_t& ph) {
         for (int k = warp; k <= j; k += nw) {
             const double* vk = Vs + k * R;
             double s = 0.0;
             for (int r = lane; r < Rm; r += 32) s = fma(vk[r], ws[r], s);
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            if (lane < G) *cl.map_shared_rank(&hp[me * ld + k], lane) = s;
+            if (lane < G) send8(&hp[me * ld + k], s, bar, lane);
         }
-        cl.sync();
+        if (tid == 0) expect_bytes(bar, static_cast<uint32_t>(G * (j + 1) * 8));
+        wait_parity(bar, ph & 1);
+        ++ph;
         for (int k = tid; k <= j; k += kEigThreads) {
             double h = 0.0;
             for (int c = 0; c < G; ++c) h += hp[c * ld + k];
@@ -851,10 +868,10 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         }
         __syncthreads();
         mark(1);
-        cgs_pass(hp1, j);
+        cgs_pass(hp1, j, &mbar[0], ph1);
         const double h1j = hsh[j];
         mark(2);
-        cgs_pass(hp2, j);
+        cgs_pass(hp2, j, &mbar[1], ph2);
         const double alpha = h1j + hsh[j];
         mark(3);
         double nrm = publish();
@@ -875,8 +892,8 @@ __global__ void __launch_bounds__(kEigThreads, 1)
             for (int r = tid; r < Rm; r += kEigThreads)
                 ws[r] = hash_unit(static_cast<uint64_t>(r0 + r), 0xb00ull + breakdowns);
             __syncthreads();
-            cgs_pass(hp1, j);
-            cgs_pass(hp2, j);
+            cgs_pass(hp1, j, &mbar[0], ph1);
+            cgs_pass(hp2, j, &mbar[1], ph2);
             nrm = publish();
         }
         inv_beta = 1.0 / nrm;
