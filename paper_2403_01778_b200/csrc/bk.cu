@@ -1216,6 +1216,11 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
     __shared__ double part[2][16][kBkW];              // pushed backward partials, by parity
     __shared__ double zp[2 * kBkW];
     __shared__ double nrm2[16];
+    // message barriers by panel parity (dsmem.cuh): the slot values (and, in
+    // the backward pass, the partials) a panel needs count on mbar[par]
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ double tok[2][16];  // forward-pass tokens (see recv)
+    uint32_t mph[2] = {0, 0};
     const int n = static_cast<int>(s.n);
     const int G = gridDim.x, me = blockIdx.x, tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -1245,7 +1250,26 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         for (int e = tid; e < m * G; e += kBkThreads) {
             const int j = e % m, d = e / m;
             const int row = slot_row(P, c0, w, j);
-            if (row >= lo && row < hi) *cl.map_shared_rank(&gsl[par][j], d) = zs[row - lo];
+            if (row >= lo && row < hi) send8(&gsl[par][j], zs[row - lo], &mbar[par], d);
+        }
+    };
+    // panel p's messages at this CTA: its m slot values, plus G w partials
+    // (backward) or one token from every CTA (forward).  Only the owners of a
+    // panel's slot rows send slot values, so without the tokens a CTA with
+    // nothing to send imposes no wait and others could run two panels ahead
+    // into the same-parity buffer; a token is sent after its sender has read
+    // the previous panel's buffer (the backward partials come from every CTA).
+    auto recv = [&](int p, int par, bool partials) {
+        int c0, c1;
+        pbounds(p, c0, c1);
+        const int w = c1 - c0, m = w + rec(p)[0];
+        if (tid == 0) expect_bytes(&mbar[par], static_cast<uint32_t>((m + (partials ? G * w : G)) * 8));
+        if (par == 0) {
+            wait_parity(&mbar[0], mph[0] & 1);
+            ++mph[0];
+        } else {
+            wait_parity(&mbar[1], mph[1] & 1);
+            ++mph[1];
         }
     };
     // forward: Lb[par][t][i] = L(c0+i, c0+t), i > t (column t contiguous)
@@ -1273,13 +1297,22 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     for (int r = tid; r < R; r += kBkThreads) zs[r] = s.x[lo + r];
+    if (tid == 0) {
+        mbar_init1(&mbar[0]);
+        mbar_init1(&mbar[1]);
+        mbar_init_fence();
+    }
     __syncthreads();
+    cl.sync();  // barriers initialised, every CTA running, before any DSMEM store
+    auto token = [&](int par) {
+        if (tid < G) send8(&tok[par][me], 0.0, &mbar[par], tid);
+    };
     if (np > 0) {
         prefetch_rows(0);
         push_slots(0, 0);
+        token(0);
         load_fwd_block(0, 0);
     }
-    cl.sync();
     // ---- forward
     for (int p = 0; p < np; ++p) {
         const int par = p & 1;
@@ -1287,6 +1320,8 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         pbounds(p, c0, c1);
         const int* P = rec(p);
         const int w = c1 - c0, m = w + P[0];
+        recv(p, par, false);
+        __syncthreads();  // load_fwd_block(p) of the previous iteration is complete
         if (tid < m) zp[tid] = gsl[par][P[4 + kBkW + tid]];
         __syncthreads();
         if (warp == 0) {
@@ -1316,10 +1351,13 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
             }
         }
         __syncthreads();
-        if (p + 1 < np) prefetch_rows(p + 1);
-        if (p + 1 < np) push_slots(p + 1, par ^ 1);
-        cl.sync();
+        if (p + 1 < np) {
+            prefetch_rows(p + 1);
+            push_slots(p + 1, par ^ 1);
+            token(par ^ 1);
+        }
     }
+    cl.sync();  // D^-1 below reads / writes a neighbour's z for straddling 2x2 blocks
     // ---- D^-1 (sym_eig.cpp:338-352); a 2x2 pair is solved by its first row's owner
     for (int r = tid; r < R; r += kBkThreads) {
         const int k = lo + r;
@@ -1351,7 +1389,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
             for (int r = r0 + lane; r < R; r += 32) acc += ct[r] * zs[r];
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane < G) *cl.map_shared_rank(&part[par][me][t], lane) = acc;
+            if (lane < G) send8(&part[par][me][t], acc, &mbar[par], lane);
         }
         push_slots(p, par);
     };
@@ -1361,13 +1399,13 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         __syncthreads();
         push_back(np - 1, (np - 1) & 1);
     }
-    cl.sync();
     for (int p = np - 1; p >= 0; --p) {
         const int par = p & 1;
         int c0, c1;
         pbounds(p, c0, c1);
         const int* P = rec(p);
         const int w = c1 - c0, m = w + P[0];
+        recv(p, par, true);
         __syncthreads();  // push_back(p) finished reading Lr
         if (p > 0) prefetch_rows(p - 1);
         // backward block: Lb[par][i][t] = L(c0+i, c0+t), i > t (row i contiguous)
@@ -1400,7 +1438,6 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (p > 0) push_back(p - 1, par ^ 1);
-        cl.sync();
     }
     // ---- normalise (sym_eig.cpp:425-431)
     {
