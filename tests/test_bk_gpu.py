@@ -140,3 +140,20 @@ def test_rqi_large_n_fallback_paths(gpu_ctx):
     r = s @ y - rho * y
     c = float(x @ r)
     assert np.linalg.norm(r - c * x) <= 1e-9 * np.linalg.norm(r)
+
+
+def test_rqi_deterministic_multi_cta(gpu_ctx):
+    """n = 2500 (10-CTA panel cluster and cluster solve, both exchanging
+    st.async messages without cluster barriers): repeated RQI steps are
+    bit-identical."""
+    import paper_2403_01778_b200 as r1
+    n = 2500
+    rng = np.random.default_rng(2500)
+    m = rng.standard_normal((n, n))
+    s = m + m.T
+    x = rng.standard_normal(n)
+    x /= np.linalg.norm(x)
+    y0 = r1.rayleigh_quotient_step(s, x)
+    assert y0 is not None
+    for _ in range(3):
+        assert np.array_equal(r1.rayleigh_quotient_step(s, x), y0)
