@@ -1,1 +1,1 @@
-for g in 148 96 64 48 32; do R1_EIG_GRID=$g timeout 120 python tools/solve_probe.py C2 C5 --alg hoscf --reps 3 2>&1 | grep rep2 | sed "s/^/G=$g /" | cut -c1-140; done
+timeout 900 python -m pytest tests/test_acceptance_gpu.py -q --durations=5 2>&1 | tail -25
