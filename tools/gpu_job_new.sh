@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_acceptance_gpu.py -q --durations=5 2>&1 | tail -25
+timeout 600 python -m pytest tests/test_reference_kats_gpu.py -q 2>&1 | tail -15
