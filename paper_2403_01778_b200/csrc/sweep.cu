@@ -411,7 +411,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     sweep3_box_kernel(const SweepArgs p, const __grid_constant__ BoxMaps maps, int nst,
                       int stage_dbl) {
     static_assert(KO * NCB <= 32, "C1 reduction holds KO * NCB values per lane");
-    static_assert(NRA % 2 == 0, "rows are read in pairs");
+    static_assert(NRA % 2 == 0 && NRA <= 8, "rows are read in pairs, at most 4 pairs per lane");
     constexpr int RMAX = 32 * NRA;
     constexpr int NP = NRA / 2;
     extern __shared__ __align__(1024) double smem[];
@@ -424,10 +424,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // A lane's NRA rows are NP 16-B pairs at byte offset 32*lane: lanes l and
-    // l+4 of a quarter warp would hit the same banks, so odd quarter-lanes take
-    // their pairs in swapped order (pair slot q holds pair q ^ hsw).
-    const int hsw = NP > 1 ? (lane >> 2) & 1 : 0;
+    // A lane's NRA rows are NP 16-B pairs at byte offset 16*NP*lane.  NP = 2:
+    // lanes l and l+4 of a quarter warp would hit the same banks, so odd
+    // quarter-lanes take their pairs in swapped order (pair slot q holds pair
+    // q ^ hsw); NP = 4: lanes l, l+2, l+4, l+6 collide, hsw = (l >> 1) & 3.
+    const int hsw = NP == 4 ? (lane >> 1) & 3 : (NP > 1 ? (lane >> 2) & 1 : 0);
     for (int i = threadIdx.x; i < ring_dbl / 2; i += blockDim.x)
         reinterpret_cast<double2*>(ring)[i] = make_double2(0.0, 0.0);
     if (threadIdx.x == 0) {
@@ -1008,7 +1009,19 @@ void tile_level(Level& L, int num_sms) {
     if (L.tma) {
         // Balanced tiles on the fixed RMAX x CMAX consumer grid, in the merged view.
         L.nra = L.MI0 > 64 ? 4 : 2;
-        const int rm = 32 * L.nra, cm = kBoxNWC * kBoxNCB;
+        L.ncb = kBoxNCB;
+        // 128 < I0 <= 256, unmerged: one 256 x 30 row tile (8 rows x 2 columns
+        // per lane, the same 16 accumulators) instead of two 128 x 60 ones —
+        // no C1 partials, and no 128-B line shared by two row tiles (C3 200^4:
+        // with a 1600-B column pitch every column's split fell inside a line,
+        // 8% extra DRAM reads)
+        static const char* n8_env = std::getenv("R1_SWEEP_NRA8");
+        const bool nra8 = n8_env ? std::atoi(n8_env) != 0 : true;
+        if (nra8 && L.K == 1 && L.MI0 > 128 && L.MI0 <= 256) {
+            L.nra = 8;
+            L.ncb = 2;
+        }
+        const int rm = 32 * L.nra, cm = kBoxNWC * L.ncb;
         L.G0 = static_cast<int>((L.MI0 + rm - 1) / rm);
         L.r0 = static_cast<int>((L.MI0 + L.G0 - 1) / L.G0);
         // Whole 128-B lines per tile row when the (merged) column pitch is a
@@ -1019,7 +1032,7 @@ void tile_level(Level& L, int num_sms) {
         // a half-line column pitch (8 I0 = 64 mod 128, unmerged): round the row
         // tile up to whole lines, so the tile split is line-aligned in every
         // other column (C3 200^4: 100 -> 112 rows, -1.5%)
-        if (L.K == 1 && (8 * L.I0) % 128 == 64 && L.r0 % 16 != 0) {
+        if (L.G0 > 1 && L.K == 1 && (8 * L.I0) % 128 == 64 && L.r0 % 16 != 0) {
             const int r16 = (L.r0 + 15) / 16 * 16;
             if (r16 <= rm && static_cast<int64_t>(r16) * ((L.MI0 + L.r0 - 1) / L.r0 - 1) < L.MI0) L.r0 = r16;
         }
@@ -1305,10 +1318,10 @@ void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const C
     check_launch(ctx, "sweep3_kernel");
 }
 
-template <int NRA, bool SR, int KO>
+template <int NRA, bool SR, int KO, int NCB = kBoxNCB>
 void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
     static int configured_device = -1;
-    auto kern = sweep3_box_kernel<NRA, kBoxNCB, kBoxNWC, SR, KO>;
+    auto kern = sweep3_box_kernel<NRA, NCB, kBoxNWC, SR, KO>;
     if (configured_device != ctx->device) {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBudget)));
@@ -1341,7 +1354,10 @@ void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
     if (L.tma) {
         static const char* sr = std::getenv("R1_SWEEP_STAGE_REGS");
         const bool stage_regs = sr ? std::atoi(sr) != 0 : true;
-        if (L.nra == 4) {
+        if (L.nra == 8) {
+            if (stage_regs) launch_box<8, true, 1, 2>(ctx, L, a);
+            else launch_box<8, false, 1, 2>(ctx, L, a);
+        } else if (L.nra == 4) {
             if (stage_regs) launch_box<4, true, 1>(ctx, L, a);
             else launch_box<4, false, 1>(ctx, L, a);
         } else if (L.KO == 4) {
@@ -1447,7 +1463,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
             static const char* dm = std::getenv("R1_DEBUG_SWEEP_MODE");
             s.debug_mode = dm ? std::atoi(dm) : 0;
         }
-        if (L.nra == 4)
+        if (L.nra == 4 || L.nra == 8)  // (nra 8: box kernel only)
             launch_sweep<4, 8, 3>(ctx, L, s);
         else if (L.nra == 2)
             launch_sweep<2, 8, 5>(ctx, L, s);

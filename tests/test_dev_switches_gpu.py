@@ -45,12 +45,21 @@ a = ref.generate("exp", dims)
 got = r1.ihoscf(r1.DenseTensor(dims, a), r1.SolveOptions(tol=1e-8))
 want = ref.solve("ihoscf", a, dims, tol=1e-8, max_iters=500, seed=0)
 assert got.converged and abs(got.result.lambda_ - want["lam"]) <= 1e-10 * want["lam"]
+# sweep (every block) against the oracle restatement
+from oracle import rank1_oracle as o
+for dims in ((200, 200, 7), (200, 64, 6, 5), (1000, 4, 3)):
+    a = o.oracle_random_tensor(dims, 3)
+    f = o.oracle_random_unit_factors(dims, 4)
+    got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
+    scale = o.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
+    assert np.all(np.abs(got - o.build_j(a, dims, f)) <= 1e-13 * scale + 1e-300), dims
 print("ok")
 """
 
 
 @pytest.mark.parametrize("env", [{"R1_RQI_CUSOLVER": "1"}, {"R1_BK_GRID_SOLVE": "1"},
-                                 {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"}])
+                                 {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"},
+                                 {"R1_SWEEP_NRA8": "0"}, {"R1_SWEEP_MERGE": "0"}])
 def test_switch_paths(gpu_ctx, env):
     r = subprocess.run([sys.executable, "-c", CHECK], env=dict(os.environ, **env), capture_output=True,
                        text=True, timeout=600)

@@ -19,6 +19,9 @@ SHAPES = [
     (40, 12, 6, 2), (100, 4, 2, 2, 2),
     # small single-tile faces: KO o-panels per box (KO = 2 and 4)
     (30, 20, 6), (64, 60, 12), (8, 6, 4, 2, 3),
+    # 128 < I0 <= 256 unmerged: one 256-row x 30-column tile per column strip
+    # (8 rows x 2 columns per lane), ragged last column tile, recursion levels
+    (200, 200, 7), (130, 61, 5), (256, 31, 4), (200, 64, 6, 5), (250, 33, 2, 2, 2),
     # extreme aspect ratios: a long fastest mode, a tiny face with a long
     # outer mode, unit modes
     (100000, 3, 2), (2, 2, 50000), (1, 1, 1, 1, 1000), (5000, 1, 7), (1, 4000, 3),
