@@ -421,6 +421,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * KO * NWC * RMAX);
     uint64_t* empty = full + kMaxStages;
     int4* meta = reinterpret_cast<int4*>(empty + kMaxStages);  // per stage {seg, tile, o, flags}
+    uint64_t* red_full = reinterpret_cast<uint64_t*>(meta + kMaxStages);  // [2] C0 partial slots
+    uint64_t* red_empty = red_full + 2;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -435,6 +437,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
         for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NWC);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&red_full[s], NWC);
+            mbar_init(&red_empty[s], NWC);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -514,6 +520,31 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     int coff[NCB];  // smem offset (double2 units) of the thread's columns
     double* P0row = nullptr;
     double* P1row = nullptr;
+    // KO == 1: the C0 block reduction of panel q (partials in red slot q & 1)
+    // is summed one panel later, after the warp has written panel q + 1's
+    // partials — an mbarrier pair per slot instead of a CTA barrier per panel,
+    // so no warp waits for the slowest one at every panel and the sums overlap
+    // the next panel's loads (C3 200^4: the barrier-synchronous reduction cost
+    // 18% of the level-0 kernel)
+    int pc = 0;                 // panels consumed by this CTA
+    double* pend_dst = nullptr;  // C0 row of panel pc - 1
+    int pend_r0e = 0;
+    auto reduce_pending = [&]() {
+        const int q = pc - 1, slot = q & 1;
+        if (warp * 32 < pend_r0e) {
+            mbar_wait(&red_full[slot], (q >> 1) & 1);
+            const int i = threadIdx.x;
+            if (i < pend_r0e) {
+                const double* rr = red + slot * NWC * RMAX + i;
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX];
+                pend_dst[i] = sum;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&red_empty[slot]);
+    };
     for (;;) {
         mbar_wait(&full[stage], phase);
         const int4 md = meta[stage];
@@ -633,17 +664,20 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 }
             }
 
-            double2* rb =
-                reinterpret_cast<double2*>(red + rbuf * NWC * RMAX + warp * RMAX) + (NRA / 2) * lane;
+            {
+                static_assert(NRA <= NWC, "one C0 row per consumer thread");
+                const int slot = pc & 1;
+                mbar_wait(&red_empty[slot], ((pc >> 1) & 1) ^ 1);
+                double2* rb =
+                    reinterpret_cast<double2*>(red + slot * NWC * RMAX + warp * RMAX) + (NRA / 2) * lane;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) rb[q ^ hsw] = make_double2(c0p[2 * q], c0p[2 * q + 1]);
-            asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory");
-            const double* rr = red + rbuf * NWC * RMAX;
-            for (int i = threadIdx.x; i < r0e; i += NWC * 32) {
-                double sum = 0.0;
-#pragma unroll
-                for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX + i];
-                P0row[static_cast<int64_t>(o) * MI0 + i] = sum;
+                for (int q = 0; q < NP; ++q) rb[q ^ hsw] = make_double2(c0p[2 * q], c0p[2 * q + 1]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&red_full[slot]);
+                if (pc > 0) reduce_pending();
+                pend_dst = P0row + static_cast<int64_t>(o) * MI0;
+                pend_r0e = r0e;
+                ++pc;
             }
             } else {
             const double2* st = reinterpret_cast<const double2*>(ring + stage * stage_dbl);
@@ -772,6 +806,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 }
             }
         }
+    }
+    if constexpr (KO == 1) {
+        if (pc > 0) reduce_pending();
     }
     if (p.trace && threadIdx.x == 0) {
         unsigned long long t_end;
@@ -935,6 +972,7 @@ struct Level {
     int KO = 1;                // o-panels per box (small faces); segments count o-groups
     int64_t MI0 = 0, MI1 = 0;  // merged view K I0 x I1/K (tiles live here)
     int nra = 4, ncb = 8, stages = 3;
+    int nwc = 15;  // consumer warps (box kernel)
     int stage_dbl = 0;
     int dyn_first = 0, ndyn = 0;  // dynamic-tail segments (box kernel only)
     bool tma = false;
@@ -1017,11 +1055,12 @@ void tile_level(Level& L, int num_sms) {
         // 8% extra DRAM reads)
         static const char* n8_env = std::getenv("R1_SWEEP_NRA8");
         const bool nra8 = n8_env ? std::atoi(n8_env) != 0 : true;
+        L.nwc = kBoxNWC;  // (8 warps x 4 columns at I0 = 200 measured no faster)
         if (nra8 && L.K == 1 && L.MI0 > 128 && L.MI0 <= 256) {
             L.nra = 8;
             L.ncb = 2;
         }
-        const int rm = 32 * L.nra, cm = kBoxNWC * L.ncb;
+        const int rm = 32 * L.nra, cm = L.nwc * L.ncb;
         L.G0 = static_cast<int>((L.MI0 + rm - 1) / rm);
         L.r0 = static_cast<int>((L.MI0 + L.G0 - 1) / L.G0);
         // Whole 128-B lines per tile row when the (merged) column pitch is a
@@ -1052,8 +1091,8 @@ void tile_level(Level& L, int num_sms) {
                     L.KO = ko;
                     break;
                 }
-        const size_t red = static_cast<size_t>(2) * L.KO * kBoxNWC * rm * 8;
-        const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16;
+        const size_t red = static_cast<size_t>(2) * L.KO * L.nwc * rm * 8;
+        const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16 + 4 * 8;
         const size_t box = static_cast<size_t>(L.r0) * L.t1 * 8 * L.KO;
         const size_t ring = kSmemBudget - red - bars - rm * 8 - 1024;
         L.stages = static_cast<int>(std::min<size_t>(kMaxStages, ring / box));
@@ -1318,10 +1357,10 @@ void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const C
     check_launch(ctx, "sweep3_kernel");
 }
 
-template <int NRA, bool SR, int KO, int NCB = kBoxNCB>
+template <int NRA, bool SR, int KO, int NCB = kBoxNCB, int NWC = kBoxNWC>
 void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
     static int configured_device = -1;
-    auto kern = sweep3_box_kernel<NRA, NCB, kBoxNWC, SR, KO>;
+    auto kern = sweep3_box_kernel<NRA, NCB, NWC, SR, KO>;
     if (configured_device != ctx->device) {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBudget)));
@@ -1341,7 +1380,7 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
         R1_CUDA(cudaEventCreate(&e1));
         R1_CUDA(cudaEventRecord(e0, ctx->stream));
     }
-    kern<<<L.ncta, (kBoxNWC + 1) * 32, L.smem, ctx->stream>>>(a, maps, L.stages, L.stage_dbl);
+    kern<<<L.ncta, (NWC + 1) * 32, L.smem, ctx->stream>>>(a, maps, L.stages, L.stage_dbl);
     check_launch(ctx, "sweep3_box_kernel");
     if (timed) {
         R1_CUDA(cudaEventRecord(e1, ctx->stream));
