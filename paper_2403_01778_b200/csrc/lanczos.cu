@@ -853,15 +853,23 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         // v_j = w * inv_beta (own rows into V, all rows from wfull), w = J v_j
         for (int r = tid; r < Rm; r += kEigThreads) Vs[j * R + r] = ws[r] * inv_beta;
         for (int r = warp; r < Rm; r += nw) {
+            // 8 independent loads per lane in flight: at n > ~600 the rows
+            // live in L2 (they do not fit next to V in shared memory) and a
+            // 2-deep loop was latency-bound (~5 us per step at n = 800)
             const double* sr = Sown + static_cast<size_t>(r) * n;
-            double s0 = 0.0, s1 = 0.0;
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
             int u = lane;
-            for (; u + 32 < n; u += 64) {
-                s0 = fma(sr[u], wfull[u], s0);
-                s1 = fma(sr[u + 32], wfull[u + 32], s1);
+            for (; u + 7 * 32 < n; u += 8 * 32) {
+                double x[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x[k] = sr[u + 32 * k];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) s4[k & 3] = fma(x[k], wfull[u + 32 * k], s4[k & 3]);
             }
-            if (u < n) s0 = fma(sr[u], wfull[u], s0);
-            double s = s0 + s1;
+#pragma unroll
+            for (int k = 0; k < 7; ++k)
+                if (u + 32 * k < n) s4[k & 3] = fma(sr[u + 32 * k], wfull[u + 32 * k], s4[k & 3]);
+            double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
             if (lane == 0) ws[r] = s * inv_beta * op.scale;
