@@ -16,7 +16,10 @@ def shares(path):
     for r in rows[start + 1:]:
         if len(r) < len(h) or r[im] != "gpu__time_duration.sum":
             continue
-        name = r[ik].split("(")[0].replace("void ", "").replace("unnamed>::", "").replace("r1::", "")
+        name = r[ik].split("(")[0].replace("void ", "").replace("<unnamed>::", "").replace("unnamed>::", "")
+        name = name.replace("r1::", "")
+        if name.startswith("at::"):  # torch's own kernels (input generation in the probes)
+            continue
         v = float(r[iv].replace(",", ""))
         v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[iu], 1.0)
         agg[name][0] += 1
