@@ -77,6 +77,7 @@ struct EigArgs {
     const double* x1;  // previous solve's other-end Ritz vector (start = x0 + x1), or null
     double* other_out; // this solve's other-end Ritz vector (unit), or null
     int debug_text;    // development: print the phase split of t_extremes
+    double warm_noise; // weight of the random component of a warm start vector
 };
 
 __device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     };
     for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
         const double r = hash_unit(static_cast<uint64_t>(t), 0x5eedull);
-        a.w[t] = a.x0 ? a.x0[t] + (a.x1 ? a.x1[t] : 0.0) + 1e-3 * r / sqrt(static_cast<double>(n)) : r;
+        a.w[t] = a.x0 ? a.x0[t] + (a.x1 ? a.x1[t] : 0.0) + a.warm_noise * r / sqrt(static_cast<double>(n)) : r;
     }
     set_v0_from_w();
 
@@ -837,7 +838,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     for (int r = tid; r < Rm; r += kEigThreads) {
         const int t = r0 + r;
         const double rr = hash_unit(static_cast<uint64_t>(t), 0x5eedull);
-        ws[r] = a.x0 ? a.x0[t] + (a.x1 ? a.x1[t] : 0.0) + 1e-3 * rr / sqrt(static_cast<double>(n)) : rr;
+        ws[r] = a.x0 ? a.x0[t] + (a.x1 ? a.x1[t] : 0.0) + a.warm_noise * rr / sqrt(static_cast<double>(n)) : rr;
     }
     __syncthreads();
     double inv_beta = 1.0 / publish();
@@ -1137,6 +1138,10 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.out_vec = vec_dev;
     static const bool dbg_text = std::getenv("R1_DEBUG_EIG_TEXT") != nullptr;
     a.debug_text = dbg_text ? 1 : 0;
+    static const char* wn = std::getenv("R1_EIG_WARM_NOISE");  // development
+    // 1e-6 (was 1e-3): the previous Ritz vectors are good to ~1e-5 or better,
+    // a 1e-3 random component only had to be filtered out again (C1 eigen -6%)
+    a.warm_noise = wn ? std::atof(wn) : 1e-6;
     if (solver_chain) {
         if (!P.hint.ptr) {
             P.hint.ensure(sizeof(int));
