@@ -848,6 +848,23 @@ struct FinishArgs {
 // Element per thread.  With K == 1 the C0 / C1 partial copies have the output
 // layout (a plain sum of copies); K is a power of two.  IDX is the index type
 // (32-bit whenever the level's element counts allow).
+// s = ((0 + v_0) + v_1) + ... in index order, the loads issued 8 at a time
+// (predicated) so they are in flight together: the second stage is a
+// latency-bound gather of G partials per output
+template <typename F>
+__device__ __forceinline__ double ordered_sum(int cnt, F at) {
+    double s = 0.0;
+    for (int b = 0; b < cnt; b += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = b + u < cnt ? __ldcs(at(b + u)) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (b + u < cnt) s += v[u];
+    }
+    return s;
+}
+
 template <typename IDX>
 __global__ void finish_kernel(const FinishArgs f) {
     const IDX nb = static_cast<IDX>(f.n_b01), n0 = static_cast<IDX>(f.n_c0);
@@ -867,37 +884,33 @@ __global__ void finish_kernel(const FinishArgs f) {
             const double* src = f.P01 + static_cast<int64_t>(c - static_cast<IDX>(g1) * f.t1) * f.r0 +
                                 (r - static_cast<IDX>(g0) * f.r0);
             const int sb = __ldg(f.tile_seg + tile), se = __ldg(f.tile_seg + tile + 1);
-#pragma unroll 4
-            for (int k = sb; k < se; ++k) s += __ldcs(src + k * tile_elems);
+            s = ordered_sum(se - sb, [&](int t) { return src + (sb + t) * tile_elems; });
             f.b01[e] = s;
         } else if (e < nb + n0) {
             const IDX x = e - nb;
             if (K == 1) {
                 const double* src = f.P0 + x;
-#pragma unroll 6
-                for (int g = 0; g < f.G1; ++g) s += __ldcs(src + g * f.stride0);
+                s = ordered_sum(f.G1, [&](int g) { return src + g * f.stride0; });
             } else {
                 const IDX o = x / I0, i0 = x - o * I0;
                 const double* src = f.P0 + static_cast<int64_t>(o) * K * f.I0 + i0;
-                for (int g = 0; g < f.G1; ++g)
-#pragma unroll 4
-                    for (int q = 0; q < K; ++q) s += __ldcs(src + g * f.stride0 + q * f.I0);
+                // (g, q) flattened, same summation order
+                s = ordered_sum(f.G1 * K,
+                                [&](int t) { return src + (t >> f.lgK) * f.stride0 + (t & (K - 1)) * f.I0; });
             }
             f.c0[x] = s;
         } else {
             const IDX x = e - nb - n0;
             if (K == 1) {
                 const double* src = f.P1 + x;
-#pragma unroll 4
-                for (int g = 0; g < f.G0; ++g) s += __ldcs(src + g * f.stride1);
+                s = ordered_sum(f.G0, [&](int g) { return src + g * f.stride1; });
             } else {
                 const IDX o = x / I1, i1 = x - o * I1;
                 const int p = static_cast<int>(i1 & (K - 1));
                 const int ga = static_cast<int>(p * f.I0 / f.r0);
                 const int gb = static_cast<int>(((p + 1) * f.I0 - 1) / f.r0);
                 const double* src = f.P1 + static_cast<int64_t>(o) * f.I1 + p * f.MI1 + (i1 >> f.lgK);
-#pragma unroll 4
-                for (int g = ga; g <= gb; ++g) s += __ldcs(src + g * f.stride1);
+                s = ordered_sum(gb - ga + 1, [&](int t) { return src + (ga + t) * f.stride1; });
             }
             f.c1[x] = s;
         }
