@@ -16,7 +16,10 @@ def _blocks(oracle, dims, seed):
 
 @pytest.mark.parametrize("dims", [(3, 4), (5, 7), (2, 2, 2), (7, 5, 9), (30, 20, 10),
                                   (6, 5, 4, 3), (4, 3, 5, 2, 3), (40, 30, 20), (100, 100, 100),
-                                  (20, 20, 20, 20)])
+                                  (20, 20, 20, 20),
+                                  # n = 301 (odd), 1024 (largest single-cluster
+                                  # kernel: J rows in L2), 1025 (grid kernel)
+                                  (101, 100, 100), (400, 324, 300), (400, 325, 300)])
 def test_eig_blocks_matches_reference(gpu_ctx, oracle, ref, dims):
     import paper_2403_01778_b200 as r1
     a, f, blocks = _blocks(oracle, dims, 31)
