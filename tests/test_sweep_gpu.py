@@ -22,6 +22,9 @@ SHAPES = [
     # 128 < I0 <= 256 unmerged: one 256-row x 30-column tile per column strip
     # (8 rows x 2 columns per lane), ragged last column tile, recursion levels
     (200, 200, 7), (130, 61, 5), (256, 31, 4), (200, 64, 6, 5), (250, 33, 2, 2, 2),
+    # the same I0 range merged (K = 2 / 4: wide enough faces), 128-row tiles
+    # straddling the class boundary
+    (200, 500, 3), (136, 480, 4), (132, 1000, 2),
     # extreme aspect ratios: a long fastest mode, a tiny face with a long
     # outer mode, unit modes
     (100000, 3, 2), (2, 2, 50000), (1, 1, 1, 1, 1000), (5000, 1, 7), (1, 4000, 3),
