@@ -1157,7 +1157,9 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     // counter (SM bandwidth shares vary by ~10%; a static split waits for the
     // slowest SM).
     const bool dyn = L.tma && npanels >= static_cast<int64_t>(L.ncta) * 64;
-    const double static_total = dyn ? (1.0 - kDynFrac) * total : total;
+    static const char* df_env = std::getenv("R1_SWEEP_DYN_FRAC");  // development
+    const double dyn_frac = df_env ? std::atof(df_env) : kDynFrac;
+    const double static_total = dyn ? (1.0 - dyn_frac) * total : total;
     const double full_cost = static_cast<double>(L.r0) * L.t1 + 512.0;
     const double per = static_total / static_cast<double>(L.ncta);
     int cur = 0;          // CTA receiving the current panel
@@ -1175,7 +1177,9 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
             }
             if (in_dyn) {
                 // guided chunk size: remaining / (2 ncta), at least kDynMinChunk panels
-                const double target = std::max(kDynMinChunk * full_cost,
+                static const char* mc_env = std::getenv("R1_SWEEP_DYN_CHUNK");  // development
+                const double min_chunk = mc_env ? std::atof(mc_env) : kDynMinChunk;
+                const double target = std::max(min_chunk * full_cost,
                                                (total - x) / (2.0 * L.ncta));
                 if (segs.size() == static_cast<size_t>(L.dyn_first) || segs.back().tile != t ||
                     segs.back().o1 != o || chunk >= target) {

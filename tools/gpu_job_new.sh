@@ -1,7 +1,6 @@
 #!/bin/bash
-timeout 900 python -m pytest tests/test_sweep_gpu.py -q -x 2>&1 | tail -2
-timeout 300 python -c "
-import sys; sys.path.insert(0,'.')
-import paper_2403_01778_b200 as r1
-ctx=r1.default_context()
-for d in [(200,500,3),(136,480,4),(132,1000,2)]: print(d, ctx.sweep_plan_info(d))"
+for i in 1 2; do
+for cfg in "R1_SWEEP_DYN_FRAC=0.25" "R1_SWEEP_DYN_FRAC=0.12" "R1_SWEEP_DYN_FRAC=0.4" "R1_SWEEP_DYN_CHUNK=4" "R1_SWEEP_DYN_CHUNK=16"; do
+echo "== $cfg"; env $cfg timeout 300 python tools/sweep_probe.py C2 C3 C5 --reps 20 2>&1 | grep -v "^   [a-z]" | sed 's/dims=.*median/median/'
+done
+done
