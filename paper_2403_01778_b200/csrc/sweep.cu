@@ -843,7 +843,18 @@ struct FinishArgs {
     int64_t stride1;
     double* c1;
     int64_t n_b01, n_c0, n_c1;
+    // x / d for 0 <= x < 2^31 as (x * m) >> s (m = ceil(2^s / d), s = 31 +
+    // ceil(log2 d): exact, Granlund-Montgomery) for d = I0, I1, r0, t1
+    uint64_t m_I0, m_I1, m_r0, m_t1;
+    int s_I0, s_I1, s_r0, s_t1;
 };
+
+void fastdiv_init(int64_t d, uint64_t& m, int& sh) {
+    int l = 0;
+    while ((int64_t(1) << l) < d) ++l;
+    sh = 31 + l;
+    m = static_cast<uint64_t>(((static_cast<unsigned __int128>(1) << sh) + d - 1) / d);
+}
 
 // Element per thread.  With K == 1 the C0 / C1 partial copies have the output
 // layout (a plain sum of copies); K is a power of two.  IDX is the index type
@@ -866,6 +877,14 @@ __device__ __forceinline__ double ordered_sum(int cnt, F at) {
 }
 
 template <typename IDX>
+__device__ __forceinline__ IDX fdiv(IDX x, int64_t d, uint64_t m, int sh) {
+    if constexpr (sizeof(IDX) == 4)
+        return static_cast<IDX>((static_cast<uint64_t>(x) * m) >> sh);  // x < 2^31
+    else
+        return x / static_cast<IDX>(d);
+}
+
+template <typename IDX>
 __global__ void finish_kernel(const FinishArgs f) {
     const IDX nb = static_cast<IDX>(f.n_b01), n0 = static_cast<IDX>(f.n_c0);
     const IDX total = nb + n0 + static_cast<IDX>(f.n_c1);
@@ -876,10 +895,11 @@ __global__ void finish_kernel(const FinishArgs f) {
          e += static_cast<IDX>(gridDim.x) * blockDim.x) {
         double s = 0.0;
         if (e < nb) {
-            const IDX i1 = e / I0, i0 = e - i1 * I0;
+            const IDX i1 = fdiv<IDX>(e, f.I0, f.m_I0, f.s_I0), i0 = e - i1 * I0;
             const IDX p = i1 & (K - 1), c = i1 >> f.lgK;
             const IDX r = p * I0 + i0;
-            const int g0 = static_cast<int>(r / f.r0), g1 = static_cast<int>(c / f.t1);
+            const int g0 = static_cast<int>(fdiv<IDX>(r, f.r0, f.m_r0, f.s_r0));
+            const int g1 = static_cast<int>(fdiv<IDX>(c, f.t1, f.m_t1, f.s_t1));
             const int tile = g0 + f.G0 * g1;
             const double* src = f.P01 + static_cast<int64_t>(c - static_cast<IDX>(g1) * f.t1) * f.r0 +
                                 (r - static_cast<IDX>(g0) * f.r0);
@@ -892,7 +912,7 @@ __global__ void finish_kernel(const FinishArgs f) {
                 const double* src = f.P0 + x;
                 s = ordered_sum(f.G1, [&](int g) { return src + g * f.stride0; });
             } else {
-                const IDX o = x / I0, i0 = x - o * I0;
+                const IDX o = fdiv<IDX>(x, f.I0, f.m_I0, f.s_I0), i0 = x - o * I0;
                 const double* src = f.P0 + static_cast<int64_t>(o) * K * f.I0 + i0;
                 // (g, q) flattened, same summation order
                 s = ordered_sum(f.G1 * K,
@@ -905,10 +925,11 @@ __global__ void finish_kernel(const FinishArgs f) {
                 const double* src = f.P1 + x;
                 s = ordered_sum(f.G0, [&](int g) { return src + g * f.stride1; });
             } else {
-                const IDX o = x / I1, i1 = x - o * I1;
+                const IDX o = fdiv<IDX>(x, f.I1, f.m_I1, f.s_I1), i1 = x - o * I1;
                 const int p = static_cast<int>(i1 & (K - 1));
-                const int ga = static_cast<int>(p * f.I0 / f.r0);
-                const int gb = static_cast<int>(((p + 1) * f.I0 - 1) / f.r0);
+                const int ga = static_cast<int>(fdiv<IDX>(static_cast<IDX>(p * f.I0), f.r0, f.m_r0, f.s_r0));
+                const int gb =
+                    static_cast<int>(fdiv<IDX>(static_cast<IDX>((p + 1) * f.I0 - 1), f.r0, f.m_r0, f.s_r0));
                 const double* src = f.P1 + static_cast<int64_t>(o) * f.I1 + p * f.MI1 + (i1 >> f.lgK);
                 s = ordered_sum(gb - ga + 1, [&](int t) { return src + (ga + t) * f.stride1; });
             }
@@ -1555,6 +1576,10 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
             f.n_c1 = L.I1 * L.O;
         }
         f.n_b01 = L.I0 * L.I1;
+        fastdiv_init(L.I0, f.m_I0, f.s_I0);
+        fastdiv_init(L.I1, f.m_I1, f.s_I1);
+        fastdiv_init(L.r0, f.m_r0, f.s_r0);
+        fastdiv_init(L.t1, f.m_t1, f.s_t1);
         if (L.nseg >= 64 * L.ntiles) {
             // many segments per tile: B01 by warps, C0/C1 (if any) below
             const int64_t warps = f.n_b01;
