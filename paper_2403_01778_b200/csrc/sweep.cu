@@ -859,19 +859,61 @@ void fastdiv_init(int64_t d, uint64_t& m, int& sh) {
 // Element per thread.  With K == 1 the C0 / C1 partial copies have the output
 // layout (a plain sum of copies); K is a power of two.  IDX is the index type
 // (32-bit whenever the level's element counts allow).
-// s = ((0 + v_0) + v_1) + ... in index order, the loads issued 8 at a time
-// (predicated) so they are in flight together: the second stage is a
-// latency-bound gather of G partials per output
-template <typename F>
-__device__ __forceinline__ double ordered_sum(int cnt, F at) {
+// Fixed-order sums of partials: s = ((0 + v_0) + v_1) + ... in index order.
+// ordered_sum over p[0], p[stride], ...: full batches of 8 loads without
+// predication, then 4, then singles; the pointer advances (no per-load
+// multiply) — the generic version cost ~480 instructions per output at C2
+__device__ __forceinline__ double ordered_sum_strided(int cnt, const double* p, int64_t stride) {
     double s = 0.0;
-    for (int b = 0; b < cnt; b += 8) {
+    int t = 0;
+    for (; t + 8 <= cnt; t += 8, p += 8 * stride) {
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = b + u < cnt ? __ldcs(at(b + u)) : 0.0;
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(p + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    if (t < cnt) {  // the rest as one predicated batch (loads in flight together)
+        const int r = cnt - t;
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = u < r ? __ldcs(p + u * stride) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            if (b + u < cnt) s += v[u];
+            if (u < r) s += v[u];
+    }
+    return s;
+}
+
+// sum over g < G (outer), q < KK (inner) of p[g stride + q inner], in that order
+template <int KK>
+__device__ __forceinline__ double ordered_sum_2d(int G, const double* p, int64_t stride, int64_t inner) {
+    constexpr int GB = KK >= 8 ? 1 : 8 / KK;  // g's per batch (8+ loads in flight)
+    double s = 0.0;
+    int g = 0;
+    for (; g + GB <= G; g += GB, p += GB * stride) {
+        double v[GB][KK];
+#pragma unroll
+        for (int a = 0; a < GB; ++a)
+#pragma unroll
+            for (int q = 0; q < KK; ++q) v[a][q] = __ldcs(p + a * stride + q * inner);
+#pragma unroll
+        for (int a = 0; a < GB; ++a)
+#pragma unroll
+            for (int q = 0; q < KK; ++q) s += v[a][q];
+    }
+    if (g < G) {  // the rest (< GB g's) as one predicated batch
+        const int r = G - g;
+        double v[GB][KK];
+#pragma unroll
+        for (int a = 0; a < GB; ++a)
+#pragma unroll
+            for (int q = 0; q < KK; ++q) v[a][q] = a < r ? __ldcs(p + a * stride + q * inner) : 0.0;
+#pragma unroll
+        for (int a = 0; a < GB; ++a)
+#pragma unroll
+            for (int q = 0; q < KK; ++q)
+                if (a < r) s += v[a][q];
     }
     return s;
 }
@@ -904,26 +946,30 @@ __global__ void finish_kernel(const FinishArgs f) {
             const double* src = f.P01 + static_cast<int64_t>(c - static_cast<IDX>(g1) * f.t1) * f.r0 +
                                 (r - static_cast<IDX>(g0) * f.r0);
             const int sb = __ldg(f.tile_seg + tile), se = __ldg(f.tile_seg + tile + 1);
-            s = ordered_sum(se - sb, [&](int t) { return src + (sb + t) * tile_elems; });
+            s = ordered_sum_strided(se - sb, src + sb * tile_elems, tile_elems);
             f.b01[e] = s;
         } else if (e < nb + n0) {
             const IDX x = e - nb;
             if (K == 1) {
                 const double* src = f.P0 + x;
-                s = ordered_sum(f.G1, [&](int g) { return src + g * f.stride0; });
+                s = ordered_sum_strided(f.G1, src, f.stride0);
             } else {
                 const IDX o = fdiv<IDX>(x, f.I0, f.m_I0, f.s_I0), i0 = x - o * I0;
                 const double* src = f.P0 + static_cast<int64_t>(o) * K * f.I0 + i0;
-                // (g, q) flattened, same summation order
-                s = ordered_sum(f.G1 * K,
-                                [&](int t) { return src + (t >> f.lgK) * f.stride0 + (t & (K - 1)) * f.I0; });
+                // g outer, q inner: the same summation order
+                switch (K) {
+                    case 2: s = ordered_sum_2d<2>(f.G1, src, f.stride0, f.I0); break;
+                    case 4: s = ordered_sum_2d<4>(f.G1, src, f.stride0, f.I0); break;
+                    case 8: s = ordered_sum_2d<8>(f.G1, src, f.stride0, f.I0); break;
+                    default: s = ordered_sum_2d<16>(f.G1, src, f.stride0, f.I0); break;
+                }
             }
             f.c0[x] = s;
         } else {
             const IDX x = e - nb - n0;
             if (K == 1) {
                 const double* src = f.P1 + x;
-                s = ordered_sum(f.G0, [&](int g) { return src + g * f.stride1; });
+                s = ordered_sum_strided(f.G0, src, f.stride1);
             } else {
                 const IDX o = fdiv<IDX>(x, f.I1, f.m_I1, f.s_I1), i1 = x - o * I1;
                 const int p = static_cast<int>(i1 & (K - 1));
@@ -931,7 +977,7 @@ __global__ void finish_kernel(const FinishArgs f) {
                 const int gb =
                     static_cast<int>(fdiv<IDX>(static_cast<IDX>((p + 1) * f.I0 - 1), f.r0, f.m_r0, f.s_r0));
                 const double* src = f.P1 + static_cast<int64_t>(o) * f.I1 + p * f.MI1 + (i1 >> f.lgK);
-                s = ordered_sum(gb - ga + 1, [&](int t) { return src + (ga + t) * f.stride1; });
+                s = ordered_sum_strided(gb - ga + 1, src + ga * f.stride1, f.stride1);
             }
             f.c1[x] = s;
         }
