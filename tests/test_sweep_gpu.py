@@ -80,6 +80,22 @@ def test_build_j_deterministic(gpu_ctx, oracle):
     assert np.array_equal(b1, b2)
 
 
+@pytest.mark.parametrize("dims", [(200, 200, 300), (1000, 64, 50), (60, 60, 60, 60)])
+def test_build_j_deterministic_box_kernel(gpu_ctx, oracle, dims):
+    """The TMA box kernel with a dynamic tail and the mbarrier-paired C0
+    reduction (256-row tiles / merged classes / KO = 2): repeated sweeps are
+    bit-identical."""
+    import paper_2403_01778_b200 as r1
+    rng = np.random.default_rng(sum(dims))
+    a = rng.standard_normal(int(np.prod(dims)))
+    f = [rng.standard_normal(k) for k in dims]
+    f = [u / np.linalg.norm(u) for u in f]
+    t = r1.DenseTensor(dims, a)
+    b0 = r1.build_j(t, r1.FactorSet(0.0, f)).blocks
+    for _ in range(4):
+        assert np.array_equal(r1.build_j(t, r1.FactorSet(0.0, f)).blocks, b0)
+
+
 def test_build_j_errors(gpu_ctx, oracle):
     """nepv.cpp:24-41 / test_nepv.cpp:104-107, 227-232."""
     import paper_2403_01778_b200 as r1
