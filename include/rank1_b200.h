@@ -134,7 +134,17 @@ int r1_tensor_create(r1_context* ctx, const uint64_t* dims, int order, r1_tensor
  * aligned and readable up to 16*ceil(8N/16) bytes. */
 int r1_tensor_wrap_device(r1_context* ctx, const double* dev, const uint64_t* dims, int order,
                           r1_tensor** out);
-/* Asynchronous H2D of the full tensor on the context stream. */
+/* Page-lock a caller-owned host range for the copy engines (cudaHostRegister)
+ * / release it.  Host-buffer entry points (r1_build_j, r1_tensor_from_host,
+ * ...) copy pinned sources directly and stream pageable ones through the
+ * context's pinned staging lanes (8 host threads x 2 x 16 MiB, memcpy and DMA
+ * overlapped); they never register the caller's memory implicitly, because a
+ * registration outlives a freed std::vector and would redirect later DMA. */
+int r1_host_register(void* host, uint64_t bytes);
+int r1_host_unregister(void* host);
+
+/* Asynchronous H2D of the full tensor on the context stream (pageable sources
+ * are staged; the call returns when the host buffer may be reused). */
 int r1_tensor_copy_from_host(r1_context* ctx, r1_tensor* t, const double* host);
 /* D2H of the whole tensor (synchronous on the context stream). */
 int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host);
@@ -160,8 +170,9 @@ int r1_build_j_device(r1_context* ctx, const r1_tensor* a, const double* factors
 /* Host form with the reference's argument checks (nepv.cpp:24-41, 199-207):
  * order>=2 (invalid_argument), factor lengths (invalid_argument), for d>2 every
  * factor nonzero (runtime_error "degenerate factor set: zero factor for mode k")
- * and unit to 1e-8 (invalid_argument).  `a_host` is copied to the device on
- * every call unless `a_dev` (nullable) is given.  Blocks are returned to host. */
+ * and unit to 1e-8 (invalid_argument).  `a_host` is copied on every call (into
+ * the context's grow-only device buffer: no allocation per call) unless `a_dev`
+ * (nullable) is given.  Blocks are returned to host. */
 int r1_build_j(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
                const uint64_t* dims, int order, const double* factors_host, double* blocks_host);
 

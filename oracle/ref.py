@@ -285,12 +285,8 @@ class SolveReportC(ctypes.Structure):
                 ("t_total", ctypes.c_double)]
 
 
-def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None,
-          rqi_accept_rule=0, record_kkt=True, determinism=True, threads=0, stop_rule=0,
-          asvd_disjoint_pairs=False):
-    """rank1::solve through the reference; returns a dict mirroring SolveReport."""
-    a, ap = _d(a)
-    dd, dp = _dims(dims)
+def _solve_opts(tol, max_iters, seed, init_factors, rqi_accept_rule, record_kkt, determinism,
+                threads, stop_rule, asvd_disjoint_pairs):
     o = SolveOptionsC()
     o.tol = tol
     o.max_iters = max_iters
@@ -307,6 +303,10 @@ def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None
                                                     for f in init_factors]))
         o.init = 1
         o.init_factors = keep.ctypes.data_as(_dp)
+    return o, keep
+
+
+def _solve_call(call, dims, max_iters):
     n = sum(dims)
     fac = np.empty(n)
     fx = np.empty(n)
@@ -315,8 +315,7 @@ def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None
     r.factors = fac.ctypes.data_as(_dp)
     r.final_x = fx.ctypes.data_as(_dp)
     r.trace = tr
-    _check(lib().ref_solve(algorithm.encode(), ap, dp, len(dims), ctypes.byref(o),
-                           ctypes.byref(r)))
+    _check(call(ctypes.byref(r)))
     offs = np.concatenate([[0], np.cumsum(dims)]).astype(int)
     trace = []
     for i in range(r.iterations):
@@ -329,6 +328,33 @@ def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None
                 converged=bool(r.converged), iterations=r.iterations, lambda0=r.lambda0,
                 restarted=bool(r.restarted), final_x=fx.copy(), trace=trace,
                 sweeps=r.total_sweeps, seconds=r.t_total)
+
+
+def solve(algorithm, a, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None,
+          rqi_accept_rule=0, record_kkt=True, determinism=True, threads=0, stop_rule=0,
+          asvd_disjoint_pairs=False):
+    """rank1::solve through the reference; returns a dict mirroring SolveReport."""
+    a, ap = _d(a)
+    dd, dp = _dims(dims)
+    o, keep = _solve_opts(tol, max_iters, seed, init_factors, rqi_accept_rule, record_kkt,
+                          determinism, threads, stop_rule, asvd_disjoint_pairs)
+    return _solve_call(lambda rp: lib().ref_solve(algorithm.encode(), ap, dp, len(dims),
+                                                  ctypes.byref(o), rp), dims, max_iters)
+
+
+_FILL = ctypes.CFUNCTYPE(None, _dp, ctypes.c_uint64, ctypes.c_void_p)
+
+
+def solve_fill(algorithm, fill, dims, tol=1e-4, max_iters=500, seed=0, init_factors=None,
+               rqi_accept_rule=0, record_kkt=True, determinism=True, threads=0, stop_rule=0):
+    """rank1::solve on a tensor the reference allocates itself (DenseTensor(dims))
+    and `fill(address, numel)` writes in place — one host copy of the tensor."""
+    dd, dp = _dims(dims)
+    o, keep = _solve_opts(tol, max_iters, seed, init_factors, rqi_accept_rule, record_kkt,
+                          determinism, threads, stop_rule, False)
+    cb = _FILL(lambda ptr, n, user: fill(ctypes.cast(ptr, ctypes.c_void_p).value, int(n)))
+    return _solve_call(lambda rp: lib().ref_solve_fill(algorithm.encode(), cb, None, dp, len(dims),
+                                                       ctypes.byref(o), rp), dims, max_iters)
 
 
 def greedy(solver, a, dims, r, tol=1e-4, max_iters=500, seed=0, stop_rule=0):
@@ -387,3 +413,47 @@ def experiment_csv(generator, a, dims, algos, seeds, base_seed=0, tol=1e-4, max_
                                     ctypes.byref(o), buf, 1 << 20))
     csv_text, _, table = buf.value.decode().partition("\n\n")
     return csv_text + "\n", table
+
+
+class RefTensor:
+    """A reference DenseTensor allocated by the reference library and filled in
+    place by `fill(address, numel)` (oracle/ref_shim.cpp ref_tensor_new): one host
+    copy, generated once, reused by several timed calls (bench.py CPU arms)."""
+
+    def __init__(self, fill, dims):
+        self.dims = tuple(int(v) for v in dims)
+        self._dd, dp = _dims(self.dims)
+        L = lib()
+        L.ref_tensor_data.restype = ctypes.c_void_p
+        self._cb = _FILL(lambda ptr, n, user: fill(ctypes.cast(ptr, ctypes.c_void_p).value, int(n)))
+        h = ctypes.c_void_p()
+        _check(L.ref_tensor_new(self._cb, None, dp, len(self.dims), ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().ref_tensor_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def time_build_j(self, factors, reps=1, threads=0, determinism=True, want_blocks=False):
+        """Per-call wall seconds of rank1::build_j (and the last call's blocks)."""
+        flat, fp = _d(np.concatenate([np.asarray(f, dtype=np.float64) for f in factors]))
+        out = np.empty(blocks_numel(self.dims)) if want_blocks else None
+        secs = np.zeros(reps)
+        _check(lib().ref_time_build_j_t(self.handle, fp, threads, 1 if determinism else 0, reps,
+                                        out.ctypes.data_as(_dp) if out is not None else None,
+                                        secs.ctypes.data_as(_dp)))
+        return out, secs
+
+    def solve(self, algorithm, tol=1e-4, max_iters=500, seed=0, init_factors=None,
+              rqi_accept_rule=0, record_kkt=True, determinism=True, threads=0, stop_rule=0):
+        o, keep = _solve_opts(tol, max_iters, seed, init_factors, rqi_accept_rule, record_kkt,
+                              determinism, threads, stop_rule, False)
+        return _solve_call(lambda rp: lib().ref_solve_t(algorithm.encode(), self.handle,
+                                                        ctypes.byref(o), rp), self.dims, max_iters)

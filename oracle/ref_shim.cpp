@@ -190,6 +190,44 @@ int ref_time_build_j(const double* a, const uint64_t* dims, int order, const dou
     });
 }
 
+// A reference DenseTensor kept alive across calls (bench.py's CPU arms): the
+// reference allocates it and `fill` writes the entries in place, so a 32 GB
+// config exists once in host memory and is generated once.
+typedef void (*ref_fill_fn)(double* out, uint64_t n, void* user);
+int ref_tensor_new(ref_fill_fn fill, void* user, const uint64_t* dims, int order, void** out) {
+    return guarded([&] {
+        auto* t = new DenseTensor(to_dims(dims, order));
+        fill(t->data(), t->size(), user);
+        *out = t;
+    });
+}
+
+int ref_tensor_free(void* t) {
+    delete static_cast<DenseTensor*>(t);
+    return 0;
+}
+
+double* ref_tensor_data(void* t) { return static_cast<DenseTensor*>(t)->data(); }
+
+int ref_time_build_j_t(void* tp, const double* factors, int threads, int determinism, int reps,
+                       double* blocks_out, double* seconds_out) {
+    return guarded([&] {
+        const DenseTensor& t = *static_cast<DenseTensor*>(tp);
+        std::vector<uint64_t> dims(t.dims().begin(), t.dims().end());
+        FactorSet f = make_factors(factors, dims.data(), static_cast<int>(dims.size()));
+        BuildOptions bo;
+        bo.threads = threads;
+        bo.determinism = determinism != 0;
+        for (int r = 0; r < reps; ++r) {
+            auto t0 = std::chrono::steady_clock::now();
+            SymBlockMatrix j = build_j(t, f, bo);
+            auto t1 = std::chrono::steady_clock::now();
+            seconds_out[r] = std::chrono::duration<double>(t1 - t0).count();
+            if (r == reps - 1 && blocks_out) write_blocks(j, blocks_out);
+        }
+    });
+}
+
 int ref_build_block(const double* a, const uint64_t* dims, int order, const double* factors,
                     int m, int n, double* out) {
     return guarded([&] {
@@ -353,10 +391,9 @@ int ref_rng_draws(uint64_t seed, uint64_t stream, int kind, int64_t count, doubl
 }
 
 // rank1::solve (solvers.cpp:509-517).  report arrays are caller-owned.
-int ref_solve(const char* algorithm, const double* a, const uint64_t* dims, int order,
-              const r1_solve_options* opts, r1_solve_report* rep) {
-    return guarded([&] {
-        DenseTensor t = make_tensor(a, dims, order);
+static void solve_into(const char* algorithm, const DenseTensor& t, const uint64_t* dims,
+                       int order, const r1_solve_options* opts, r1_solve_report* rep) {
+    {
         SolveOptions so = make_opts(opts, dims, order);
         auto t0 = std::chrono::steady_clock::now();
         SolveReport r = solve(algorithm, t, so);
@@ -396,6 +433,31 @@ int ref_solve(const char* algorithm, const double* a, const uint64_t* dims, int 
         }
         rep->total_sweeps = sweeps;
         rep->t_total = std::chrono::duration<double>(t1 - t0).count();
+    }
+}
+
+int ref_solve(const char* algorithm, const double* a, const uint64_t* dims, int order,
+              const r1_solve_options* opts, r1_solve_report* rep) {
+    return guarded([&] { solve_into(algorithm, make_tensor(a, dims, order), dims, order, opts, rep); });
+}
+
+int ref_solve_t(const char* algorithm, void* tp, const r1_solve_options* opts,
+                r1_solve_report* rep) {
+    return guarded([&] {
+        const DenseTensor& t = *static_cast<DenseTensor*>(tp);
+        std::vector<uint64_t> dims(t.dims().begin(), t.dims().end());
+        solve_into(algorithm, t, dims.data(), static_cast<int>(dims.size()), opts, rep);
+    });
+}
+
+// Same, but the tensor is created in the reference's own DenseTensor and filled
+// in place by `fill` (no second host copy: config 5 is 32 GB).
+int ref_solve_fill(const char* algorithm, ref_fill_fn fill, void* user, const uint64_t* dims,
+                   int order, const r1_solve_options* opts, r1_solve_report* rep) {
+    return guarded([&] {
+        DenseTensor t(to_dims(dims, order));
+        fill(t.data(), t.size(), user);
+        solve_into(algorithm, t, dims, order, opts, rep);
     });
 }
 

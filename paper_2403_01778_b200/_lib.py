@@ -87,6 +87,8 @@ SIGNATURES = {
     "r1_tensor_from_host": (ctypes.c_int, [_vp, _dp, _u64p, ctypes.c_int, ctypes.POINTER(_vp)]),
     "r1_tensor_create": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, ctypes.POINTER(_vp)]),
     "r1_tensor_wrap_device": (ctypes.c_int, [_vp, _vp, _u64p, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "r1_host_register": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+    "r1_host_unregister": (ctypes.c_int, [_vp]),
     "r1_tensor_copy_from_host": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_copy_to_host": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_frobenius": (ctypes.c_int, [_vp, _vp, _dp]),

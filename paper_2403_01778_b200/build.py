@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print("\n".join(logs))
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcuda", "-lcusolver"], check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcuda"], check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -1465,9 +1465,9 @@ __global__ void __launch_bounds__(kBkThreads) bk_solve_cluster_kernel(const Solv
 
 // Largest cluster (<= 16, <= one CTA per 256 rows) the device can schedule.
 int panel_cluster_size(r1_context* ctx, int64_t n) {
-    static int max16 = -1;
-    if (max16 < 0) {
-        max16 = cudaFuncSetAttribute(bk_panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+    static std::map<int, int> max_by_device;
+    configure_once(reinterpret_cast<const void*>(bk_panel_kernel), ctx->device, [&] {
+        int max16 = cudaFuncSetAttribute(bk_panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                         cudaSuccess
                     ? 16
                     : 8;
@@ -1489,8 +1489,13 @@ int panel_cluster_size(r1_context* ctx, int64_t n) {
                 max16 = 8;
             cudaGetLastError();
         }
+        max_by_device[ctx->device] = max16;
+    });
+    int max16 = 8;
+    {
+        std::lock_guard<std::mutex> g(cache_mutex());
+        max16 = max_by_device[ctx->device];
     }
-    (void)ctx;
     static const char* genv = std::getenv("R1_BK_G");  // development: force the cluster size
     if (genv) return std::max(1, std::min(max16, std::atoi(genv)));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max16, (n + 255) / 256)));
@@ -1547,8 +1552,7 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     const int rcap = static_cast<int>((n + gp - 1) / gp);
     const size_t psmem = static_cast<size_t>(rcap) * (kBkW + 6) * sizeof(double);
     const bool smem_panel = psmem <= kBkPanelSmemMax && gp <= 16 && rcap <= kBkMaxRowsPerThread * kBkThreads;
-    static int configured = -1;
-    if (configured != ctx->device) {
+    configure_once(reinterpret_cast<const void*>(bk_update_tc_kernel), ctx->device, [&] {
         for (auto fn : {bk_panel_smem_kernel<kBkThreads, false>, bk_panel_smem_kernel<kBkThreads, true>}) {
             R1_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kBkPanelSmemMax)));
@@ -1556,8 +1560,7 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         }
         R1_CUDA(cudaFuncSetAttribute(bk_update_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kBkUpdTcSmem)));
-        configured = ctx->device;
-    }
+    });
     // 256 threads even when a CTA owns 2 rows per thread (n = 6500): 512 was
     // measured 2% slower there (16-warp reductions and barriers)
     auto panel_fn = trace ? bk_panel_smem_kernel<kBkThreads, true> : bk_panel_smem_kernel<kBkThreads, false>;
@@ -1604,14 +1607,12 @@ void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const doubl
         bk_perm_kernel<<<static_cast<int>((mp + 127) / 128), 128, 0, ctx->stream>>>(
             L.ipiv, L.ps, L.perm, L.ctl, static_cast<int>(n), L.pperm);
         check_launch(ctx, "bk_perm_kernel");
-        static int configured = -1;
-        if (configured != ctx->device) {
+        configure_once(reinterpret_cast<const void*>(bk_solve_cluster_kernel), ctx->device, [&] {
             R1_CUDA(cudaFuncSetAttribute(bk_solve_cluster_kernel,
                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             R1_CUDA(cudaFuncSetAttribute(bk_solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          190 * 1024));
-            configured = ctx->device;
-        }
+        });
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(gp);
         cfg.blockDim = dim3(kBkThreads);
@@ -1652,6 +1653,7 @@ extern "C" {
 int r1x_ldlt(r1_context* ctx, int64_t n, const double* s_host, int* ipiv, double* diag,
              double* sub, int* singular, double* cond) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         DeviceBuffer A, ws, c;

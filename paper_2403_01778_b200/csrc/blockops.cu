@@ -105,6 +105,7 @@ void dot_device(r1_context* ctx, const double* x, const double* y, uint64_t n, d
 void block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                   const double* x, double* y) {
     if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "block_matvec: bad order");
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& P = mv_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
     if (!P) {
         P = std::make_shared<MvPlan>();
@@ -126,6 +127,7 @@ void block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double
 }
 
 void forget_matvec_plans(r1_context* ctx) {
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& plans = mv_plans();
     for (auto it = plans.begin(); it != plans.end();)
         if (it->first.first == ctx)

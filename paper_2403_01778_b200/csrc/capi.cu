@@ -12,6 +12,16 @@ namespace r1 {
 
 thread_local std::string g_last_error;
 
+std::mutex& cache_mutex() {
+    static std::mutex m;
+    return m;
+}
+
+std::set<std::pair<const void*, int>>& configured_set() {
+    static std::set<std::pair<const void*, int>> s;
+    return s;
+}
+
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 void forget_matvec_plans(r1_context* ctx);
@@ -57,15 +67,8 @@ void check_unit_nonzero(const uint64_t* dims, int order, const double* flat, con
     }
 }
 
-struct TempTensor {
-    r1_tensor* t = nullptr;
-    ~TempTensor() {
-        if (t) r1_tensor_destroy(t);
-    }
-};
-
 const r1_tensor* device_tensor(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
-                               const uint64_t* dims, int order, TempTensor& tmp) {
+                               const uint64_t* dims, int order) {
     if (a_dev) {
         if (static_cast<int>(a_dev->dims.size()) != order ||
             !std::equal(a_dev->dims.begin(), a_dev->dims.end(), dims))
@@ -73,9 +76,19 @@ const r1_tensor* device_tensor(r1_context* ctx, const double* a_host, const r1_t
         return a_dev;
     }
     if (!a_host) fail(R1_ERR_INVALID_ARGUMENT, "no tensor given");
-    int rc = r1_tensor_from_host(ctx, a_host, dims, order, &tmp.t);
-    if (rc != R1_OK) fail(rc, r1_last_error());
-    return tmp.t;
+    return upload_tensor(ctx, a_host, dims, order);
+}
+
+// Grow-only per-context buffers of the host-buffer entry points: the flat
+// factors (nf) then the blocks (nb).
+struct IoBuffers {
+    double* factors;
+    double* blocks;
+};
+IoBuffers io_buffers(r1_context* ctx, uint64_t nf, uint64_t nb) {
+    const uint64_t nfa = (nf + 31) & ~uint64_t(31);
+    ctx->ws_io.ensure((nfa + nb + 32) * sizeof(double));
+    return {ctx->ws_io.as<double>(), ctx->ws_io.as<double>() + nfa};
 }
 
 }  // namespace
@@ -160,6 +173,7 @@ int r1_context_destroy(r1_context* ctx) {
 
 int r1_context_set_stream(r1_context* ctx, void* s) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
     });
@@ -167,6 +181,7 @@ int r1_context_set_stream(r1_context* ctx, void* s) {
 
 int r1_context_synchronize(r1_context* ctx) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -174,6 +189,7 @@ int r1_context_synchronize(r1_context* ctx) {
 
 int r1_context_launch_count(const r1_context* ctx, uint64_t* count) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         *count = ctx->launches;
     });
@@ -182,6 +198,7 @@ int r1_context_launch_count(const r1_context* ctx, uint64_t* count) {
 // ---------------------------------------------------------------- tensors --
 int r1_tensor_create(r1_context* ctx, const uint64_t* dims, int order, r1_tensor** out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         check_dims(dims, order, "r1_tensor_create");
         auto* t = new r1_tensor();
@@ -203,10 +220,10 @@ int r1_tensor_create(r1_context* ctx, const uint64_t* dims, int order, r1_tensor
 int r1_tensor_from_host(r1_context* ctx, const double* host, const uint64_t* dims, int order,
                         r1_tensor** out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         int rc = r1_tensor_create(ctx, dims, order, out);
         if (rc != R1_OK) fail(rc, g_last_error);
-        R1_CUDA(cudaMemcpyAsync((*out)->dev, host, (*out)->numel * sizeof(double),
-                                cudaMemcpyHostToDevice, ctx->stream));
+        h2d_bytes(ctx, (*out)->dev, host, (*out)->numel * sizeof(double));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -214,6 +231,7 @@ int r1_tensor_from_host(r1_context* ctx, const double* host, const uint64_t* dim
 int r1_tensor_wrap_device(r1_context* ctx, const double* dev, const uint64_t* dims, int order,
                           r1_tensor** out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         check_dims(dims, order, "r1_tensor_wrap_device");
         if (reinterpret_cast<uintptr_t>(dev) % 16 != 0)
@@ -230,14 +248,16 @@ int r1_tensor_wrap_device(r1_context* ctx, const double* dev, const uint64_t* di
 
 int r1_tensor_copy_from_host(r1_context* ctx, r1_tensor* t, const double* host) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
-        R1_CUDA(cudaMemcpyAsync(t->dev, host, t->numel * sizeof(double), cudaMemcpyHostToDevice,
-                                ctx->stream));
+        if (!t || !host) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        h2d_bytes(ctx, t->dev, host, t->numel * sizeof(double));
     });
 }
 
 int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         if (!t || !host) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaMemcpyAsync(host, t->dev, t->numel * sizeof(double), cudaMemcpyDeviceToHost,
@@ -249,13 +269,13 @@ int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host) {
 // frobenius_norm (tensor.cpp:240-244), deterministic fixed-order device sum.
 int r1_tensor_frobenius(r1_context* ctx, const r1_tensor* t, double* out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         if (!t || !out) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
-        DeviceBuffer b;
-        b.ensure(64);
-        sumsq_device(ctx, t->dev, t->numel, b.as<double>());
+        const IoBuffers io = io_buffers(ctx, 0, 8);
+        sumsq_device(ctx, t->dev, t->numel, io.blocks);
         double h = 0.0;
-        R1_CUDA(cudaMemcpyAsync(&h, b.ptr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(&h, io.blocks, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
         *out = std::sqrt(h);
     });
@@ -280,6 +300,7 @@ uint64_t r1_blocks_numel(const uint64_t* dims, int order) { return blocks_numel(
 int r1_build_j_device(r1_context* ctx, const r1_tensor* a, const double* factors_dev,
                       double* blocks_dev, double* fro2_dev) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         if (!a) fail(R1_ERR_INVALID_ARGUMENT, "null tensor");
         const int order = static_cast<int>(a->dims.size());
@@ -292,6 +313,7 @@ int r1_build_j_device(r1_context* ctx, const r1_tensor* a, const double* factors
 int r1_build_j(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
                const uint64_t* dims, int order, const double* factors_host, double* blocks_host) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         if (order < 2) fail(R1_ERR_INVALID_ARGUMENT, "build_j: tensor order must be >= 2");
         check_dims(dims, order, "build_j");
@@ -300,18 +322,15 @@ int r1_build_j(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
             for (int k = 0; k < order; ++k) all[k] = k;
             check_unit_nonzero(dims, order, factors_host, all, order);
         }
-        TempTensor tmp;
-        const r1_tensor* t = device_tensor(ctx, a_host, a_dev, dims, order, tmp);
+        const r1_tensor* t = device_tensor(ctx, a_host, a_dev, dims, order);
         uint64_t nf = 0;
         for (int k = 0; k < order; ++k) nf += dims[k];
         const uint64_t nb = blocks_numel(dims, order);
-        DeviceBuffer f, b;
-        f.ensure(nf * sizeof(double));
-        b.ensure(nb * sizeof(double));
-        R1_CUDA(cudaMemcpyAsync(f.ptr, factors_host, nf * sizeof(double), cudaMemcpyHostToDevice,
-                                ctx->stream));
-        sweep_blocks(ctx, t->dev, dims, order, f.as<double>(), b.as<double>());
-        R1_CUDA(cudaMemcpyAsync(blocks_host, b.ptr, nb * sizeof(double), cudaMemcpyDeviceToHost,
+        const IoBuffers io = io_buffers(ctx, nf, nb);
+        R1_CUDA(cudaMemcpyAsync(io.factors, factors_host, nf * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        sweep_blocks(ctx, t->dev, dims, order, io.factors, io.blocks);
+        R1_CUDA(cudaMemcpyAsync(blocks_host, io.blocks, nb * sizeof(double), cudaMemcpyDeviceToHost,
                                 ctx->stream));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -321,6 +340,7 @@ int r1_build_block(r1_context* ctx, const double* a_host, const r1_tensor* a_dev
                    const uint64_t* dims, int order, const double* factors_host, int m, int n,
                    double* block_host) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         if (order < 2) fail(R1_ERR_INVALID_ARGUMENT, "build_block: tensor order must be >= 2");
         if (m == n) fail(R1_ERR_INVALID_ARGUMENT, "build_block: block modes must differ");
@@ -331,22 +351,18 @@ int r1_build_block(r1_context* ctx, const double* a_host, const r1_tensor* a_dev
         for (int k = 0; k < order; ++k)
             if (k != m && k != n) modes[nm++] = k;
         check_unit_nonzero(dims, order, factors_host, modes, nm);
-        TempTensor tmp;
-        const r1_tensor* t = device_tensor(ctx, a_host, a_dev, dims, order, tmp);
+        const r1_tensor* t = device_tensor(ctx, a_host, a_dev, dims, order);
         uint64_t nf = 0;
         for (int k = 0; k < order; ++k) nf += dims[k];
-        // Factors of the two kept modes never enter the block; a unit placeholder
-        // keeps the shared sweep's validation-free device path well defined.
-        std::vector<double> fac(factors_host, factors_host + nf);
+        // Factors of the two kept modes never enter block (m, n); the other
+        // blocks of the shared sweep are computed and dropped.
         const uint64_t nb = blocks_numel(dims, order);
-        DeviceBuffer f, b;
-        f.ensure(nf * sizeof(double));
-        b.ensure(nb * sizeof(double));
-        R1_CUDA(cudaMemcpyAsync(f.ptr, fac.data(), nf * sizeof(double), cudaMemcpyHostToDevice,
-                                ctx->stream));
-        sweep_blocks(ctx, t->dev, dims, order, f.as<double>(), b.as<double>());
+        const IoBuffers io = io_buffers(ctx, nf, nb);
+        R1_CUDA(cudaMemcpyAsync(io.factors, factors_host, nf * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        sweep_blocks(ctx, t->dev, dims, order, io.factors, io.blocks);
         const uint64_t off = block_offset(dims, order, m, n);
-        R1_CUDA(cudaMemcpyAsync(block_host, b.as<double>() + off, dims[m] * dims[n] * sizeof(double),
+        R1_CUDA(cudaMemcpyAsync(block_host, io.blocks + off, dims[m] * dims[n] * sizeof(double),
                                 cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -355,6 +371,7 @@ int r1_build_block(r1_context* ctx, const double* a_host, const r1_tensor* a_dev
 int r1_block_matvec_device(r1_context* ctx, const uint64_t* dims, int order,
                            const double* blocks_dev, const double* x_dev, double* y_dev) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         block_matvec(ctx, dims, order, blocks_dev, x_dev, y_dev);
     });
@@ -364,6 +381,7 @@ int r1_block_matvec_device(r1_context* ctx, const uint64_t* dims, int order,
 // top-level sweep kernel into a device buffer of 3*ncta uint64 (NULL: off).
 int r1x_set_sweep_trace(r1_context* ctx, void* dev) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         ctx->dbg_sweep_trace = static_cast<unsigned long long*>(dev);
     });
@@ -374,6 +392,7 @@ int r1x_set_sweep_trace(r1_context* ctx, void* dev) {
 // milliseconds and the number of timed launches since the last query.
 int r1x_time_kernels(r1_context* ctx, int enable) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         ctx->time_kernels = enable != 0;
     });
@@ -381,6 +400,7 @@ int r1x_time_kernels(r1_context* ctx, int enable) {
 
 int r1x_kernel_time(r1_context* ctx, double* ms, uint64_t* launches) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
         double total = 0.0;
@@ -400,6 +420,7 @@ int r1x_kernel_time(r1_context* ctx, double* ms, uint64_t* launches) {
 // Test/diagnostic hook (not in the public header): the top-level sweep plan.
 int r1x_sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* info) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         bind(ctx);
         sweep_plan_info(ctx, dims, order, info);
     });

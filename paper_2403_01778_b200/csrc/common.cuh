@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -137,6 +139,40 @@ struct PinnedBuffer {
 
 struct SweepPlan;  // sweep.cu
 
+// Per-context pinned staging lanes for pageable host -> device copies (host_io.cu).
+constexpr int kStageLanes = 8;
+struct HostStaging {
+    struct Lane {
+        cudaStream_t stream = nullptr;
+        void* buf[2] = {nullptr, nullptr};
+        cudaEvent_t done[2] = {nullptr, nullptr};
+        cudaEvent_t joined = nullptr;
+    };
+    Lane lane[kStageLanes];
+    bool ready = false;
+    void ensure(int device);
+    HostStaging() = default;
+    HostStaging(const HostStaging&) = delete;
+    HostStaging& operator=(const HostStaging&) = delete;
+    ~HostStaging();
+};
+
+// Process-wide lock for the caches keyed by context (plans, work sets,
+// handles): lookups and inserts only; the objects themselves belong to one
+// context, whose calls are serialised by the context's own mutex.
+std::mutex& cache_mutex();
+
+// Runs `f` (kernel attribute setup) once per (key, device), under the cache
+// lock so a concurrent launcher on the same device waits until it is done.
+std::set<std::pair<const void*, int>>& configured_set();
+template <typename F>
+void configure_once(const void* key, int device, F&& f) {
+    std::lock_guard<std::mutex> g(cache_mutex());
+    if (configured_set().count({key, device})) return;
+    f();
+    configured_set().insert({key, device});
+}
+
 }  // namespace r1
 
 struct r1_tensor {
@@ -164,6 +200,14 @@ struct r1_context {
     r1::DeviceBuffer ws_rqi;
     r1::DeviceBuffer ws_small;   // factors, scalars, flags
     r1::PinnedBuffer pinned;     // small host staging
+    // host-buffer entry points (host_io.cu): device copy of the caller's
+    // tensor, its view, factor / block buffers, pinned staging lanes
+    r1::DeviceBuffer ws_upload;
+    r1::DeviceBuffer ws_io;
+    r1_tensor upload_view;
+    r1::HostStaging staging;
+    // calls on one context are serialised (SURVEY §8b threading contract)
+    std::recursive_mutex mu;
     std::map<std::vector<uint64_t>, std::shared_ptr<r1::SweepPlan>> plans;
 };
 
@@ -201,7 +245,25 @@ inline uint64_t block_offset(const uint64_t* dims, int order, int m, int n) {
     return s;
 }
 
+// Serialises the calls on one context (null-safe; the entry point reports the
+// null context itself).
+struct CtxLock {
+    r1_context* c;
+    explicit CtxLock(r1_context* ctx) : c(ctx) {
+        if (c) c->mu.lock();
+    }
+    explicit CtxLock(const r1_context* ctx) : CtxLock(const_cast<r1_context*>(ctx)) {}
+    ~CtxLock() {
+        if (c) c->mu.unlock();
+    }
+    CtxLock(const CtxLock&) = delete;
+    CtxLock& operator=(const CtxLock&) = delete;
+};
+
 // --------------------------------------------------------- component APIs --
+// host_io.cu
+void h2d_bytes(r1_context* ctx, void* dst, const void* src, size_t bytes);
+const r1_tensor* upload_tensor(r1_context* ctx, const double* host, const uint64_t* dims, int order);
 // sweep.cu
 void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int order,
                   const double* factors_dev, double* blocks_dev);

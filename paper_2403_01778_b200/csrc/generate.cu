@@ -188,6 +188,7 @@ extern "C" {
 int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
                        const uint64_t* global_dims, int order, uint64_t first) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !t) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         if (cfg < 1 || cfg > 5) fail(R1_ERR_INVALID_ARGUMENT, "unknown config");
@@ -269,6 +270,7 @@ int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
 // the tensor's dims): "gaussian" | "exp" | "arcsin" | "tan".
 int r1_generate(r1_context* ctx, r1_tensor* t, const char* name, uint64_t seed) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !t || !name) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         const std::string nm(name);

@@ -115,6 +115,7 @@ extern "C" {
 int r1_rank_one_subtract(r1_context* ctx, r1_tensor* t, double lambda, const double* factors_host,
                          double* norm_out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !t) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         uint64_t n = 0;
@@ -137,6 +138,7 @@ int r1_rank_one_subtract(r1_context* ctx, r1_tensor* t, double lambda, const dou
 int r1_greedy_rank_r(r1_context* ctx, const r1_tensor* a, uint64_t r, const char* solver,
                      const r1_solve_options* opts, r1_greedy_report* rep) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !a || !opts || !rep || !solver) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         // greedy.cpp:9-12

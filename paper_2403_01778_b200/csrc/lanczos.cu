@@ -1169,9 +1169,12 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
         const int64_t base_d = 14 * ld + ld * R + 32 * ld + n + R;
         const int64_t with_s = base_d + R * n;
         constexpr int64_t cap = 215 * 1024 / 8;
-        static int small_state = -1;  // -1 unknown, 0 unavailable, 1 configured
-        if (small_state < 0) {
-            small_state = 0;
+        // capability probe once per device: can a 16-CTA cluster with the full
+        // shared-memory budget be resident?
+        static std::map<int, int> small_states;
+        int small_state = 0;
+        configure_once(reinterpret_cast<const void*>(lanczos_cluster_kernel), ctx->device, [&] {
+            int st = 0;
             if (cudaFuncSetAttribute(lanczos_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                     cudaSuccess &&
                 cudaFuncSetAttribute(lanczos_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1190,9 +1193,14 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
                 int clusters = 0;
                 if (cudaOccupancyMaxActiveClusters(&clusters, lanczos_cluster_kernel, &q) == cudaSuccess &&
                     clusters >= 1)
-                    small_state = 1;
+                    st = 1;
             }
             cudaGetLastError();
+            small_states[ctx->device] = st;
+        });
+        {
+            std::lock_guard<std::mutex> g(cache_mutex());
+            small_state = small_states[ctx->device];
         }
         if (small_state == 1 && base_d <= cap) {
             const int s_in = with_s <= cap ? 1 : 0;
@@ -1216,12 +1224,11 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
             return;
         }
     }
-    static int configured = -1;
-    if (configured != ctx->device) {
+    configure_once(reinterpret_cast<const void*>(lanczos_kernel), ctx->device, [&] {
         R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kEigDynSmem)));
-        configured = ctx->device;
-    }
+        R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    });
     int per_sm = 0;
     R1_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_kernel, kEigThreads,
                                                           kEigDynSmem));
@@ -1233,11 +1240,6 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     if (cl_size > 1 && !gs) {
         // the whole Lanczos run on ONE thread-block cluster: cluster barriers
         // instead of cooperative grid syncs
-        static int cl_configured = -1;
-        if (cl_configured != ctx->device) {
-            R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            cl_configured = ctx->device;
-        }
         a.cluster = 1;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(cl_size);
@@ -1270,6 +1272,7 @@ std::map<PlanKey, std::shared_ptr<EigPlan>>& eig_plans() {
 }  // namespace
 
 void forget_eig_plans(r1_context* ctx) {
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& m = eig_plans();
     for (auto it = m.begin(); it != m.end();)
         if (it->first.first == ctx)
@@ -1286,10 +1289,16 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
                 const double* x0, double* value_dev, double* vec_dev, int* info_host,
                 double* stats_host, bool solver_chain) {
     if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "eig: unsupported order");
-    auto& P = eig_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
-    if (!P) {
-        P = std::make_shared<EigPlan>();
-        blockop_layout(P->op, dims, order, &P->coldot_n, &P->rowpart_n, int64_t(1) << 40);
+    std::shared_ptr<EigPlan> P;
+    {
+        std::lock_guard<std::mutex> cache_lock(cache_mutex());
+        auto& slot = eig_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
+        if (!slot) {
+            slot = std::make_shared<EigPlan>();
+            blockop_layout(slot->op, dims, order, &slot->coldot_n, &slot->rowpart_n,
+                           int64_t(1) << 40);
+        }
+        P = slot;
     }
     P->op.blocks = blocks;
     P->op.dense = nullptr;
@@ -1299,11 +1308,16 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
 // Same on a dense symmetric n x n matrix S (device, column-major).
 void eig_dense(r1_context* ctx, int64_t n, const double* S, const double* x0, double* value_dev,
                double* vec_dev, int* info_host, double* stats_host) {
-    auto& P = eig_plans()[{ctx, std::vector<uint64_t>{0, static_cast<uint64_t>(n)}}];
-    if (!P) {
-        P = std::make_shared<EigPlan>();
-        denseop_layout(P->op, n, &P->rowpart_n);
-        P->coldot_n = 0;
+    std::shared_ptr<EigPlan> P;
+    {
+        std::lock_guard<std::mutex> cache_lock(cache_mutex());
+        auto& slot = eig_plans()[{ctx, std::vector<uint64_t>{0, static_cast<uint64_t>(n)}}];
+        if (!slot) {
+            slot = std::make_shared<EigPlan>();
+            denseop_layout(slot->op, n, &slot->rowpart_n);
+            slot->coldot_n = 0;
+        }
+        P = slot;
     }
     P->op.dense = S;
     P->op.blocks = nullptr;

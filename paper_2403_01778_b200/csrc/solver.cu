@@ -179,6 +179,7 @@ std::map<std::pair<r1_context*, std::vector<uint64_t>>, std::shared_ptr<Work>>& 
 Work& work_for(r1_context* ctx, const r1_tensor* a, bool dense) {
     std::vector<uint64_t> key = a->dims;
     key.push_back(dense ? 1 : 0);
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& w = work_cache()[{ctx, key}];
     if (!w) w = std::make_shared<Work>(ctx, a, dense);
     w->A = a;
@@ -562,6 +563,7 @@ std::vector<double> initial_factors(const r1_tensor* a, const r1_solve_options& 
 }  // namespace
 
 void forget_solver_work(r1_context* ctx) {
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& m = work_cache();
     for (auto it = m.begin(); it != m.end();)
         if (it->first.first == ctx)
@@ -579,6 +581,7 @@ extern "C" {
 int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
              const r1_solve_options* opts, r1_solve_report* report) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         const std::string alg = algorithm ? algorithm : "";
@@ -634,6 +637,7 @@ int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
 int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
                          const double* x0_dev, double* value_dev, double* vec_dev) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         eig_blocks(ctx, dims, order, blocks_dev, x0_dev, value_dev, vec_dev, nullptr, nullptr);
@@ -644,6 +648,7 @@ int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const
 int r1x_eig_blocks_info(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
                         double* value, double* vec, int* info, double* stats) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         const uint64_t nb = blocks_numel(dims, order);
@@ -666,6 +671,7 @@ int r1x_eig_blocks_info(r1_context* ctx, const uint64_t* dims, int order, const 
 int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_host, double* value,
                                    double* vec) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         if (n <= 0) fail(R1_ERR_INVALID_ARGUMENT, "largest_magnitude_eigenpair: empty matrix");
@@ -695,6 +701,7 @@ int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_h
 int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host, const double* x_host,
                               double* y_host, int* accepted) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         if (n <= 0) fail(R1_ERR_INVALID_ARGUMENT, "rayleigh_quotient_step: size mismatch");
@@ -718,6 +725,7 @@ int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host, 
 int r1_scf_stopping_value(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
                           const double* x_host, double lambda, double* out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         const uint64_t nb = blocks_numel(dims, order);
@@ -748,6 +756,7 @@ int r1_scf_stopping_value(r1_context* ctx, const uint64_t* dims, int order, cons
 int r1_kkt_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
                        const double* factors_host, double* out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         const uint64_t nb = blocks_numel(dims, order);
@@ -796,6 +805,7 @@ int r1_kkt_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const d
 int r1_kkt_report(r1_context* ctx, const double* a_host, const r1_tensor* a_dev, const uint64_t* dims,
                   int order, const double* factors_host, double* out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         const uint64_t nb = blocks_numel(dims, order);
         std::vector<double> blocks(nb);

@@ -20,7 +20,6 @@
 #include "blockmv.cuh"
 #include "solver_ops.cuh"
 
-#include <cusolverDn.h>
 
 #include <cmath>
 #include <cstdlib>
@@ -248,54 +247,6 @@ __global__ void bump_kernel(double* __restrict__ shifts, const double* __restric
     shifts[1] = rho != 0.0 ? rho * (1.0 + 1e-10) : 1e-10 * fmax(sqrt(fro2[0]), 1e-300);
 }
 
-// max|eig(D)| / min|eig(D)| over LAPACK-format BK pivot blocks (lower):
-// ipiv[k] > 0: 1x1; ipiv[k] = ipiv[k+1] < 0: 2x2 at (k,k),(k+1,k),(k+1,k+1).
-__global__ void diag_condition_kernel(const double* __restrict__ W, const int* __restrict__ ipiv,
-                                      int64_t n, const int* __restrict__ info,
-                                      double* __restrict__ cond) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (info[0] != 0) {
-        cond[0] = INFINITY;
-        return;
-    }
-    double lo = INFINITY, hi = 0.0;
-    int64_t k = 0;
-    while (k < n) {
-        if (ipiv[k] > 0) {
-            const double m = fabs(W[k + k * n]);
-            lo = fmin(lo, m);
-            hi = fmax(hi, m);
-            ++k;
-        } else {
-            const double a = W[k + k * n], c = W[(k + 1) + (k + 1) * n], bb = W[(k + 1) + k * n];
-            const double mid = 0.5 * (a + c);
-            const double rad = hypot(0.5 * (a - c), bb);
-            const double e1 = fabs(mid + rad), e2 = fabs(mid - rad);
-            lo = fmin(lo, fmin(e1, e2));
-            hi = fmax(hi, fmax(e1, e2));
-            k += 2;
-        }
-    }
-    cond[0] = lo == 0.0 ? INFINITY : hi / lo;
-}
-
-__global__ void ipiv64_kernel(const int* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[i] = in[i];
-}
-
-__global__ void normalize_check_kernel(double* __restrict__ y, int64_t n, int* __restrict__ ok) {
-    __shared__ double sh[32];
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(y[i], y[i], s);
-    const double nrm = sqrt(block_reduce_sum(s, sh));
-    const bool good = isfinite(nrm) && nrm != 0.0;
-    if (good)
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] /= nrm;
-    if (threadIdx.x == 0) ok[0] = good ? 1 : 0;
-}
-
 Dims make_dims(const uint64_t* dims, int order) {
     Dims dm{};
     dm.d = order;
@@ -305,15 +256,9 @@ Dims make_dims(const uint64_t* dims, int order) {
 }
 
 struct SolverHandle {
-    cusolverDnHandle_t h = nullptr;
-    DeviceBuffer work, ipiv64, dwork, dop;  // RQI / dense-assembly scratch, reused
-    DeviceBuffer dense;                     // dense J for r1_rqi_blocks_device
-    DescCache<BlockOp> dops;                // block-operator descriptors (dense assembly)
-    std::vector<char> hwork;
-    std::vector<uint64_t> dop_dims;
-    ~SolverHandle() {
-        if (h) cusolverDnDestroy(h);
-    }
+    DeviceBuffer work;         // Bunch-Kaufman workspace, reused
+    DeviceBuffer dense;        // dense J for r1_rqi_blocks_device
+    DescCache<BlockOp> dops;   // block-operator descriptors (dense assembly)
 };
 
 std::map<r1_context*, std::shared_ptr<SolverHandle>>& solver_handles() {
@@ -322,25 +267,18 @@ std::map<r1_context*, std::shared_ptr<SolverHandle>>& solver_handles() {
 }
 
 SolverHandle& handle_state(r1_context* ctx) {
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& H = solver_handles()[ctx];
     if (!H) H = std::make_shared<SolverHandle>();
     return *H;
 }
 
-cusolverDnHandle_t solver_handle(r1_context* ctx) {
-    SolverHandle& H = handle_state(ctx);
-    if (!H.h && cusolverDnCreate(&H.h) != CUSOLVER_STATUS_SUCCESS) {
-        H.h = nullptr;
-        fail(R1_ERR_CUDA, "cusolverDnCreate failed");
-    }
-    if (cusolverDnSetStream(H.h, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
-        fail(R1_ERR_CUDA, "cusolverDnSetStream failed");
-    return H.h;
-}
-
 }  // namespace
 
-void forget_solver_handles(r1_context* ctx) { solver_handles().erase(ctx); }
+void forget_solver_handles(r1_context* ctx) {
+    std::lock_guard<std::mutex> cache_lock(cache_mutex());
+    solver_handles().erase(ctx);
+}
 
 void split_stack(r1_context* ctx, const uint64_t* dims, int order, const double* x, double* u,
                  double* xhat, int* flags_dev) {
@@ -397,89 +335,17 @@ void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const d
     check_launch(ctx, "dense_kernel");
 }
 
-// One RQI step on the dense symmetric S (device, n x n, column-major) and x
-// (device).  Returns true and y (device, unit) when accepted, false for
-// std::nullopt.  Synchronous (the accept decision is a host branch).
-bool rqi_step_bk(r1_context* ctx, int64_t n, const double* S, const double* x, double* y);
-
-bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, double* y) {
-    // the hand-written Bunch-Kaufman (bk.cu); R1_RQI_CUSOLVER=1 selects the
-    // cuSOLVER dsytrf path kept for A/B checks
-    static const char* env = std::getenv("R1_RQI_CUSOLVER");
-    if (!(env && std::atoi(env) != 0)) return rqi_step_bk(ctx, n, S, x, y);
-    cusolverDnHandle_t h = solver_handle(ctx);
-    const size_t nn = static_cast<size_t>(n) * n;
-    ctx->ws_rqi.ensure((nn + 4 * n + 128) * sizeof(double));
-    double* W = ctx->ws_rqi.as<double>();
-    double* scal = W + nn;  // [0] rho, [1] bumped, [2] cond, [3] fro(S)^2 ...
-    int* ipiv = reinterpret_cast<int*>(scal + 16);
-    int* info = ipiv + n + 8;
-    int lwork = 0;
-    if (cusolverDnDsytrf_bufferSize(h, static_cast<int>(n), W, static_cast<int>(n), &lwork) !=
-        CUSOLVER_STATUS_SUCCESS)
-        fail(R1_ERR_CUDA, "cusolverDnDsytrf_bufferSize failed");
-    SolverHandle& H = handle_state(ctx);
-    DeviceBuffer& work = H.work;
-    DeviceBuffer& ipiv64 = H.ipiv64;
-    work.ensure(std::max<size_t>(1, static_cast<size_t>(lwork)) * sizeof(double));
-    ipiv64.ensure(std::max<int64_t>(n, 1) * sizeof(int64_t));
-    // rho = x'Sx (sym_eig.cpp:417-418); ||S||_F only matters when rho == 0
-    double* sx = scal + 16 + (n + 16) / 2 + 8;  // after ipiv/info (ints)
-    dense_matvec_kernel<<<dense_matvec_grid(n, ctx->num_sms), 256, 0, ctx->stream>>>(S, x, n, sx);
-    check_launch(ctx, "dense_matvec_kernel");
-    dot_device(ctx, x, sx, static_cast<uint64_t>(n), scal);
-    sumsq_device(ctx, S, nn, scal + 3);
-    bump_kernel<<<1, 1, 0, ctx->stream>>>(scal, scal + 3);
-    check_launch(ctx, "bump_kernel");
-    const int g = static_cast<int>(std::min<size_t>((nn + 255) / 256, ctx->num_sms * 16));
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        shift_copy_kernel<<<std::max(g, 1), 256, 0, ctx->stream>>>(S, W, n, scal + attempt);
-        check_launch(ctx, "shift_copy_kernel");
-        if (cusolverDnDsytrf(h, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), W, static_cast<int>(n),
-                             ipiv, work.as<double>(), lwork, info) != CUSOLVER_STATUS_SUCCESS)
-            fail(R1_ERR_CUDA, "cusolverDnDsytrf failed");
-        count_launch(ctx);
-        diag_condition_kernel<<<1, 32, 0, ctx->stream>>>(W, ipiv, n, info, scal + 2);
-        check_launch(ctx, "diag_condition_kernel");
-        double cond = 0.0;
-        R1_CUDA(cudaMemcpyAsync(&cond, scal + 2, sizeof(double), cudaMemcpyDeviceToHost,
-                                ctx->stream));
-        R1_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (!(cond <= 1e14)) continue;  // singular or ill-conditioned shift
-        R1_CUDA(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-        ipiv64_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 64))), 256, 0,
-                        ctx->stream>>>(ipiv, ipiv64.as<int64_t>(), n);
-        check_launch(ctx, "ipiv64_kernel");
-        size_t dws = 0, hws = 0;
-        if (cusolverDnXsytrs_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, W, n,
-                                        ipiv64.as<int64_t>(), CUDA_R_64F, y, n, &dws, &hws) !=
-            CUSOLVER_STATUS_SUCCESS)
-            fail(R1_ERR_CUDA, "cusolverDnXsytrs_bufferSize failed");
-        H.dwork.ensure(std::max<size_t>(dws, 16));
-        if (H.hwork.size() < std::max<size_t>(hws, 16)) H.hwork.resize(std::max<size_t>(hws, 16));
-        if (cusolverDnXsytrs(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, W, n, ipiv64.as<int64_t>(),
-                             CUDA_R_64F, y, n, H.dwork.ptr, dws, H.hwork.data(), hws, info) !=
-            CUSOLVER_STATUS_SUCCESS)
-            fail(R1_ERR_CUDA, "cusolverDnXsytrs failed");
-        count_launch(ctx);
-        normalize_check_kernel<<<1, kOpsThreads, 0, ctx->stream>>>(y, n, info + 1);
-        check_launch(ctx, "normalize_check_kernel");
-        int ok = 0;
-        R1_CUDA(cudaMemcpyAsync(&ok, info + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        R1_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (ok) return true;
-    }
-    return false;
-}
-
 size_t bk_workspace_bytes(int64_t n, int num_sms);
 void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev);
 void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const double* x, double* y,
               int* ok_dev);
 
-// rayleigh_quotient_step (sym_eig.cpp:411-438) on the hand-written
-// Bunch-Kaufman: rho = x'Sx, attempt(rho), then attempt(bumped) once.
-bool rqi_step_bk(r1_context* ctx, int64_t n, const double* S, const double* x, double* y) {
+// One RQI step on the dense symmetric S (device, n x n, column-major) and x
+// (device): rayleigh_quotient_step (sym_eig.cpp:411-438) on the hand-written
+// Bunch-Kaufman (bk.cu): rho = x'Sx, attempt(rho), then attempt(bumped) once.
+// Returns true and y (device, unit) when accepted, false for std::nullopt.
+// Synchronous (the accept decision is a host branch).
+bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, double* y) {
     const size_t nn = static_cast<size_t>(n) * n;
     ctx->ws_rqi.ensure((nn + 2 * n + 128) * sizeof(double));
     double* W = ctx->ws_rqi.as<double>();
@@ -525,6 +391,7 @@ extern "C" {
 int r1_rqi_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
                          const double* x_dev, double* y_dev, int* accepted) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !dims || !accepted) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         int64_t n = 0;

@@ -1430,26 +1430,23 @@ CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t 
 
 template <int NRA, int NCB, int STAGES, bool TMA>
 void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const CUtensorMap& m) {
-    static int configured_device = -1;  // attribute is per function (and device)
     auto kern = sweep3_kernel<NRA, NCB, STAGES, TMA>;
-    if (configured_device != ctx->device) {
+    // L.smem never exceeds kSmemBudget: set the maximum once per device
+    configure_once(reinterpret_cast<const void*>(kern), ctx->device, [&] {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(L.smem)));
-        configured_device = ctx->device;
-    }
+                                     static_cast<int>(kSmemBudget)));
+    });
     kern<<<L.ncta, kThreads, L.smem, ctx->stream>>>(a, m);
     check_launch(ctx, "sweep3_kernel");
 }
 
 template <int NRA, bool SR, int KO, int NCB = kBoxNCB, int NWC = kBoxNWC>
 void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
-    static int configured_device = -1;
     auto kern = sweep3_box_kernel<NRA, NCB, NWC, SR, KO>;
-    if (configured_device != ctx->device) {
+    configure_once(reinterpret_cast<const void*>(kern), ctx->device, [&] {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBudget)));
-        configured_device = ctx->device;
-    }
+    });
     BoxMaps maps;
     const int64_t rem0 = L.MI0 - static_cast<int64_t>(L.G0 - 1) * L.r0;
     const int64_t rem1 = L.MI1 - static_cast<int64_t>(L.G1 - 1) * L.t1;

@@ -63,6 +63,7 @@ extern "C" {
 
 int r1_tensor_read_dt1(r1_context* ctx, const char* path, r1_tensor** out) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !path || !out) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         const std::string p(path);
@@ -123,6 +124,7 @@ int r1_tensor_read_dt1(r1_context* ctx, const char* path, r1_tensor** out) {
 
 int r1_tensor_write_dt1(r1_context* ctx, const r1_tensor* t, const char* path) {
     return abi_guard([&] {
+        CtxLock lk_(ctx);
         if (!ctx || !t || !path) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
         R1_CUDA(cudaSetDevice(ctx->device));
         const std::string p(path);
