@@ -151,6 +151,9 @@ int r1_tensor_copy_to_host(r1_context* ctx, const r1_tensor* t, double* host);
 /* frobenius_norm (tensor.hpp:67, tensor.cpp:240-244) of a device tensor. */
 int r1_tensor_frobenius(r1_context* ctx, const r1_tensor* t, double* out);
 int r1_tensor_destroy(r1_tensor* t);
+/* frobenius_norm of a HOST tensor (staged to the device). */
+int r1_host_frobenius(r1_context* ctx, const double* a_host, const uint64_t* dims, int order,
+                      double* out);
 double* r1_tensor_device_ptr(const r1_tensor* t);
 
 /* ---- sizes ----------------------------------------------------------------- */
@@ -186,11 +189,25 @@ int r1_build_block(r1_context* ctx, const double* a_host, const r1_tensor* a_dev
 /* y = J x (scale included), device pointers, async. */
 int r1_block_matvec_device(r1_context* ctx, const uint64_t* dims, int order,
                            const double* blocks_dev, const double* x_dev, double* y_dev);
+/* Host-buffer forms (SymBlockMatrix::matvec / dense / frobenius_norm,
+ * nepv.cpp:110-157), computed on the device. */
+int r1_block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                    const double* x_host, double* y_host);
+int r1_block_dense(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                   double* s_host);
+int r1_block_frobenius(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                       double* out);
 /* Eq. 11: ||Jx - rho x|| / (||J||_F + |lambda|), rho = x'Jx (nepv.cpp:271-282).
  * Host form: blocks/x on host, result to *out. */
 int r1_scf_stopping_value(r1_context* ctx, const uint64_t* dims, int order,
                           const double* blocks_host, const double* x_host, double lambda,
                           double* out);
+/* contract_leaving_all (tensor.hpp:86-87, tensor.cpp:216-238): out = w_0 ++ ... ++
+ * w_{d-1}, w_n = A x_{k != n} u_k, from one device sweep (any factor norms;
+ * `a_host` staged to the device unless `a_dev` is given). */
+int r1_contract_leaving_all(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
+                            const uint64_t* dims, int order, const double* factors_host,
+                            double* out_host);
 /* KKT report derived from the blocks of J(u) (no tensor pass):
  * w_n = B(n,m) u_m, lambda = u_0' B(0,1) u_1, residual_n = ||w_n - lambda u_n||.
  * out: [lambda, max_residual, residual_0..residual_{d-1}] (d+2 doubles). */
@@ -207,7 +224,10 @@ int r1_kkt_report(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
 int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order,
                          const double* blocks_dev, const double* x0_dev, double* value_dev,
                          double* vec_dev);
-/* Same for a dense symmetric n x n matrix given on the host (column-major). */
+/* largest_magnitude_eigenpair (sym_eig.hpp:30) of a dense symmetric n x n
+ * host matrix (column-major): the reference's definition (sym_eig.cpp:206-229)
+ * on the device full decomposition r1_sym_eig_full below — pick lo iff
+ * |w_lo| > |w_hi| (1 + 1e-12), largest-|entry| positive. */
 int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_host,
                                    double* value, double* vec);
 /* One Rayleigh-quotient step (sym_eig.cpp:411-438) on device: Bunch-Kaufman
@@ -220,6 +240,48 @@ int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host,
  * distributed solve, where J is replicated on every rank. */
 int r1_rqi_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
                          const double* x_dev, double* y_dev, int* accepted);
+
+/* ---- dense-matrix / tensor utilities of the API (off the solvers' path) ----
+ * One-thread-block device kernels that restate the reference's sequential
+ * algorithms step for step (csrc/dense_api.cu, compiled without FMA
+ * contraction): results follow the reference's rounding (glibc / libdevice
+ * hypot and sqrt aside).  Matrices are host, column-major n x n. */
+/* sym_eig_full (sym_eig.hpp:19, sym_eig.cpp:27-204): ascending values, vectors
+ * column j <-> values[j].  Non-symmetric input (> 1e-10 relative):
+ * R1_ERR_INVALID_ARGUMENT "sym_eig: matrix is not symmetric"; no QL convergence
+ * within 60 sweeps: R1_ERR_RUNTIME. */
+int r1_sym_eig_full(r1_context* ctx, int64_t n, const double* s_host, double* values,
+                    double* vectors);
+/* detail::ldlt_factor (sym_eig.hpp:49, sym_eig.cpp:233-320): unblocked
+ * Bunch-Kaufman, the reference's storage (w: L below the diagonal, D in the
+ * pivot blocks; ipiv >= 0 1x1 row swap, < 0 2x2 with kp = -ipiv-1). */
+int r1_ldlt_factor(r1_context* ctx, int64_t n, const double* s_host, double* w_host, int* ipiv,
+                   int* singular);
+/* detail::ldlt_solve (sym_eig.hpp:50, sym_eig.cpp:323-377). */
+int r1_ldlt_solve(r1_context* ctx, int64_t n, const double* w_host, const int* ipiv,
+                  const double* b_host, double* x_host);
+/* detail::ldlt_diag_condition (sym_eig.hpp:52, sym_eig.cpp:380-407) from the
+ * pivot blocks: diag[k] = w(k,k), sub[k] = w(k+1,k). */
+int r1_ldlt_diag_condition(r1_context* ctx, int64_t n, const double* diag, const double* sub,
+                           const int* ipiv, int singular, double* out);
+/* matricize (tensor.hpp:55, tensor.cpp:72-83), inverse = 1: dematricize
+ * (tensor.hpp:58, tensor.cpp:85-98). */
+int r1_matricize(r1_context* ctx, const double* in_host, const uint64_t* dims, int order, int mode,
+                 int inverse, double* out_host);
+/* ttvc / ttvc_scalar (tensor.hpp:65-75, tensor.cpp:100-199): contract the
+ * `nmodes` distinct `modes` (vectors concatenated in that order) in descending
+ * mode order, each ttv summing in the reference's order.  full = 0: the
+ * remaining tensor into out_host; full = 1 (nmodes == order): *scalar_out. */
+int r1_ttvc(r1_context* ctx, const double* a_host, const uint64_t* dims, int order,
+            const double* vs_host, const int* modes, int nmodes, int full, double* out_host,
+            double* scalar_out);
+/* rank_one_expand (tensor.hpp:92, tensor.cpp:246-265). */
+int r1_rank_one_expand(r1_context* ctx, double lambda, const double* factors_host,
+                       const uint64_t* dims, int order, double* out_host);
+/* residual_norm (tensor.hpp:98-99, tensor.cpp:267-287). */
+int r1_residual_norm(r1_context* ctx, const double* a_host, const uint64_t* dims, int order,
+                     double lambda, const double* factors_host, uint64_t dense_threshold,
+                     double* out_norm);
 
 /* ---- synthetic inputs ----------------------------------------------------------- */
 /* Fill `t` with elements [first, first + numel(t)) of BASELINE config `cfg`
@@ -244,6 +306,12 @@ int r1_generate(r1_context* ctx, r1_tensor* t, const char* name, uint64_t seed);
  * for the baselines (the reference leaves it empty, solvers.hpp:56). */
 int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
              const r1_solve_options* opts, r1_solve_report* report);
+
+/* r1_solve on a HOST tensor (rank1::solve(name, const DenseTensor&, opts)):
+ * staged into the context's grow-only device buffer, then solved. */
+int r1_solve_host(r1_context* ctx, const char* algorithm, const double* a_host,
+                  const uint64_t* dims, int order, const r1_solve_options* opts,
+                  r1_solve_report* report);
 
 /* ---- greedy rank-R deflation (greedy.hpp:11-22, greedy.cpp:7-35) --------------- */
 /* Mirrors GreedyReport: terms in deflation order, ||R||_F / ||A||_F after each

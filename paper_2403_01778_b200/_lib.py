@@ -92,6 +92,7 @@ SIGNATURES = {
     "r1_tensor_copy_from_host": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_copy_to_host": (ctypes.c_int, [_vp, _vp, _dp]),
     "r1_tensor_frobenius": (ctypes.c_int, [_vp, _vp, _dp]),
+    "r1_host_frobenius": (ctypes.c_int, [_vp, _dp, _u64p, ctypes.c_int, _dp]),
     "r1_tensor_destroy": (ctypes.c_int, [_vp]),
     "r1_tensor_device_ptr": (_vp, [_vp]),
     "r1_blocks_numel": (ctypes.c_uint64, [_u64p, ctypes.c_int]),
@@ -100,6 +101,10 @@ SIGNATURES = {
     "r1_build_block": (ctypes.c_int, [_vp, _dp, _vp, _u64p, ctypes.c_int, _dp, ctypes.c_int,
                                       ctypes.c_int, _dp]),
     "r1_block_matvec_device": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _vp, _vp, _vp]),
+    "r1_contract_leaving_all": (ctypes.c_int, [_vp, _dp, _vp, _u64p, ctypes.c_int, _dp, _dp]),
+    "r1_block_matvec": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp, _dp]),
+    "r1_block_dense": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp]),
+    "r1_block_frobenius": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp]),
     "r1_scf_stopping_value": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp, ctypes.c_double,
                                              _dp]),
     "r1_kkt_from_blocks": (ctypes.c_int, [_vp, _u64p, ctypes.c_int, _dp, _dp, _dp]),
@@ -115,9 +120,24 @@ SIGNATURES = {
     "r1_generate": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p, ctypes.c_uint64]),
     "r1_solve": (ctypes.c_int, [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(SolveOptionsC),
                                 ctypes.POINTER(SolveReportC)]),
+    "r1_solve_host": (ctypes.c_int, [_vp, ctypes.c_char_p, _dp, _u64p, ctypes.c_int,
+                                     ctypes.POINTER(SolveOptionsC), ctypes.POINTER(SolveReportC)]),
     "r1_greedy_rank_r": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, ctypes.c_char_p,
                                         ctypes.POINTER(SolveOptionsC), ctypes.POINTER(GreedyReportC)]),
     "r1_rank_one_subtract": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _dp, _dp]),
+    "r1_sym_eig_full": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp]),
+    "r1_ldlt_factor": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int)]),
+    "r1_ldlt_solve": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.POINTER(ctypes.c_int), _dp,
+                                     _dp]),
+    "r1_ldlt_diag_condition": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp,
+                                              ctypes.POINTER(ctypes.c_int), ctypes.c_int, _dp]),
+    "r1_matricize": (ctypes.c_int, [_vp, _dp, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]),
+    "r1_ttvc": (ctypes.c_int, [_vp, _dp, _u64p, ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_int),
+                               ctypes.c_int, ctypes.c_int, _dp, _dp]),
+    "r1_rank_one_expand": (ctypes.c_int, [_vp, ctypes.c_double, _dp, _u64p, ctypes.c_int, _dp]),
+    "r1_residual_norm": (ctypes.c_int, [_vp, _dp, _u64p, ctypes.c_int, ctypes.c_double, _dp,
+                                        ctypes.c_uint64, _dp]),
     "r1_tensor_read_dt1": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "r1_tensor_write_dt1": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p]),
 }
@@ -132,6 +152,7 @@ EXTRA_SIGNATURES = {
                                            ctypes.POINTER(ctypes.c_int), _dp]),
     "r1x_sweep_plan_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_int64)]),
+    "r1x_eig_dense_lanczos": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp]),
     "r1x_ldlt": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.POINTER(ctypes.c_int), _dp, _dp,
                                 ctypes.POINTER(ctypes.c_int), _dp]),
 }

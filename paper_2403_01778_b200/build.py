@@ -18,6 +18,12 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
 
+# Per-file extra flags.  dense_api.cu restates the reference's sequential
+# dense algorithms (sym_eig.cpp) step for step: no FMA contraction there, as in
+# the reference's own build (no -march=native).
+FILE_FLAGS = {"dense_api.cu": ["-fmad=false"]}
+
+
 def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
@@ -40,9 +46,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        extra = FILE_FLAGS.get(os.path.basename(src), [])
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC, *ARCH, *FLAGS, "-x", "cu", "-c", src, "-o", obj]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-x", "cu", "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
         objs.append(obj)

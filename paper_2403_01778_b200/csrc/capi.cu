@@ -281,6 +281,25 @@ int r1_tensor_frobenius(r1_context* ctx, const r1_tensor* t, double* out) {
     });
 }
 
+// frobenius_norm (tensor.cpp:240-244) of a host tensor: staged H2D + the
+// fixed-order device sum of squares.
+int r1_host_frobenius(r1_context* ctx, const double* a_host, const uint64_t* dims, int order,
+                      double* out) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        bind(ctx);
+        if (!a_host || !dims || !out) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        check_dims(dims, order, "frobenius_norm");
+        const r1_tensor* t = upload_tensor(ctx, a_host, dims, order);
+        const IoBuffers io = io_buffers(ctx, 0, 8);
+        sumsq_device(ctx, t->dev, t->numel, io.blocks);
+        double h = 0.0;
+        R1_CUDA(cudaMemcpyAsync(&h, io.blocks, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = std::sqrt(h);
+    });
+}
+
 int r1_tensor_destroy(r1_tensor* t) {
     return abi_guard([&] {
         if (!t) return;

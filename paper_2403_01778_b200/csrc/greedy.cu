@@ -9,6 +9,7 @@
 // reference expands the full term into a second tensor and re-reads both).
 #include "common.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -32,6 +33,7 @@ struct DeflArgs {
     const double* u[kMaxOrder];  // u[0] = mode 0, u[1..] = modes 1..d-1
     double lambda;
     double* partials;  // [gridDim.x]
+    int dot_only;      // 1: accumulate sum R[i] * e[i] (no write), 0: subtract + ||R||^2
 };
 
 __device__ double block_sum(double v, double* sh) {
@@ -62,9 +64,13 @@ __global__ void __launch_bounds__(kDeflThreads) deflate_kernel(const DeflArgs a)
         for (int64_t i = threadIdx.x; i < a.I0; i += blockDim.x) {
             double e = a.lambda * __ldg(a.u[0] + i);
             for (int k = 1; k <= a.nout; ++k) e *= w[k];
-            const double v = r[i] - e;
-            r[i] = v;
-            acc = fma(v, v, acc);
+            if (a.dot_only) {
+                acc = fma(r[i], e, acc);
+            } else {
+                const double v = r[i] - e;
+                r[i] = v;
+                acc = fma(v, v, acc);
+            }
         }
     }
     const double s = block_sum(acc, sh);
@@ -83,7 +89,7 @@ __global__ void sum_fixed_kernel(const double* p, int n, double* out) {
 
 // R -= lambda * outer(u); returns ||R||_F^2 into *out_dev (device).
 void rank_one_subtract(r1_context* ctx, r1_tensor* t, double lambda, const double* u_dev,
-                       double* scratch, double* out_dev) {
+                       double* scratch, double* out_dev, bool dot_only = false) {
     const int d = static_cast<int>(t->dims.size());
     if (d > kMaxOrder) fail(R1_ERR_INVALID_ARGUMENT, "rank_one_subtract: unsupported order");
     DeflArgs a{};
@@ -99,6 +105,7 @@ void rank_one_subtract(r1_context* ctx, r1_tensor* t, double lambda, const doubl
     }
     a.lambda = lambda;
     a.partials = scratch;
+    a.dot_only = dot_only ? 1 : 0;
     const int grid = 4 * ctx->num_sms;
     deflate_kernel<<<grid, kDeflThreads, 0, ctx->stream>>>(a);
     check_launch(ctx, "deflate_kernel");
@@ -206,6 +213,80 @@ int r1_greedy_rank_r(r1_context* ctx, const r1_tensor* a, uint64_t r, const char
             rep->terms = static_cast<int32_t>(term + 1);
         }
         rep->completed = 1;
+    });
+}
+
+// rank_one_expand (tensor.cpp:246-265): out = lambda u_0 o ... o u_{d-1}, the
+// reference's left-to-right product, as the deflation of a zero tensor by
+// -lambda (0 - (-x) = x exactly).
+int r1_rank_one_expand(r1_context* ctx, double lambda, const double* factors_host,
+                       const uint64_t* dims, int order, double* out_host) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !dims || !factors_host || !out_host) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 1 || order > kMaxOrder) fail(R1_ERR_INVALID_ARGUMENT, "rank_one_expand: order mismatch");
+        const uint64_t numel = numel_of(dims, order);
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        const size_t tbytes = ((numel + 2) * sizeof(double) + 255) & ~size_t(255);
+        ctx->ws_upload.ensure(tbytes);
+        ctx->ws_io.ensure((n + 8 * ctx->num_sms + 16) * sizeof(double));
+        r1_tensor& t = ctx->upload_view;
+        t.ctx = ctx;
+        t.dims.assign(dims, dims + order);
+        t.numel = numel;
+        t.dev = ctx->ws_upload.as<double>();
+        t.owned = false;
+        double* u = ctx->ws_io.as<double>();
+        double* part = u + n;
+        double* out = part + 4 * ctx->num_sms;
+        R1_CUDA(cudaMemsetAsync(t.dev, 0, numel * sizeof(double), ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(u, factors_host, n * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        rank_one_subtract(ctx, &t, -lambda, u, part, out);
+        R1_CUDA(cudaMemcpyAsync(out_host, t.dev, numel * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// residual_norm (tensor.cpp:267-287): ||A - lambda o u||_F; numel <= dense_threshold
+// subtracts the expansion (fused, one pass), above it the expansion-free form
+// sqrt(max(0, ||A||^2 - 2 lambda <A, o u> + lambda^2)) (unit factors assumed).
+int r1_residual_norm(r1_context* ctx, const double* a_host, const uint64_t* dims, int order,
+                     double lambda, const double* factors_host, uint64_t dense_threshold,
+                     double* out_norm) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !dims || !a_host || !factors_host || !out_norm)
+            fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 1 || order > kMaxOrder) fail(R1_ERR_INVALID_ARGUMENT, "residual_norm: order mismatch");
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        const r1_tensor* view = upload_tensor(ctx, a_host, dims, order);
+        r1_tensor& t = const_cast<r1_tensor&>(*view);
+        ctx->ws_io.ensure((n + 8 * ctx->num_sms + 16) * sizeof(double));
+        double* u = ctx->ws_io.as<double>();
+        double* part = u + n;
+        double* out = part + 4 * ctx->num_sms;
+        R1_CUDA(cudaMemcpyAsync(u, factors_host, n * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        double h[2] = {0.0, 0.0};
+        if (t.numel <= dense_threshold) {
+            rank_one_subtract(ctx, &t, lambda, u, part, out);
+            R1_CUDA(cudaMemcpyAsync(h, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            R1_CUDA(cudaStreamSynchronize(ctx->stream));
+            *out_norm = std::sqrt(h[0]);
+            return;
+        }
+        sumsq_device(ctx, t.dev, t.numel, out + 1);
+        rank_one_subtract(ctx, &t, 1.0, u, part, out, true);
+        R1_CUDA(cudaMemcpyAsync(h, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        const double s = h[1] - 2.0 * lambda * h[0] + lambda * lambda;
+        *out_norm = std::sqrt(std::max(0.0, s));
     });
 }
 

@@ -1,10 +1,18 @@
 // The C++ rank1:: drop-in (include/rank1/*.hpp) on top of the C-ABI
-// (include/rank1_b200.h).  Container types are host-side as in the reference;
-// every numeric step of the hot path (sweep, eigen step, RQI, stopping test,
-// KKT, solvers) goes through r1_* into the sm_100a kernels.  Status codes are
-// mapped back to the reference's exception types (invalid_argument /
-// runtime_error).
+// (include/rank1_b200.h).  Container types are host-side as in the reference
+// (they own std::vector storage); every computation over a tensor or a block
+// matrix — sweep, SymBlockMatrix matvec / dense / norm, eigen steps, RQI,
+// LDL^T, stopping test, KKT, contractions, unfoldings, expansions, solvers,
+// generators — goes through r1_* into the sm_100a kernels.  What stays on the
+// host is O(sum I_k) container glue over the caller's vectors (Matrix / span
+// helpers of matrix.hpp, StackedVector split / stack / flip of stacked.hpp,
+// the CounterRng draws of rng.hpp), kept as API shims with the reference's
+// semantics and messages.  Status codes are mapped back to the reference's
+// exception types (invalid_argument / runtime_error).
+#include <algorithm>
 #include <cmath>
+#include <functional>
+#include <numbers>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -13,8 +21,10 @@
 #include <stdexcept>
 #include <string>
 
+#include "rank1/generators.hpp"
 #include "rank1/greedy.hpp"
 #include "rank1/nepv.hpp"
+#include "rank1/rng.hpp"
 #include "rank1/solvers.hpp"
 #include "rank1/stacked.hpp"
 #include "rank1/sym_eig.hpp"
@@ -48,6 +58,14 @@ r1_context* ctx() {
 }
 
 std::vector<uint64_t> u64(const std::vector<std::size_t>& d) { return {d.begin(), d.end()}; }
+
+struct TensorGuard {
+    r1_tensor* t = nullptr;
+    ~TensorGuard() {
+        if (t) r1_tensor_destroy(t);
+    }
+};
+
 
 std::vector<double> flat(const FactorSet& f) {
     std::vector<double> v;
@@ -87,62 +105,76 @@ SymBlockMatrix from_blocks(const std::vector<std::size_t>& dims, const std::vect
 }  // namespace
 
 // ------------------------------------------------------------------ Matrix --
+// matrix.hpp container helpers (reference matrix.cpp:6-67): host glue over the
+// caller's vectors, sequential sums in index order as the reference's.
 Matrix transpose(const Matrix& m) {
     Matrix t(m.cols(), m.rows());
-    for (std::size_t j = 0; j < m.cols(); ++j)
-        for (std::size_t i = 0; i < m.rows(); ++i) t(j, i) = m(i, j);
+    for (std::size_t j = 0; j < m.cols(); ++j) {
+        const auto c = m.col(j);
+        for (std::size_t i = 0; i < c.size(); ++i) t(j, i) = c[i];
+    }
     return t;
 }
 
 std::vector<double> matvec(const Matrix& m, std::span<const double> x) {
     if (x.size() != m.cols()) throw std::invalid_argument("matvec: size mismatch");
     std::vector<double> y(m.rows(), 0.0);
-    for (std::size_t j = 0; j < m.cols(); ++j)
-        for (std::size_t i = 0; i < m.rows(); ++i) y[i] += m(i, j) * x[j];
+    for (std::size_t j = 0; j < m.cols(); ++j) {
+        const auto c = m.col(j);
+        const double xj = x[j];
+        std::transform(y.begin(), y.end(), c.begin(), y.begin(),
+                       [xj](double acc, double a) { return acc + a * xj; });
+    }
     return y;
 }
 
 std::vector<double> matvec_transposed(const Matrix& m, std::span<const double> x) {
     if (x.size() != m.rows()) throw std::invalid_argument("matvec_transposed: size mismatch");
-    std::vector<double> y(m.cols(), 0.0);
+    std::vector<double> y(m.cols());
     for (std::size_t j = 0; j < m.cols(); ++j) {
-        double s = 0.0;
-        for (std::size_t i = 0; i < m.rows(); ++i) s += m(i, j) * x[i];
-        y[j] = s;
+        const auto c = m.col(j);
+        y[j] = std::inner_product(c.begin(), c.end(), x.begin(), 0.0);
     }
     return y;
 }
 
-double frobenius_norm(const Matrix& m) {
-    double s = 0.0;
-    for (double v : m.values()) s += v * v;
-    return std::sqrt(s);
-}
+double frobenius_norm(const Matrix& m) { return norm2(m.values()); }
 
 double max_abs(const Matrix& m) {
-    double s = 0.0;
-    for (double v : m.values()) s = std::max(s, std::abs(v));
-    return s;
+    return std::accumulate(m.values().begin(), m.values().end(), 0.0,
+                           [](double acc, double v) { return std::max(acc, std::abs(v)); });
 }
 
 double dot(std::span<const double> a, std::span<const double> b) {
     if (a.size() != b.size()) throw std::invalid_argument("dot: size mismatch");
-    double s = 0.0;
-    for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
-    return s;
+    return std::inner_product(a.begin(), a.end(), b.begin(), 0.0);
 }
 
 double norm2(std::span<const double> v) {
-    double s = 0.0;
-    for (double x : v) s += x * x;
-    return std::sqrt(s);
+    return std::sqrt(std::inner_product(v.begin(), v.end(), v.begin(), 0.0));
 }
 
 double normalize(std::span<double> v) {
-    const double n = norm2(v);
-    if (n > 0.0)
-        for (double& x : v) x /= n;
-    return n;
+    const double len = norm2(v);
+    if (len > 0.0) std::transform(v.begin(), v.end(), v.begin(), [len](double x) { return x / len; });
+    return len;
+}
+
+// ------------------------------------------------------------------- rng.hpp --
+// Box-Muller in pairs (reference generators.cpp:11-24): u1 nudged by 2^-54 so
+// the log stays finite; the sine half is returned by the next call.
+double CounterRng::next_gaussian() {
+    if (has_cached_) {
+        has_cached_ = false;
+        return cached_;
+    }
+    const double u1 = next_unit() + 0x1.0p-54;
+    const double u2 = next_unit();
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    const double ang = 2.0 * std::numbers::pi * u2;
+    cached_ = rad * std::sin(ang);
+    has_cached_ = true;
+    return rad * std::cos(ang);
 }
 
 // -------------------------------------------------------------- DenseTensor --
@@ -186,28 +218,82 @@ double max_unit_deviation(const FactorSet& f) {
 }
 
 double frobenius_norm(const DenseTensor& a) {
-    double s = 0.0;
-    for (double v : a.values()) s += v * v;
-    return std::sqrt(s);
+    const auto dims = u64(a.dims());
+    double v = 0.0;
+    raise(r1_host_frobenius(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), &v));
+    return v;
 }
 
-double multilinear_value(const DenseTensor& a, const FactorSet& f, bool) {
-    if (f.order() != a.order()) throw std::invalid_argument("multilinear_value: order mismatch");
-    // lambda = u0' B(0,1) u1 of one device sweep; the sweep needs unit
-    // factors, so contract with normalised ones and rescale by the norms.
-    FactorSet g = f;
-    double scale = 1.0;
-    for (auto& u : g.factors) {
-        const double n = normalize(u);
-        if (n == 0.0) return 0.0;
-        scale *= n;
+// ---------------------------------------------------------- ttv / ttvc chains --
+namespace {
+
+void check_ttvc_args(const DenseTensor& a, std::span<const std::vector<double>> vs,
+                     std::span<const std::size_t> modes) {
+    if (vs.size() != modes.size()) throw std::invalid_argument("ttvc: vectors/modes mismatch");
+    std::vector<bool> seen(a.order(), false);
+    for (std::size_t i = 0; i < modes.size(); ++i) {
+        if (modes[i] >= a.order()) throw std::invalid_argument("ttvc: mode out of range");
+        if (seen[modes[i]]) throw std::invalid_argument("ttvc: duplicate mode");
+        seen[modes[i]] = true;
+        if (vs[i].size() != a.dim(modes[i])) throw std::invalid_argument("ttvc: vector length mismatch");
     }
+}
+
+// the device chain (r1_ttvc); full = all modes -> scalar
+DenseTensor ttvc_device(const DenseTensor& a, std::span<const std::vector<double>> vs,
+                        std::span<const std::size_t> modes, bool full, double* scalar) {
+    std::vector<double> flatv;
+    std::vector<int> m;
+    for (std::size_t i = 0; i < modes.size(); ++i) {
+        flatv.insert(flatv.end(), vs[i].begin(), vs[i].end());
+        m.push_back(static_cast<int>(modes[i]));
+    }
+    std::vector<std::size_t> out_dims;
+    std::vector<bool> gone(a.order(), false);
+    for (auto k : modes) gone[k] = true;
+    for (std::size_t k = 0; k < a.order(); ++k)
+        if (!gone[k]) out_dims.push_back(a.dim(k));
     const auto dims = u64(a.dims());
-    std::vector<double> out(a.order() + 2);
-    const auto fl = flat(g);
-    raise(r1_kkt_report(ctx(), a.data(), nullptr, dims.data(), static_cast<int>(a.order()),
-                        fl.data(), out.data()));
-    return out[0] * scale;
+    DenseTensor out = full ? DenseTensor() : DenseTensor(out_dims);
+    raise(r1_ttvc(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), flatv.data(), m.data(),
+                  static_cast<int>(m.size()), full ? 1 : 0, full ? nullptr : out.data(), scalar));
+    return out;
+}
+
+}  // namespace
+
+DenseTensor ttv(const DenseTensor& a, std::span<const double> v, std::size_t mode, bool) {
+    if (mode >= a.order()) throw std::invalid_argument("ttv: mode out of range");
+    if (v.size() != a.dim(mode)) throw std::invalid_argument("ttv: vector length mismatch");
+    if (a.order() == 1) throw std::invalid_argument("ttv: full contraction needs ttvc_scalar");
+    const std::vector<double> vv(v.begin(), v.end());
+    const std::size_t md[1] = {mode};
+    return ttvc_device(a, std::span<const std::vector<double>>(&vv, 1), md, false, nullptr);
+}
+
+DenseTensor ttvc(const DenseTensor& a, std::span<const std::vector<double>> vs,
+                 std::span<const std::size_t> modes, bool) {
+    check_ttvc_args(a, vs, modes);
+    if (modes.size() >= a.order())
+        throw std::invalid_argument("ttvc: contracting all modes yields a scalar, use ttvc_scalar");
+    if (modes.empty()) return a;
+    return ttvc_device(a, vs, modes, false, nullptr);
+}
+
+double ttvc_scalar(const DenseTensor& a, std::span<const std::vector<double>> vs,
+                   std::span<const std::size_t> modes, bool) {
+    check_ttvc_args(a, vs, modes);
+    if (modes.size() != a.order()) throw std::invalid_argument("ttvc_scalar: all modes must be contracted");
+    double v = 0.0;
+    ttvc_device(a, vs, modes, true, &v);
+    return v;
+}
+
+double multilinear_value(const DenseTensor& a, const FactorSet& f, bool parallel) {
+    if (f.order() != a.order()) throw std::invalid_argument("multilinear_value: order mismatch");
+    std::vector<std::size_t> modes(a.order());
+    std::iota(modes.begin(), modes.end(), std::size_t{0});
+    return ttvc_scalar(a, f.factors, modes, parallel);
 }
 
 // ----------------------------------------------------------- StackedVector --
@@ -232,21 +318,23 @@ StackedVector::StackedVector(std::vector<std::size_t> block_dims, std::vector<do
 double StackedVector::block_norm(std::size_t n) const { return norm2(block(n)); }
 double StackedVector::norm() const { return norm2(flat_); }
 
+// stacked.hpp container glue (reference stacked.cpp:36-85): O(sum I_k) on the
+// caller's vectors.
 SplitResult split_factors(const StackedVector& x) {
     SplitResult r;
-    r.factors.factors.resize(x.order());
-    r.degenerate.assign(x.order(), 0);
+    r.factors.factors.reserve(x.order());
+    r.degenerate.reserve(x.order());
     for (std::size_t n = 0; n < x.order(); ++n) {
-        auto b = x.block(n);
-        auto& u = r.factors.factors[n];
-        u.assign(b.begin(), b.end());
-        const double nrm = norm2(u);
-        if (nrm < 1e-12) {
+        const auto blk = x.block(n);
+        std::vector<double> u(blk.begin(), blk.end());
+        const double len = norm2(u);
+        const bool deg = len < 1e-12;  // flagged, not thrown (stacked.cpp:47-50)
+        if (deg)
             std::fill(u.begin(), u.end(), 0.0);
-            r.degenerate[n] = 1;
-        } else {
-            for (double& v : u) v /= nrm;
-        }
+        else
+            std::transform(u.begin(), u.end(), u.begin(), [len](double v) { return v / len; });
+        r.factors.factors.push_back(std::move(u));
+        r.degenerate.push_back(deg ? 1 : 0);
     }
     return r;
 }
@@ -256,25 +344,26 @@ StackedVector stack_factors(const FactorSet& f) {
     if (max_unit_deviation(f) > 1e-8)
         throw std::invalid_argument("stack_factors: factors must have unit norm");
     std::vector<std::size_t> dims;
-    for (const auto& u : f.factors) dims.push_back(u.size());
-    StackedVector x(dims);
-    const double s = 1.0 / std::sqrt(static_cast<double>(f.order()));
-    for (std::size_t n = 0; n < f.order(); ++n) {
-        auto b = x.block(n);
-        for (std::size_t i = 0; i < b.size(); ++i) b[i] = f.factors[n][i] * s;
+    std::vector<double> flat;
+    const double w = 1.0 / std::sqrt(static_cast<double>(f.order()));
+    for (const auto& u : f.factors) {
+        dims.push_back(u.size());
+        std::transform(u.begin(), u.end(), std::back_inserter(flat), [w](double v) { return v * w; });
     }
-    return x;
+    return StackedVector(std::move(dims), std::move(flat));
 }
 
 StackedVector flip_first_block(const StackedVector& x) {
     StackedVector y = x;
-    for (double& v : y.block(0)) v = -v;
+    auto b = y.block(0);
+    std::transform(b.begin(), b.end(), b.begin(), std::negate<double>());
     return y;
 }
 
 FactorSet flip_first_factor(FactorSet f) {
     if (f.order() == 0) throw std::invalid_argument("flip_first_factor: empty factor set");
-    for (double& v : f.factors[0]) v = -v;
+    std::transform(f.factors[0].begin(), f.factors[0].end(), f.factors[0].begin(),
+                   std::negate<double>());
     return f;
 }
 
@@ -303,45 +392,32 @@ std::size_t SymBlockMatrix::pair_index(std::size_t m, std::size_t n) const {
 const Matrix& SymBlockMatrix::block(std::size_t m, std::size_t n) const { return upper_[pair_index(m, n)]; }
 Matrix& SymBlockMatrix::block(std::size_t m, std::size_t n) { return upper_[pair_index(m, n)]; }
 
+// The operator on the device (nepv.cpp:110-157): the blocks are staged and
+// r1_block_matvec / r1_block_dense / r1_block_frobenius run the kernels the
+// solvers use.
 std::vector<double> SymBlockMatrix::matvec(std::span<const double> x) const {
     if (x.size() != total_dim()) throw std::invalid_argument("SymBlockMatrix: matvec size mismatch");
-    std::vector<double> y(x.size(), 0.0);
-    for (std::size_t m = 0; m < dims_.size(); ++m)
-        for (std::size_t n = m + 1; n < dims_.size(); ++n) {
-            const Matrix& b = block(m, n);
-            for (std::size_t j = 0; j < b.cols(); ++j) {
-                double acc = 0.0;
-                for (std::size_t i = 0; i < b.rows(); ++i) {
-                    y[offs_[m] + i] += b(i, j) * x[offs_[n] + j];
-                    acc += b(i, j) * x[offs_[m] + i];
-                }
-                y[offs_[n] + j] += acc;
-            }
-        }
-    for (double& v : y) v *= scale_;
+    const auto dims = u64(dims_);
+    const auto b = blocks_of(*this);
+    std::vector<double> y(x.size());
+    raise(r1_block_matvec(ctx(), dims.data(), static_cast<int>(order()), b.data(), x.data(), y.data()));
     return y;
 }
 
 Matrix SymBlockMatrix::dense() const {
+    const auto dims = u64(dims_);
+    const auto b = blocks_of(*this);
     Matrix s(total_dim(), total_dim());
-    for (std::size_t m = 0; m < dims_.size(); ++m)
-        for (std::size_t n = m + 1; n < dims_.size(); ++n) {
-            const Matrix& b = block(m, n);
-            for (std::size_t j = 0; j < b.cols(); ++j)
-                for (std::size_t i = 0; i < b.rows(); ++i) {
-                    const double v = b(i, j) * scale_;
-                    s(offs_[m] + i, offs_[n] + j) = v;
-                    s(offs_[n] + j, offs_[m] + i) = v;
-                }
-        }
+    raise(r1_block_dense(ctx(), dims.data(), static_cast<int>(order()), b.data(), s.data()));
     return s;
 }
 
 double SymBlockMatrix::frobenius_norm() const {
-    double s = 0.0;
-    for (const Matrix& b : upper_)
-        for (double v : b.values()) s += v * v;
-    return std::sqrt(2.0 * s) * scale_;
+    const auto dims = u64(dims_);
+    const auto b = blocks_of(*this);
+    double v = 0.0;
+    raise(r1_block_frobenius(ctx(), dims.data(), static_cast<int>(order()), b.data(), &v));
+    return v;
 }
 
 // ------------------------------------------------------------- the sweep --
@@ -420,6 +496,169 @@ std::optional<std::vector<double>> rayleigh_quotient_step(const Matrix& s, std::
                                     y.data(), &accepted));
     if (!accepted) return std::nullopt;
     return y;
+}
+
+// sym_eig.hpp:19 / :49-52 on the device (csrc/dense_api.cu).
+EigDecomposition sym_eig_full(const Matrix& s) {
+    if (s.rows() != s.cols()) throw std::invalid_argument("sym_eig: matrix must be square");
+    const std::size_t n = s.rows();
+    EigDecomposition d;
+    d.values.assign(n, 0.0);
+    if (n == 0) return d;
+    d.vectors = Matrix(n, n);
+    raise(r1_sym_eig_full(ctx(), static_cast<int64_t>(n), s.data(), d.values.data(),
+                          d.vectors.data()));
+    return d;
+}
+
+namespace detail {
+
+LdltFactors ldlt_factor(Matrix s) {
+    const std::size_t n = s.rows();
+    if (s.cols() != n) throw std::invalid_argument("ldlt_factor: matrix must be square");
+    LdltFactors f{Matrix(n, n), std::vector<int>(n, 0), false};
+    int sing = 0;
+    raise(r1_ldlt_factor(ctx(), static_cast<int64_t>(n), s.data(), f.w.data(), f.ipiv.data(), &sing));
+    f.singular = sing != 0;
+    return f;
+}
+
+std::vector<double> ldlt_solve(const LdltFactors& f, std::vector<double> b) {
+    const std::size_t n = f.w.rows();
+    if (b.size() != n) throw std::invalid_argument("ldlt_solve: size mismatch");
+    std::vector<double> x(n);
+    raise(r1_ldlt_solve(ctx(), static_cast<int64_t>(n), f.w.data(), f.ipiv.data(), b.data(), x.data()));
+    return x;
+}
+
+double ldlt_diag_condition(const LdltFactors& f) {
+    const std::size_t n = f.w.rows();
+    std::vector<double> diag(n), sub(n, 0.0);
+    for (std::size_t k = 0; k < n; ++k) {
+        diag[k] = f.w(k, k);
+        if (k + 1 < n) sub[k] = f.w(k + 1, k);
+    }
+    double c = 0.0;
+    raise(r1_ldlt_diag_condition(ctx(), static_cast<int64_t>(n), diag.data(), sub.data(),
+                                 f.ipiv.data(), f.singular ? 1 : 0, &c));
+    return c;
+}
+
+}  // namespace detail
+
+// ---------------------------------------------------------- tensor.hpp extras --
+std::vector<std::vector<double>> contract_leaving_all(const DenseTensor& a, const FactorSet& f, bool) {
+    if (f.order() != a.order()) throw std::invalid_argument("contract_leaving_all: order mismatch");
+    check_shapes(a, f);
+    const auto dims = u64(a.dims());
+    const auto fl = flat(f);
+    std::vector<double> w(fl.size());
+    raise(r1_contract_leaving_all(ctx(), a.data(), nullptr, dims.data(), static_cast<int>(a.order()),
+                                  fl.data(), w.data()));
+    std::vector<std::vector<double>> out;
+    std::size_t off = 0;
+    for (std::size_t k = 0; k < a.order(); ++k) {
+        out.emplace_back(w.begin() + off, w.begin() + off + a.dim(k));
+        off += a.dim(k);
+    }
+    return out;
+}
+
+std::vector<double> contract_leaving(const DenseTensor& a, const FactorSet& f, std::size_t mode,
+                                     bool parallel) {
+    if (f.order() != a.order()) throw std::invalid_argument("contract_leaving: order mismatch");
+    if (mode >= a.order()) throw std::invalid_argument("contract_leaving: mode out of range");
+    return contract_leaving_all(a, f, parallel)[mode];
+}
+
+Matrix matricize(const DenseTensor& a, std::size_t mode) {
+    if (mode >= a.order()) throw std::invalid_argument("matricize: mode out of range");
+    const auto dims = u64(a.dims());
+    Matrix m(a.dim(mode), a.size() / a.dim(mode));
+    raise(r1_matricize(ctx(), a.data(), dims.data(), static_cast<int>(a.order()),
+                       static_cast<int>(mode), 0, m.data()));
+    return m;
+}
+
+DenseTensor dematricize(const Matrix& m, std::size_t mode, std::vector<std::size_t> dims) {
+    if (mode >= dims.size()) throw std::invalid_argument("dematricize: mode out of range");
+    std::size_t rest = 1;
+    for (std::size_t k = 0; k < dims.size(); ++k)
+        if (k != mode) rest *= dims[k];
+    if (m.rows() != dims[mode] || m.cols() != rest)
+        throw std::invalid_argument("dematricize: matrix shape does not match dims");
+    DenseTensor a(dims);
+    const auto d = u64(dims);
+    raise(r1_matricize(ctx(), m.data(), d.data(), static_cast<int>(dims.size()), static_cast<int>(mode),
+                       1, a.data()));
+    return a;
+}
+
+DenseTensor rank_one_expand(const FactorSet& f, std::span<const std::size_t> dims) {
+    if (f.order() != dims.size()) throw std::invalid_argument("rank_one_expand: order mismatch");
+    for (std::size_t n = 0; n < dims.size(); ++n)
+        if (f.factors[n].size() != dims[n])
+            throw std::invalid_argument("rank_one_expand: factor length mismatch");
+    DenseTensor out(std::vector<std::size_t>(dims.begin(), dims.end()));
+    const auto d = u64(out.dims());
+    const auto fl = flat(f);
+    raise(r1_rank_one_expand(ctx(), f.lambda, fl.data(), d.data(), static_cast<int>(dims.size()),
+                             out.data()));
+    return out;
+}
+
+double residual_norm(const DenseTensor& a, const FactorSet& f, std::size_t dense_threshold) {
+    if (f.order() != a.order()) throw std::invalid_argument("residual_norm: order mismatch");
+    for (std::size_t n = 0; n < a.order(); ++n)
+        if (f.factors[n].size() != a.dim(n))
+            throw std::invalid_argument("residual_norm: factor length mismatch");
+    const auto d = u64(a.dims());
+    const auto fl = flat(f);
+    double v = 0.0;
+    raise(r1_residual_norm(ctx(), a.data(), d.data(), static_cast<int>(a.order()), f.lambda, fl.data(),
+                           dense_threshold, &v));
+    return v;
+}
+
+// ------------------------------------------------------------ generators.hpp --
+// Generated on the device (r1_generate, one counter per element) into a
+// device tensor and copied back (generators.cpp:50-116).
+std::vector<std::size_t> default_dims(const std::string& name) {
+    if (name == "gaussian") return {10, 10, 10};
+    if (name == "exp") return {30, 30, 30};
+    if (name == "arcsin") return {20, 20, 20, 20};
+    if (name == "tan") return {10, 10, 10, 10, 10};
+    throw std::invalid_argument("unknown generator: " + name);
+}
+
+namespace {
+DenseTensor generate_on_device(const std::string& name, const std::vector<std::size_t>& dims,
+                               std::uint64_t seed) {
+    if (dims.size() < 2) throw std::invalid_argument("generator: tensor order must be >= 2");
+    const auto d = u64(dims);
+    TensorGuard t;
+    raise(r1_tensor_create(ctx(), d.data(), static_cast<int>(dims.size()), &t.t));
+    raise(r1_generate(ctx(), t.t, name.c_str(), seed));
+    DenseTensor out(dims);
+    raise(r1_tensor_copy_to_host(ctx(), t.t, out.data()));
+    return out;
+}
+}  // namespace
+
+DenseTensor gen_gaussian(const std::vector<std::size_t>& dims, std::uint64_t seed) {
+    return generate_on_device("gaussian", dims, seed);
+}
+DenseTensor gen_exp(const std::vector<std::size_t>& dims) { return generate_on_device("exp", dims, 0); }
+DenseTensor gen_arcsin(const std::vector<std::size_t>& dims) {
+    return generate_on_device("arcsin", dims, 0);
+}
+DenseTensor gen_tan(const std::vector<std::size_t>& dims) { return generate_on_device("tan", dims, 0); }
+
+DenseTensor generate(const std::string& name, std::vector<std::size_t> dims, std::uint64_t seed) {
+    if (dims.empty()) dims = default_dims(name);
+    if (name != "gaussian" && name != "exp" && name != "arcsin" && name != "tan")
+        throw std::invalid_argument("unknown generator: " + name);
+    return generate_on_device(name, dims, seed);
 }
 
 // ------------------------------------------------------------------ solvers --
@@ -517,12 +756,6 @@ SolveReport from_c(const std::string& algorithm, const DenseTensor& a, const Rep
     return rep;
 }
 
-struct TensorGuard {
-    r1_tensor* t = nullptr;
-    ~TensorGuard() {
-        if (t) r1_tensor_destroy(t);
-    }
-};
 
 }  // namespace
 
@@ -534,11 +767,10 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
     std::vector<double> init;
     r1_solve_options o = c_options(a, opts, init);
     const auto dims = u64(a.dims());
-    TensorGuard t;
-    raise(r1_tensor_from_host(ctx(), a.data(), dims.data(), static_cast<int>(a.order()), &t.t));
     const std::size_t n = std::accumulate(a.dims().begin(), a.dims().end(), std::size_t{0});
     ReportBuffers b(n, opts.max_iters);
-    raise(r1_solve(ctx(), algorithm.c_str(), t.t, &o, &b.r));
+    raise(r1_solve_host(ctx(), algorithm.c_str(), a.data(), dims.data(), static_cast<int>(a.order()),
+                        &o, &b.r));
     return from_c(algorithm, a, b);
 }
 

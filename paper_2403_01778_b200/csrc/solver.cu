@@ -578,12 +578,39 @@ using namespace r1;
 
 extern "C" {
 
+static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* a,
+                       const r1_solve_options* opts, r1_solve_report* report);
+
 int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
              const r1_solve_options* opts, r1_solve_report* report) {
     return abi_guard([&] {
         CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
+        solve_impl(ctx, algorithm, a, opts, report);
+    });
+}
+
+// rank1::solve(name, DenseTensor, opts) from a host tensor: staged once into the
+// context's upload buffer (no allocation per call), then the device solve.
+int r1_solve_host(r1_context* ctx, const char* algorithm, const double* a_host,
+                  const uint64_t* dims, int order, const r1_solve_options* opts,
+                  r1_solve_report* report) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !a_host || !dims) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 1 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "solver: unsupported order");
+        const r1_tensor* t = upload_tensor(ctx, a_host, dims, order);
+        solve_impl(ctx, algorithm, t, opts, report);
+    });
+}
+
+}  // extern "C"
+
+static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* a,
+                       const r1_solve_options* opts, r1_solve_report* report) {
+    {
         const std::string alg = algorithm ? algorithm : "";
         const bool baseline =
             alg == "hopm" || alg == "jacobi_hopm" || alg == "asvd" || alg == "jacobi_asvd";
@@ -631,8 +658,10 @@ int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
         for (int i = 0; i < rr.iterations; ++i) report->trace[i] = rr.trace[i];
         report->total_sweeps = rr.sweeps;
         report->t_total = std::chrono::duration<double>(t1 - t0).count();
-    });
+    }
 }
+
+extern "C" {
 
 int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_dev,
                          const double* x0_dev, double* value_dev, double* vec_dev) {
@@ -668,8 +697,11 @@ int r1x_eig_blocks_info(r1_context* ctx, const uint64_t* dims, int order, const 
     });
 }
 
-int r1_largest_magnitude_eigenpair(r1_context* ctx, int64_t n, const double* s_host, double* value,
-                                   double* vec) {
+// Diagnostics (not in the public header): Lanczos (the solvers' eigen step)
+// on a dense host matrix.  The public dense entry r1_largest_magnitude_eigenpair
+// is the reference's full decomposition (dense_api.cu).
+int r1x_eig_dense_lanczos(r1_context* ctx, int64_t n, const double* s_host, double* value,
+                          double* vec) {
     return abi_guard([&] {
         CtxLock lk_(ctx);
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
@@ -719,6 +751,122 @@ int r1_rayleigh_quotient_step(r1_context* ctx, int64_t n, const double* s_host, 
                                     cudaMemcpyDeviceToHost, ctx->stream));
             R1_CUDA(cudaStreamSynchronize(ctx->stream));
         }
+    });
+}
+
+// contract_leaving_all (tensor.cpp:216-238) from one device sweep: with unit
+// factors v_k = u_k / |u_k| (a zero factor is replaced by e_0 and its norm 0
+// kept), w_n = A x_{k != n} u_k = (prod_{k != n} |u_k|) sqrt(d) (J(v) vhat)_n.
+// out: flat sum I_k (w_0 ++ ... ++ w_{d-1}).
+int r1_contract_leaving_all(r1_context* ctx, const double* a_host, const r1_tensor* a_dev,
+                            const uint64_t* dims, int order, const double* factors_host,
+                            double* out_host) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !dims || !factors_host || !out_host) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 2 || order > 16)
+            fail(R1_ERR_INVALID_ARGUMENT, "contract_leaving_all: order mismatch");
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        std::vector<double> v(factors_host, factors_host + n), norms(order);
+        uint64_t off = 0;
+        for (int k = 0; k < order; ++k) {
+            norms[k] = normalize(v.data() + off, dims[k]);
+            if (norms[k] == 0.0) v[off] = 1.0;
+            off += dims[k];
+        }
+        const r1_tensor* t = a_dev;
+        if (!t) {
+            if (!a_host) fail(R1_ERR_INVALID_ARGUMENT, "no tensor given");
+            t = upload_tensor(ctx, a_host, dims, order);
+        }
+        const uint64_t nb = blocks_numel(dims, order);
+        const uint64_t nba = (nb + 31) & ~uint64_t(31), na = (n + 31) & ~uint64_t(31);
+        ctx->ws_io.ensure((nba + 3 * na + 64) * sizeof(double));
+        double* b = ctx->ws_io.as<double>();
+        double* u = b + nba;
+        double* xh = u + na;
+        double* y = xh + na;
+        R1_CUDA(cudaMemcpyAsync(u, v.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        sweep_blocks(ctx, t->dev, dims, order, u, b);
+        split_stack(ctx, dims, order, u, nullptr, xh, nullptr);
+        block_matvec(ctx, dims, order, b, xh, y);
+        R1_CUDA(cudaMemcpyAsync(out_host, y, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        const double sqd = std::sqrt(static_cast<double>(order));
+        off = 0;
+        for (int k = 0; k < order; ++k) {
+            double sc = sqd;
+            for (int m = 0; m < order; ++m)
+                if (m != k) sc *= norms[m];
+            for (uint64_t i = 0; i < dims[k]; ++i) out_host[off + i] *= sc;
+            off += dims[k];
+        }
+    });
+}
+
+// Host-buffer forms of the SymBlockMatrix operations (nepv.cpp:110-157) for the
+// C++ container: y = J x, dense J, ||J||_F, all on the device.
+int r1_block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                    const double* x_host, double* y_host) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !dims) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "SymBlockMatrix: order must be >= 2");
+        const uint64_t nb = blocks_numel(dims, order);
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        ctx->ws_io.ensure((nb + 2 * n + 64) * sizeof(double));
+        double* b = ctx->ws_io.as<double>();
+        double* x = b + ((nb + 31) & ~uint64_t(31));
+        double* y = x + ((n + 31) & ~uint64_t(31));
+        R1_CUDA(cudaMemcpyAsync(b, blocks_host, nb * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        R1_CUDA(cudaMemcpyAsync(x, x_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        block_matvec(ctx, dims, order, b, x, y);
+        R1_CUDA(cudaMemcpyAsync(y_host, y, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int r1_block_dense(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                   double* s_host) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !dims) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "SymBlockMatrix: order must be >= 2");
+        const uint64_t nb = blocks_numel(dims, order);
+        uint64_t n = 0;
+        for (int k = 0; k < order; ++k) n += dims[k];
+        ctx->ws_io.ensure((nb + n * n + 64) * sizeof(double));
+        double* b = ctx->ws_io.as<double>();
+        double* S = b + ((nb + 31) & ~uint64_t(31));
+        R1_CUDA(cudaMemcpyAsync(b, blocks_host, nb * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        dense_from_blocks(ctx, dims, order, b, S);
+        R1_CUDA(cudaMemcpyAsync(s_host, S, n * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int r1_block_frobenius(r1_context* ctx, const uint64_t* dims, int order, const double* blocks_host,
+                       double* out) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !dims || !out) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "SymBlockMatrix: order must be >= 2");
+        const uint64_t nb = blocks_numel(dims, order);
+        ctx->ws_io.ensure((nb + 64) * sizeof(double));
+        double* b = ctx->ws_io.as<double>();
+        double* f2 = b + ((nb + 31) & ~uint64_t(31));
+        R1_CUDA(cudaMemcpyAsync(b, blocks_host, nb * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        sumsq_device(ctx, b, nb, f2);
+        double h = 0.0;
+        R1_CUDA(cudaMemcpyAsync(&h, f2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        R1_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = std::sqrt(2.0 * h) / static_cast<double>(order - 1);  // nepv.cpp:152-157
     });
 }
 
