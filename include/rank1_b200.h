@@ -76,6 +76,11 @@ typedef struct r1_solve_options {
      * (BASELINE config 1's "relative sigma change" rule).  0 = reference
      * behaviour (Eq. 11 residual only, solvers.cpp:175-178). */
     double scf_lambda_rtol;
+    /* Extension: when nonzero HOSCF also stops once the stacked eigenvector
+     * turns by less than this between iterations, |sin angle(x_k, x_{k-1})|
+     * <= scf_angle_tol (the factor-change rule of PAPER.md:400-408).  Evaluated
+     * on the device with Eq. 11 and the sigma rule.  0 = off. */
+    double scf_angle_tol;
 } r1_solve_options;
 
 /* Mirrors rank1::IterationRecord (solvers.hpp:33-43). */
@@ -87,9 +92,12 @@ typedef struct r1_iteration_record {
     int32_t rqi_accepted;
     int32_t n_sweeps;      /* extension: build_j sweeps charged to this iteration */
     double lambda_pre_rqi;
-    double t_build_j;      /* seconds, CUDA events on the solver stream          */
+    double t_build_j;      /* seconds, device-timed (events / %globaltimer)      */
     double t_eig;
     double t_other;
+    /* extension: |sin angle(x_k, x_{k-1})| of the stacked eigenvectors (HOSCF;
+     * -1 for the first iteration and where not computed) */
+    double factor_change;
 } r1_iteration_record;
 
 /* Mirrors rank1::SolveReport (solvers.hpp:45-58).  The caller owns every

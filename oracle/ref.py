@@ -266,7 +266,8 @@ class SolveOptionsC(ctypes.Structure):
                 ("rqi_accept_rule", ctypes.c_int32), ("stop_rule", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("record_kkt", ctypes.c_int32),
                 ("asvd_disjoint_pairs", ctypes.c_int32),
-                ("reuse_intermediates", ctypes.c_int32), ("scf_lambda_rtol", ctypes.c_double)]
+                ("reuse_intermediates", ctypes.c_int32), ("scf_lambda_rtol", ctypes.c_double),
+                ("scf_angle_tol", ctypes.c_double)]
 
 
 class IterationRecordC(ctypes.Structure):
@@ -274,7 +275,8 @@ class IterationRecordC(ctypes.Structure):
                 ("eq11_value", ctypes.c_double), ("kkt_max_residual", ctypes.c_double),
                 ("rqi_accepted", ctypes.c_int32), ("n_sweeps", ctypes.c_int32),
                 ("lambda_pre_rqi", ctypes.c_double), ("t_build_j", ctypes.c_double),
-                ("t_eig", ctypes.c_double), ("t_other", ctypes.c_double)]
+                ("t_eig", ctypes.c_double), ("t_other", ctypes.c_double),
+                ("factor_change", ctypes.c_double)]
 
 
 class SolveReportC(ctypes.Structure):

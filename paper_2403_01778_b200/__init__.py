@@ -372,7 +372,9 @@ def stack_factors(f: FactorSet) -> StackedVector:
 
 @dataclass
 class SolveOptions:
-    """solvers.hpp:17-31 (same defaults) + one extension, scf_lambda_rtol."""
+    """solvers.hpp:17-31 (same defaults) + two device-side stop extensions:
+    scf_lambda_rtol (relative sigma change) and scf_angle_tol (factor change,
+    |sin angle(x_k, x_{k-1})|); 0 = off."""
     tol: float = 1e-4
     max_iters: int = 500
     seed: int = 0
@@ -386,6 +388,7 @@ class SolveOptions:
     asvd_disjoint_pairs: bool = False
     reuse_intermediates: bool = False
     scf_lambda_rtol: float = 0.0
+    scf_angle_tol: float = 0.0
 
 
 @dataclass
@@ -400,6 +403,7 @@ class IterationRecord:
     t_eig: float = 0.0
     t_other: float = 0.0
     n_sweeps: int = 1
+    factor_change: float = -1.0
 
 
 @dataclass
@@ -598,6 +602,7 @@ def _options_c(o: SolveOptions, dims):
     c.reuse_intermediates = 1 if o.reuse_intermediates else 0
     c.asvd_disjoint_pairs = 1 if o.asvd_disjoint_pairs else 0
     c.scf_lambda_rtol = o.scf_lambda_rtol
+    c.scf_angle_tol = o.scf_angle_tol
     keep = None
     if o.init == "provided":
         if len(o.init_factors) != len(dims):
@@ -659,7 +664,7 @@ def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None) 
         rep.trace.append(IterationRecord(t_.lambda_, t_.stop_value, t_.eq11_value,
                                          t_.kkt_max_residual, bool(t_.rqi_accepted),
                                          t_.lambda_pre_rqi, t_.t_build_j, t_.t_eig, t_.t_other,
-                                         int(t_.n_sweeps)))
+                                         int(t_.n_sweeps), t_.factor_change))
     return rep
 
 

@@ -48,7 +48,8 @@ class SolveOptionsC(ctypes.Structure):
                 ("rqi_accept_rule", ctypes.c_int32), ("stop_rule", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("record_kkt", ctypes.c_int32),
                 ("asvd_disjoint_pairs", ctypes.c_int32),
-                ("reuse_intermediates", ctypes.c_int32), ("scf_lambda_rtol", ctypes.c_double)]
+                ("reuse_intermediates", ctypes.c_int32), ("scf_lambda_rtol", ctypes.c_double),
+                ("scf_angle_tol", ctypes.c_double)]
 
 
 class IterationRecordC(ctypes.Structure):
@@ -56,7 +57,8 @@ class IterationRecordC(ctypes.Structure):
                 ("eq11_value", ctypes.c_double), ("kkt_max_residual", ctypes.c_double),
                 ("rqi_accepted", ctypes.c_int32), ("n_sweeps", ctypes.c_int32),
                 ("lambda_pre_rqi", ctypes.c_double), ("t_build_j", ctypes.c_double),
-                ("t_eig", ctypes.c_double), ("t_other", ctypes.c_double)]
+                ("t_eig", ctypes.c_double), ("t_other", ctypes.c_double),
+                ("factor_change", ctypes.c_double)]
 
 
 class SolveReportC(ctypes.Structure):
@@ -152,6 +154,7 @@ EXTRA_SIGNATURES = {
                                            ctypes.POINTER(ctypes.c_int), _dp]),
     "r1x_sweep_plan_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_int64)]),
+    "r1x_solver_graph_mode": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     "r1x_eig_dense_lanczos": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp]),
     "r1x_ldlt": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.POINTER(ctypes.c_int), _dp, _dp,
                                 ctypes.POINTER(ctypes.c_int), _dp]),

@@ -1496,7 +1496,7 @@ int panel_cluster_size(r1_context* ctx, int64_t n) {
         std::lock_guard<std::mutex> g(cache_mutex());
         max16 = max_by_device[ctx->device];
     }
-    static const char* genv = std::getenv("R1_BK_G");  // development: force the cluster size
+    static const char* genv = dev_env("R1_BK_G");  // development: force the cluster size
     if (genv) return std::max(1, std::min(max16, std::atoi(genv)));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max16, (n + 255) / 256)));
 }
@@ -1525,7 +1525,7 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     bk_init_kernel<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 64))), 256, 0,
                      ctx->stream>>>(L.perm, L.ps, n);
     check_launch(ctx, "bk_init_kernel");
-    static const bool trace = std::getenv("R1_BK_TRACE") != nullptr;
+    static const bool trace = dev_env("R1_BK_TRACE") != nullptr;
     static DeviceBuffer tbuf;
     if (trace) {
         tbuf.ensure(16 * sizeof(unsigned long long));
@@ -1599,7 +1599,7 @@ void bk_solve(r1_context* ctx, int64_t n, const double* A, void* ws, const doubl
               int* ok_dev) {
     const BkLayout L = bk_layout(ws, n, ctx->num_sms);
     SolveArgs s{n, A, L.ipiv, L.ps, L.perm, L.ctl, x, L.z, y, L.part, ok_dev};
-    static const char* gsolve = std::getenv("R1_BK_GRID_SOLVE");
+    static const char* gsolve = dev_env("R1_BK_GRID_SOLVE");
     const int gp = panel_cluster_size(ctx, n);
     if (!(gsolve && std::atoi(gsolve)) && n < (int64_t(1) << 30)) {
         // cluster solve: interchanges composed per panel, z in shared memory

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include <cstdint>
@@ -40,6 +41,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define R1_CUDA(x) ::r1::cuda_check((x), #x, __FILE__, __LINE__)
 
 void set_last_error(const std::string& msg);
+
+// Development switches exist only in the development build
+// (build.py --dev -> librank1_b200_dev.so, -DR1_DEV_SWITCHES); the release
+// library ignores the environment.
+#ifdef R1_DEV_SWITCHES
+inline const char* dev_env(const char* name) { return std::getenv(name); }
+#else
+inline const char* dev_env(const char*) { return nullptr; }
+#endif
 
 // Runs f, mapping exceptions onto the ABI status codes (never throws).
 template <typename F>
@@ -91,20 +101,27 @@ struct DeviceBuffer {
 
 // Device copies of small host descriptors (BlockOp ...) keyed by content: a
 // descriptor uploaded before is reused, so the hot loops (HOSCF alternates two
-// block buffers) do no pageable host-to-device copy — which would make the host
-// wait for the stream.  Users share one stream, so reusing a slot is ordered
-// after the kernels that read it.
+// block buffers) do no host-to-device copy — which would make the host wait
+// for the stream.  The host copies live in pinned memory, so an upload issued
+// while the stream is being captured into a CUDA graph is a legal memcpy node
+// (replayed from the same, unchanging slot).  Users share one stream, so
+// reusing a slot is ordered after the kernels that read it.
 template <typename T, int N = 4>
 struct DescCache {
-    T host[N];
+    T* host = nullptr;  // N pinned slots
     bool used[N] = {};
     int next = 0;
     void* dev[N] = {};
+    DescCache() = default;
+    DescCache(const DescCache&) = delete;
+    DescCache& operator=(const DescCache&) = delete;
     ~DescCache() {
         for (auto p : dev)
             if (p) cudaFree(p);
+        if (host) cudaFreeHost(host);
     }
     const T* get(const T& d, cudaStream_t s) {
+        if (!host) R1_CUDA(cudaMallocHost(&host, N * sizeof(T)));
         for (int i = 0; i < N; ++i)
             if (used[i] && std::memcmp(&host[i], &d, sizeof(T)) == 0) return static_cast<T*>(dev[i]);
         const int i = next;
@@ -206,6 +223,9 @@ struct r1_context {
     r1::DeviceBuffer ws_io;
     r1_tensor upload_view;
     r1::HostStaging staging;
+    // diagnostics: how the last HOSCF solve drove its loop (0 direct launches,
+    // 1 CUDA-graph replays, 2 graph replays behind conditional IF nodes)
+    int solver_graph_mode = -1;
     // calls on one context are serialised (SURVEY §8b threading contract)
     std::recursive_mutex mu;
     std::map<std::vector<uint64_t>, std::shared_ptr<r1::SweepPlan>> plans;

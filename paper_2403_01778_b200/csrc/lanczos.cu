@@ -1054,14 +1054,14 @@ namespace {
 
 void finish_lanczos(r1_context* ctx, const EigArgs& a, int* info_host, double* stats_host) {
     const int64_t n = a.n;
-    static const bool dbg = std::getenv("R1_DEBUG_EIG") != nullptr;
+    static const bool dbg = dev_env("R1_DEBUG_EIG") != nullptr;
     if (dbg) {
         int ctl[5];
         double st[16];
         R1_CUDA(cudaMemcpyAsync(ctl, a.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaMemcpyAsync(st, a.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
         R1_CUDA(cudaStreamSynchronize(ctx->stream));
-        static const bool dbg_t = std::getenv("R1_DEBUG_EIG_T") != nullptr;
+        static const bool dbg_t = dev_env("R1_DEBUG_EIG_T") != nullptr;
         if (dbg_t) {
             std::vector<double> al(ctl[2]), be(ctl[2]);
             R1_CUDA(cudaMemcpy(al.data(), a.alpha, al.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1109,8 +1109,8 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     EigArgs a{};
     a.n = n;
     a.maxm = maxm;
-    static const char* ce = std::getenv("R1_EIG_CHECK");
-    static const char* ms = std::getenv("R1_EIG_MIN_STEPS");
+    static const char* ce = dev_env("R1_EIG_CHECK");
+    static const char* ms = dev_env("R1_EIG_MIN_STEPS");
     a.check_every = n <= 64 ? 1 : (ce ? std::max(1, std::atoi(ce)) : 8);
     // the warm start (previous eigenvector) converges the picked end within a
     // few steps; the first check comes after 8 (C2 solve 0.87 -> 0.33 ms)
@@ -1136,9 +1136,9 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.op = P.dop.get(op, ctx->stream);
     a.out_value = value_dev;
     a.out_vec = vec_dev;
-    static const bool dbg_text = std::getenv("R1_DEBUG_EIG_TEXT") != nullptr;
+    static const bool dbg_text = dev_env("R1_DEBUG_EIG_TEXT") != nullptr;
     a.debug_text = dbg_text ? 1 : 0;
-    static const char* wn = std::getenv("R1_EIG_WARM_NOISE");  // development
+    static const char* wn = dev_env("R1_EIG_WARM_NOISE");  // development
     // 1e-6 (was 1e-3): the previous Ritz vectors are good to ~1e-5 or better,
     // a 1e-3 random component only had to be filtered out again (C1 eigen -6%)
     a.warm_noise = wn ? std::atof(wn) : 1e-6;
@@ -1148,7 +1148,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
             R1_CUDA(cudaMemsetAsync(P.hint.ptr, 0, sizeof(int), ctx->stream));
         }
         a.hint = P.hint.as<int>();
-        static const char* he = std::getenv("R1_EIG_HINT");  // development: 0 disables the hint
+        static const char* he = dev_env("R1_EIG_HINT");  // development: 0 disables the hint
         a.warm = x0 != nullptr && !(he && std::atoi(he) == 0) ? 1 : 0;
         P.other.ensure(static_cast<size_t>(n) * sizeof(double));
         a.x1 = x0 != nullptr && P.other_valid ? P.other.as<double>() : nullptr;
@@ -1157,9 +1157,9 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     }
 
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
-    static const char* gs = std::getenv("R1_EIG_GRID");
-    static const char* gc = std::getenv("R1_EIG_CLUSTER");
-    static const char* gsm = std::getenv("R1_EIG_SMALL");
+    static const char* gs = dev_env("R1_EIG_GRID");
+    static const char* gc = dev_env("R1_EIG_CLUSTER");
+    static const char* gsm = dev_env("R1_EIG_SMALL");
     if (n <= kSmallN && !gs && !gc && !(gsm && std::atoi(gsm) == 0)) {
         // one thread-block cluster, rows of J / V / w on chip
         const int G = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (n + 15) / 16)));

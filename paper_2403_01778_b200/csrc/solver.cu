@@ -78,15 +78,22 @@ struct Degenerate : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// CUDA events for the phase timings, created once per working set and reused
+// by every solve (reset() rewinds the pool).
 struct Events {
     std::vector<cudaEvent_t> ev;
+    size_t used = 0;
     ~Events() {
         for (auto e : ev) cudaEventDestroy(e);
     }
+    void reset() { used = 0; }
     cudaEvent_t rec(cudaStream_t s) {
-        cudaEvent_t e;
-        R1_CUDA(cudaEventCreate(&e));
-        ev.push_back(e);
+        if (used == ev.size()) {
+            cudaEvent_t e;
+            R1_CUDA(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+        cudaEvent_t e = ev[used++];
         R1_CUDA(cudaEventRecord(e, s));
         return e;
     }
@@ -110,6 +117,8 @@ struct Work {
     double *fro2, *fro2mid, *mu, *post, *postmid, *dotv;
     int* flags;
     PinnedBuffer hst;  // host staging
+    std::shared_ptr<void> hd;  // HoscfDev (device-loop state), created on first use
+    Events events;             // phase-timing events (iHOSCF / baselines), reused
 
     Work(r1_context* c, const r1_tensor* a, bool dense)
         : ctx(c), A(a), dims(a->dims), d(static_cast<int>(a->dims.size())) {
@@ -197,9 +206,364 @@ struct RunResult {
     int sweeps = 0;
 };
 
+// ---- HOSCF with the loop control on the device ----------------------------
+// Each iteration k (solvers.cpp:143-179) is the same device sequence
+//   eigen step on J(u_{k-1}) -> split / stack -> sweep J(u_k) -> post step ->
+//   record (trace slot, stop decision, warm-start vector),
+// so it is captured ONCE per solve as a CUDA graph (two parities: the factor /
+// block buffers ping-pong) and replayed.  The stop test — Eq. 11 <= tol
+// (:175-178), plus the extensions relative-sigma change and factor change
+// |sin angle(x_k, x_{k-1})| — is evaluated on the device
+// by the record kernel, which writes one status word.  Each replay is wrapped
+// in a conditional IF node whose condition a gate kernel sets from that status,
+// so the host enqueues iterations in batches and reads the 8-byte state once
+// per batch: after a stop the remaining replays are empty.  Phase times come
+// from %globaltimer stamps in the trace.  Without conditional-node support the
+// graphs are replayed one per status read; without graphs the same kernels are
+// launched directly.
+
+struct DevRecord {
+    double lambda, stop_value, eq11, kkt, angle, pad;
+    unsigned long long t[5];  // globaltimer: start, after eig, after split, after sweep, end
+};
+
+struct IterState {
+    int counter;  // iterations completed
+    int status;   // 0 running, 1 Eq.11, 2 sigma change, 3 factor change, 4 max_iters, 5 degenerate
+};
+
+struct IterParams {
+    double tol, lambda_rtol, angle_tol;
+    int max_iters, record_kkt;
+    int64_t n;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void stamp_kernel(const IterState* st, DevRecord* trace, int which) {
+    trace[st->counter].t[which] = global_ns();
+}
+
+__global__ void gate_kernel(const IterState* st, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, st->status == 0 ? 1u : 0u);
+}
+
+constexpr int kRecThreads = 256;
+
+__device__ double rec_block_sum(double v, double* sh) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int k = 0; k < kRecThreads / 32; ++k) s += sh[k];
+    return s;
+}
+
+// post = [rho, eq11, kkt, fro, lambda, ...] of the new J (post_kernel)
+__global__ void __launch_bounds__(kRecThreads) record_kernel(IterState* st, DevRecord* trace,
+                                                             const IterParams* prm,
+                                                             const double* __restrict__ post,
+                                                             const double* __restrict__ mu,
+                                                             const int* __restrict__ flags,
+                                                             const double* __restrict__ X,
+                                                             double* __restrict__ Xprev) {
+    __shared__ double sh[32];
+    const int k = st->counter + 1;
+    const int64_t n = prm->n;
+    double angle = -1.0;
+    if (k > 1) {
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < n; i += kRecThreads) s = fma(X[i], Xprev[i], s);
+        const double c = rec_block_sum(s, sh);
+        s = 0.0;
+        for (int64_t i = threadIdx.x; i < n; i += kRecThreads) {
+            const double r = X[i] - c * Xprev[i];
+            s = fma(r, r, s);
+        }
+        angle = sqrt(rec_block_sum(s, sh));
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += kRecThreads) Xprev[i] = X[i];
+    if (threadIdx.x != 0) return;
+    DevRecord& r = trace[k - 1];
+    if (flags[0]) {  // split_factors found a zero block: the restart path (solvers.cpp:78-91)
+        st->status = 5;
+        return;
+    }
+    const double lam = mu[0];
+    r.lambda = lam;
+    r.eq11 = post[1];
+    r.stop_value = post[1];
+    r.kkt = prm->record_kkt ? post[2] : __longlong_as_double(0x7ff8000000000000ll);
+    r.angle = angle;
+    int status = 0;
+    if (r.stop_value <= prm->tol)
+        status = 1;
+    else if (prm->lambda_rtol > 0.0 && k > 1 && fabs(lam - trace[k - 2].lambda) <= prm->lambda_rtol * fabs(lam))
+        status = 2;
+    else if (prm->angle_tol > 0.0 && k > 1 && angle <= prm->angle_tol)
+        status = 3;
+    else if (k >= prm->max_iters)
+        status = 4;
+    r.t[4] = global_ns();
+    st->status = status;
+    st->counter = k;
+}
+
+struct HoscfDev {
+    DeviceBuffer mem;     // IterState + IterParams + trace
+    IterState* state = nullptr;
+    IterParams* params = nullptr;
+    DevRecord* trace = nullptr;
+    int cap = 0;
+    PinnedBuffer hst;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    bool conditional = false;
+    uint64_t launches_per_iter = 0;
+    ~HoscfDev() {
+        for (auto e : exec)
+            if (e) cudaGraphExecDestroy(e);
+    }
+    void ensure(int max_iters) {
+        if (max_iters <= cap) return;
+        const size_t bytes = 256 + static_cast<size_t>(max_iters + 1) * sizeof(DevRecord);
+        mem.ensure(bytes);
+        state = mem.as<IterState>();
+        params = reinterpret_cast<IterParams*>(mem.as<char>() + 64);
+        trace = reinterpret_cast<DevRecord*>(mem.as<char>() + 256);
+        cap = max_iters;
+    }
+};
+
+// One HOSCF iteration on the device; p = parity (reads buffers p, writes p^1).
+void enqueue_hoscf_iteration(Work& w, HoscfDev& D, int p, bool warm) {
+    r1_context* ctx = w.ctx;
+    const cudaStream_t st = w.st();
+    double* Ub[2] = {w.U, w.Umid};
+    double* Jb[2] = {w.J, w.Jmid};
+    double* fb[2] = {w.fro2, w.fro2mid};
+    double* pb[2] = {w.post, w.postmid};
+    const int q = p ^ 1;
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 0);
+    check_launch(ctx, "stamp_kernel");
+    eig_blocks(ctx, w.dims.data(), w.d, Jb[p], warm ? w.Xprev : nullptr, w.mu, w.X, nullptr, nullptr,
+               true);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 1);
+    check_launch(ctx, "stamp_kernel");
+    split_stack(ctx, w.dims.data(), w.d, w.X, Ub[q], w.Xhat, w.flags);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 2);
+    check_launch(ctx, "stamp_kernel");
+    w.sweep(Ub[q], Jb[q], fb[q]);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 3);
+    check_launch(ctx, "stamp_kernel");
+    w.post_step(Jb[q], fb[q], w.Xhat, Ub[q], w.mu, 0.0, pb[q]);
+    record_kernel<<<1, kRecThreads, 0, st>>>(D.state, D.trace, D.params, pb[q], w.mu, w.flags, w.X,
+                                             w.Xprev);
+    check_launch(ctx, "record_kernel");
+}
+
+// Capture the parity-p iteration as [gate] -> IF(status == 0) {iteration} (or
+// the bare iteration when conditional = false) and instantiate it.
+cudaGraphExec_t capture_iteration(Work& w, HoscfDev& D, int p, bool conditional, uint64_t* launches) {
+    const cudaStream_t st = w.st();
+    cudaGraph_t g = nullptr;
+    R1_CUDA(cudaGraphCreate(&g, 0));
+    struct G {
+        cudaGraph_t g;
+        ~G() {
+            if (g) cudaGraphDestroy(g);
+        }
+    } guard{g};
+    cudaGraph_t body = g;
+    if (conditional) {
+        cudaGraphConditionalHandle h;
+        R1_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+        R1_CUDA(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        gate_kernel<<<1, 1, 0, st>>>(D.state, h);
+        cudaGraph_t cap = nullptr;
+        R1_CUDA(cudaStreamEndCapture(st, &cap));
+        size_t nn = 0;
+        R1_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        R1_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        R1_CUDA(cudaGraphAddNode(&cnode, g, nodes.data(), nn, &cp));
+        body = cp.conditional.phGraph_out[0];
+    }
+    const uint64_t l0 = w.ctx->launches;
+    R1_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+        enqueue_hoscf_iteration(w, D, p, true);
+    } catch (...) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(st, &junk);
+        cudaGetLastError();
+        throw;
+    }
+    cudaGraph_t cap = nullptr;
+    R1_CUDA(cudaStreamEndCapture(st, &cap));
+    *launches = w.ctx->launches - l0;
+    w.ctx->launches = l0;  // counted per executed replay instead
+    cudaGraphExec_t exec = nullptr;
+    R1_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    return exec;
+}
+
+RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<double>& u0) {
+    RunResult rr;
+    r1_context* ctx = w.ctx;
+    const cudaStream_t st = w.st();
+    const int d = w.d;
+    const int64_t n = w.n;
+    if (!w.hd) w.hd = std::make_shared<HoscfDev>();
+    HoscfDev& D = *static_cast<HoscfDev*>(w.hd.get());
+    D.ensure(o.max_iters);
+    // parameters and state (pageable -> synchronous copies, before any capture)
+    IterParams prm{o.tol, o.scf_lambda_rtol, o.scf_angle_tol, o.max_iters, o.record_kkt, n};
+    IterState s0{0, 0};
+    R1_CUDA(cudaMemcpyAsync(D.params, &prm, sizeof(prm), cudaMemcpyHostToDevice, st));
+    R1_CUDA(cudaMemcpyAsync(D.state, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
+
+    // lambda0 and J(u0) (the reference's build_j before the loop, solvers.cpp:131-141)
+    R1_CUDA(cudaMemcpyAsync(w.U, u0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    split_stack(ctx, w.dims.data(), d, w.U, nullptr, w.Xhat, w.flags);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 2);  // trace[0].t[2..3]: the initial sweep
+    check_launch(ctx, "stamp_kernel");
+    w.sweep(w.U, w.J, w.fro2);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 3);
+    check_launch(ctx, "stamp_kernel");
+    unsigned long long t_init[2];
+    R1_CUDA(cudaMemcpyAsync(t_init, &D.trace[0].t[2], sizeof(t_init), cudaMemcpyDeviceToHost, st));
+    w.post_step(w.J, w.fro2, w.Xhat, w.U, nullptr, 0.0, w.post);
+    double* h = w.hst.as<double>();
+    w.fetch(h, w.post, 8);
+    // iteration 1: cold eigen step, launched directly
+    enqueue_hoscf_iteration(w, D, 0, false);
+    IterState* hs = reinterpret_cast<IterState*>(h + 16);
+    w.fetch(hs, D.state, 1);
+    w.sync();
+    rr.lambda0 = h[4];
+    const double t_init_sweep = (t_init[1] - t_init[0]) * 1e-9;
+
+    // iterations 2.. : graph replays with the device stop test
+    int done = hs->counter, status = hs->status;
+    if (status == 0) {
+        bool graphs = true;
+        static const char* nog = dev_env("R1_SOLVER_GRAPHS");  // development: 0 = direct launches
+        if (nog && std::atoi(nog) == 0) graphs = false;
+        uint64_t per_iter = 0;
+        if (graphs) {
+            for (auto& e : D.exec)
+                if (e) {
+                    cudaGraphExecDestroy(e);
+                    e = nullptr;
+                }
+            D.conditional = true;
+            try {
+                D.exec[1] = capture_iteration(w, D, 1, true, &per_iter);
+                D.exec[0] = capture_iteration(w, D, 0, true, &per_iter);
+            } catch (const Error&) {
+                cudaGetLastError();
+                for (auto& e : D.exec)
+                    if (e) {
+                        cudaGraphExecDestroy(e);
+                        e = nullptr;
+                    }
+                D.conditional = false;
+                try {
+                    D.exec[1] = capture_iteration(w, D, 1, false, &per_iter);
+                    D.exec[0] = capture_iteration(w, D, 0, false, &per_iter);
+                } catch (const Error&) {
+                    cudaGetLastError();
+                    graphs = false;
+                }
+            }
+        }
+        ctx->solver_graph_mode = graphs ? (D.conditional ? 2 : 1) : 0;
+        int batch = D.conditional && graphs ? 2 : 1;
+        int k = done;  // iterations enqueued so far
+        while (status == 0) {
+            const int nb = std::min(batch, o.max_iters - k);
+            for (int b = 0; b < nb; ++b, ++k) {
+                const int p = k & 1;  // iteration k+1 reads the buffers of parity k & 1
+                if (graphs)
+                    R1_CUDA(cudaGraphLaunch(D.exec[p], st));
+                else
+                    enqueue_hoscf_iteration(w, D, p, true);
+            }
+            w.fetch(hs, D.state, 1);
+            w.sync();
+            if (graphs) ctx->launches += per_iter * static_cast<uint64_t>(hs->counter - done);
+            done = hs->counter;
+            status = hs->status;
+            k = done;
+            batch = std::min(batch * 2, 32);
+        }
+    }
+    if (status == 5)
+        throw Degenerate("hoscf: eigenvector block collapsed to zero");
+
+    // trace and final state
+    std::vector<DevRecord> tr(done);
+    if (done) R1_CUDA(cudaMemcpyAsync(tr.data(), D.trace, done * sizeof(DevRecord), cudaMemcpyDeviceToHost, st));
+    const int fin = done & 1;  // buffers written by the last iteration
+    double* Ub[2] = {w.U, w.Umid};
+    double* pb[2] = {w.post, w.postmid};
+    rr.factors.resize(n);
+    rr.final_x.resize(n);
+    w.fetch(h, pb[fin], 8);
+    w.fetch(rr.factors.data(), Ub[fin], n);
+    w.fetch(rr.final_x.data(), w.Xprev, n);
+    w.sync();
+    if (fin == 1) {  // keep the Work's canonical buffers pointing at the current state
+        std::swap(w.U, w.Umid);
+        std::swap(w.J, w.Jmid);
+        std::swap(w.fro2, w.fro2mid);
+        std::swap(w.post, w.postmid);
+    }
+    double lam = h[4];
+    if (lam < 0.0) {  // finalize_sign (solvers.cpp:70-76)
+        lam = -lam;
+        for (uint64_t i = 0; i < w.dims[0]; ++i) rr.factors[i] = -rr.factors[i];
+    }
+    rr.lambda = lam;
+    rr.iterations = done;
+    rr.converged = status >= 1 && status <= 3;
+    rr.sweeps = 1 + done;
+    for (int i = 0; i < done; ++i) {
+        const DevRecord& q = tr[i];
+        r1_iteration_record rec{};
+        rec.lambda = q.lambda;
+        rec.stop_value = q.stop_value;
+        rec.eq11_value = q.eq11;
+        rec.kkt_max_residual = q.kkt;
+        rec.rqi_accepted = 0;
+        rec.n_sweeps = i == 0 ? 2 : 1;
+        rec.lambda_pre_rqi = std::numeric_limits<double>::quiet_NaN();
+        rec.factor_change = q.angle;
+        rec.t_eig = (q.t[1] - q.t[0]) * 1e-9;
+        rec.t_build_j = (q.t[3] - q.t[2]) * 1e-9 + (i == 0 ? t_init_sweep : 0.0);
+        rec.t_other = (q.t[2] - q.t[1]) * 1e-9 + (q.t[4] - q.t[3]) * 1e-9;
+        rr.trace.push_back(rec);
+    }
+    return rr;
+}
+
 RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0, bool accelerated) {
     RunResult rr;
-    Events ev;
+    Events& ev = w.events;
+    ev.reset();
     const cudaStream_t st = w.st();
     const int d = w.d;
     const int64_t n = w.n;
@@ -217,6 +581,7 @@ RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
     rr.sweeps = 1;
     struct Marks {
         cudaEvent_t a, b, c, d2, e;
+        cudaEvent_t f = nullptr, g = nullptr;  // the accepted-RQI sweep (solvers.cpp:266-270)
     };
     std::vector<Marks> marks;
     bool have_prev = false;
@@ -227,6 +592,7 @@ RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
     for (int k = 1; k <= o.max_iters; ++k) {
         r1_iteration_record rec{};
         rec.lambda_pre_rqi = kNan;
+        rec.factor_change = -1.0;
         rec.n_sweeps = (k == 1) ? 2 : 1;
         Marks mk;
         mk.a = ev.rec(st);
@@ -287,7 +653,9 @@ RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
                 std::swap(w.U, w.Urqi);
                 // xhat of the refined factors (stack_factors(u), :272)
                 split_stack(w.ctx, w.dims.data(), d, w.U, nullptr, w.XhatR, w.flags);
+                mk.f = ev.rec(st);
                 w.sweep(w.U, w.J, w.fro2);
+                mk.g = ev.rec(st);
                 rec.n_sweeps += 1;
                 w.post_step(w.J, w.fro2, w.XhatR, w.U, nullptr, rho_y, w.post);
                 w.fetch(h + 16, w.post, 8);
@@ -346,8 +714,9 @@ RunResult run(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
         auto& r = rr.trace[k];
         const Marks& m = marks[k];
         r.t_eig = Events::secs(m.a, m.b);
-        r.t_build_j = Events::secs(m.c, m.d2) + (k == 0 ? Events::secs(e0, e1) : 0.0);
-        r.t_other = Events::secs(m.b, m.c) + Events::secs(m.d2, m.e);
+        const double t_rqi_sweep = m.f ? Events::secs(m.f, m.g) : 0.0;
+        r.t_build_j = Events::secs(m.c, m.d2) + (k == 0 ? Events::secs(e0, e1) : 0.0) + t_rqi_sweep;
+        r.t_other = Events::secs(m.b, m.c) + Events::secs(m.d2, m.e) - t_rqi_sweep;
     }
     return rr;
 }
@@ -381,7 +750,8 @@ std::vector<std::pair<int, int>> asvd_pairs(int d, bool disjoint, int iteration)
 RunResult run_baseline(Work& w, const r1_solve_options& o, const std::vector<double>& u0,
                        Baseline kind) {
     RunResult rr;
-    Events ev;
+    Events& ev = w.events;
+    ev.reset();
     r1_context* ctx = w.ctx;
     const cudaStream_t st = w.st();
     const int d = w.d;
@@ -440,6 +810,7 @@ RunResult run_baseline(Work& w, const r1_solve_options& o, const std::vector<dou
     for (int k = 1; k <= o.max_iters; ++k) {
         r1_iteration_record rec{};
         rec.lambda_pre_rqi = kNan;
+        rec.factor_change = -1.0;
         cudaEvent_t t0 = ev.rec(st);
         const size_t nsw0 = sweeps.size();
         double lambda = 0.0;
@@ -631,7 +1002,8 @@ static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* 
                             : alg == "asvd"        ? Baseline::asvd
                                                    : Baseline::jacobi_asvd;
         auto go = [&](const std::vector<double>& u0) {
-            return baseline ? run_baseline(w, *opts, u0, bk) : run(w, *opts, u0, acc);
+            if (baseline) return run_baseline(w, *opts, u0, bk);
+            return acc ? run(w, *opts, u0, true) : run_hoscf_dev(w, *opts, u0);
         };
         try {
             rr = go(initial_factors(a, *opts));
@@ -670,6 +1042,15 @@ int r1_eig_blocks_device(r1_context* ctx, const uint64_t* dims, int order, const
         if (!ctx) fail(R1_ERR_INVALID_ARGUMENT, "null context");
         R1_CUDA(cudaSetDevice(ctx->device));
         eig_blocks(ctx, dims, order, blocks_dev, x0_dev, value_dev, vec_dev, nullptr, nullptr);
+    });
+}
+
+// Diagnostics (not in the public header): the loop mode of the last HOSCF solve.
+int r1x_solver_graph_mode(r1_context* ctx, int* mode) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !mode) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        *mode = ctx->solver_graph_mode;
     });
 }
 

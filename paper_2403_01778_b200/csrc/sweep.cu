@@ -1096,7 +1096,7 @@ size_t smem_bytes(int nra, int ncb, int stages, bool tma) {
 // one class because I0 % 4 == 0.
 int alignment_classes(const Level& L) {
     // R1_SWEEP_MERGE: 0 never merge, 1 (default) when it keeps tiles full, 2 whenever legal
-    static const char* env = std::getenv("R1_SWEEP_MERGE");
+    static const char* env = dev_env("R1_SWEEP_MERGE");
     const int mode = env ? std::atoi(env) : 1;
     if (mode == 0) return 1;
     if (!L.tma || L.I0 % 4 != 0) return 1;
@@ -1133,7 +1133,7 @@ void tile_level(Level& L, int num_sms) {
         // no C1 partials, and no 128-B line shared by two row tiles (C3 200^4:
         // with a 1600-B column pitch every column's split fell inside a line,
         // 8% extra DRAM reads)
-        static const char* n8_env = std::getenv("R1_SWEEP_NRA8");
+        static const char* n8_env = dev_env("R1_SWEEP_NRA8");
         const bool nra8 = n8_env ? std::atoi(n8_env) != 0 : true;
         L.nwc = kBoxNWC;  // (8 warps x 4 columns at I0 = 200 measured no faster)
         if (nra8 && L.K == 1 && L.MI0 > 128 && L.MI0 <= 256) {
@@ -1163,7 +1163,7 @@ void tile_level(Level& L, int num_sms) {
         // a single small face tile: KO panels per box amortise the per-panel
         // reductions (C4: 60 x 60 faces)
         L.KO = 1;
-        static const char* ko_env = std::getenv("R1_SWEEP_KO");
+        static const char* ko_env = dev_env("R1_SWEEP_KO");
         const int ko_max = ko_env ? std::atoi(ko_env) : 2;  // measured: 2 beats 4 on C4
         if (L.ntiles == 1 && L.r0 * L.t1 <= 64 * 64 && L.nra == 2)
             for (int ko = ko_max; ko > 1; ko >>= 1)
@@ -1212,7 +1212,7 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     double total = 0.0;
     for (int t = 0; t < L.ntiles; ++t) total += panel_cost(t) * static_cast<double>(Og);
     // Enough CTAs to fill the chip, but at least ~min_panels panels each.
-    static const char* mp_env = std::getenv("R1_SWEEP_MIN_PANELS");
+    static const char* mp_env = dev_env("R1_SWEEP_MIN_PANELS");
     // 4 (was 16): the small recursion levels (60^3 at C4) ran on one CTA
     const int64_t min_panels = mp_env ? std::max(1, std::atoi(mp_env)) : 4;
     int64_t ncta = std::min<int64_t>(num_sms, std::max<int64_t>(1, npanels / min_panels));
@@ -1224,7 +1224,7 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     // counter (SM bandwidth shares vary by ~10%; a static split waits for the
     // slowest SM).
     const bool dyn = L.tma && npanels >= static_cast<int64_t>(L.ncta) * 64;
-    static const char* df_env = std::getenv("R1_SWEEP_DYN_FRAC");  // development
+    static const char* df_env = dev_env("R1_SWEEP_DYN_FRAC");  // development
     const double dyn_frac = df_env ? std::atof(df_env) : kDynFrac;
     const double static_total = dyn ? (1.0 - dyn_frac) * total : total;
     const double full_cost = static_cast<double>(L.r0) * L.t1 + 512.0;
@@ -1244,7 +1244,7 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
             }
             if (in_dyn) {
                 // guided chunk size: remaining / (2 ncta), at least kDynMinChunk panels
-                static const char* mc_env = std::getenv("R1_SWEEP_DYN_CHUNK");  // development
+                static const char* mc_env = dev_env("R1_SWEEP_DYN_CHUNK");  // development
                 const double min_chunk = mc_env ? std::atof(mc_env) : kDynMinChunk;
                 const double target = std::max(min_chunk * full_cost,
                                                (total - x) / (2.0 * L.ncta));
@@ -1472,7 +1472,7 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
 template <int NRA, int NCB, int STAGES>
 void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
     if (L.tma) {
-        static const char* sr = std::getenv("R1_SWEEP_STAGE_REGS");
+        static const char* sr = dev_env("R1_SWEEP_STAGE_REGS");
         const bool stage_regs = sr ? std::atoi(sr) != 0 : true;
         if (L.nra == 8) {
             if (stage_regs) launch_box<8, true, 1, 2>(ctx, L, a);
@@ -1580,7 +1580,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.dyn_counter = reinterpret_cast<int*>(P->counters.as<char>() + 64 * level_idx);
         ++level_idx;
         {
-            static const char* dm = std::getenv("R1_DEBUG_SWEEP_MODE");
+            static const char* dm = dev_env("R1_DEBUG_SWEEP_MODE");
             s.debug_mode = dm ? std::atoi(dm) : 0;
         }
         if (L.nra == 4 || L.nra == 8)  // (nra 8: box kernel only)

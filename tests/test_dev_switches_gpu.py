@@ -1,6 +1,7 @@
 """The alternative paths behind the development switches stay
-correct: each runs in a fresh process (the switches are read once) against
-the compiled reference / numpy."""
+correct: each runs in a fresh process (the switches are read once) on the
+DEVELOPMENT build (librank1_b200_dev.so: the release library ignores the
+environment) against the compiled reference / numpy."""
 import os
 import subprocess
 import sys
@@ -17,7 +18,7 @@ sys.path.insert(0, {ROOT!r})
 import paper_2403_01778_b200 as r1
 from oracle import ref
 ctx = r1.default_context()
-# RQI (BK factor + solve, or cuSOLVER) against the reference
+# RQI (BK factor + solve) against the reference
 for n in (40, 333, 700):
     rng = np.random.default_rng(n)
     m = rng.standard_normal((n, n))
@@ -57,10 +58,16 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"R1_RQI_CUSOLVER": "1"}, {"R1_BK_GRID_SOLVE": "1"},
+DEV_LIB = os.path.join(ROOT, "paper_2403_01778_b200", "librank1_b200_dev.so")
+
+
+@pytest.mark.parametrize("env", [{"R1_SOLVER_GRAPHS": "0"}, {"R1_BK_GRID_SOLVE": "1"},
                                  {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"},
                                  {"R1_SWEEP_NRA8": "0"}, {"R1_SWEEP_MERGE": "0"}])
 def test_switch_paths(gpu_ctx, env):
+    if not os.path.exists(DEV_LIB):
+        pytest.skip("development build not present (build.py --dev)")
+    env = dict(env, R1_LIB_PATH=DEV_LIB)
     r = subprocess.run([sys.executable, "-c", CHECK], env=dict(os.environ, **env), capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
