@@ -120,16 +120,21 @@ struct DescCache {
             if (p) cudaFree(p);
         if (host) cudaFreeHost(host);
     }
+    // All slots are allocated on the first (never captured) use, so a miss
+    // while a graph is being captured only records a pinned-host memcpy node.
     const T* get(const T& d, cudaStream_t s) {
-        if (!host) R1_CUDA(cudaMallocHost(&host, N * sizeof(T)));
+        if (!host) {
+            R1_CUDA(cudaMallocHost(&host, N * sizeof(T)));
+            for (int i = 0; i < N; ++i) R1_CUDA(cudaMalloc(&dev[i], sizeof(T)));
+        }
         for (int i = 0; i < N; ++i)
             if (used[i] && std::memcmp(&host[i], &d, sizeof(T)) == 0) return static_cast<T*>(dev[i]);
         const int i = next;
         next = (next + 1) % N;
+        used[i] = false;
         std::memcpy(&host[i], &d, sizeof(T));
-        used[i] = true;
-        if (!dev[i]) R1_CUDA(cudaMalloc(&dev[i], sizeof(T)));
         R1_CUDA(cudaMemcpyAsync(dev[i], &host[i], sizeof(T), cudaMemcpyHostToDevice, s));
+        used[i] = true;
         return static_cast<T*>(dev[i]);
     }
 };

@@ -10,6 +10,7 @@
 #include "solver_ops.cuh"
 
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -236,6 +237,7 @@ struct IterParams {
     double tol, lambda_rtol, angle_tol;
     int max_iters, record_kkt;
     int64_t n;
+    int debug;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -244,8 +246,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-__global__ void stamp_kernel(const IterState* st, DevRecord* trace, int which) {
-    trace[st->counter].t[which] = global_ns();
+__global__ void stamp_kernel(const IterState* st, DevRecord* trace, int cap, int which) {
+    const int k = st->counter;
+    if (k < 0 || k > cap) {
+        printf("[r1] stamp_kernel: iteration slot %d out of range (cap %d)\n", k, cap);
+        __trap();
+    }
+    trace[k].t[which] = global_ns();
 }
 
 __global__ void gate_kernel(const IterState* st, cudaGraphConditionalHandle h) {
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(kRecThreads) record_kernel(IterState* st, DevR
     r.stop_value = post[1];
     r.kkt = prm->record_kkt ? post[2] : __longlong_as_double(0x7ff8000000000000ll);
     r.angle = angle;
+    r.pad = k > 1 ? fabs(lam - trace[k - 2].lambda) / fabs(lam) : -1.0;  // sigma change (diagnostics)
     int status = 0;
     if (r.stop_value <= prm->tol)
         status = 1;
@@ -312,6 +320,9 @@ __global__ void __launch_bounds__(kRecThreads) record_kernel(IterState* st, DevR
     else if (k >= prm->max_iters)
         status = 4;
     r.t[4] = global_ns();
+    if (prm->debug && (k <= 2 || status))
+        printf("[r1 record] k=%d tol=%g lrtol=%g atol=%g max=%d eq11=%g dl=%g angle=%g status=%d\n", k,
+               prm->tol, prm->lambda_rtol, prm->angle_tol, prm->max_iters, r.eq11, r.pad, angle, status);
     st->status = status;
     st->counter = k;
 }
@@ -345,33 +356,47 @@ struct HoscfDev {
 void enqueue_hoscf_iteration(Work& w, HoscfDev& D, int p, bool warm) {
     r1_context* ctx = w.ctx;
     const cudaStream_t st = w.st();
+    static const bool dbg = dev_env("R1_GRAPH_DEBUG") != nullptr;
+    auto note = [&](const char* what) {
+        if (dbg) std::fprintf(stderr, "[r1 iter] p=%d %s\n", p, what);
+    };
     double* Ub[2] = {w.U, w.Umid};
     double* Jb[2] = {w.J, w.Jmid};
     double* fb[2] = {w.fro2, w.fro2mid};
     double* pb[2] = {w.post, w.postmid};
     const int q = p ^ 1;
-    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 0);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 0);
     check_launch(ctx, "stamp_kernel");
+    note("eig");
     eig_blocks(ctx, w.dims.data(), w.d, Jb[p], warm ? w.Xprev : nullptr, w.mu, w.X, nullptr, nullptr,
                true);
-    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 1);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 1);
     check_launch(ctx, "stamp_kernel");
+    note("split");
     split_stack(ctx, w.dims.data(), w.d, w.X, Ub[q], w.Xhat, w.flags);
-    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 2);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 2);
     check_launch(ctx, "stamp_kernel");
+    note("sweep");
     w.sweep(Ub[q], Jb[q], fb[q]);
-    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 3);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 3);
     check_launch(ctx, "stamp_kernel");
+    note("post");
     w.post_step(Jb[q], fb[q], w.Xhat, Ub[q], w.mu, 0.0, pb[q]);
     record_kernel<<<1, kRecThreads, 0, st>>>(D.state, D.trace, D.params, pb[q], w.mu, w.flags, w.X,
                                              w.Xprev);
     check_launch(ctx, "record_kernel");
+    note("done");
 }
 
 // Capture the parity-p iteration as [gate] -> IF(status == 0) {iteration} (or
 // the bare iteration when conditional = false) and instantiate it.
 cudaGraphExec_t capture_iteration(Work& w, HoscfDev& D, int p, bool conditional, uint64_t* launches) {
     const cudaStream_t st = w.st();
+    static const bool dbg = dev_env("R1_GRAPH_DEBUG") != nullptr;
+    auto note = [&](const char* what) {
+        if (dbg) std::fprintf(stderr, "[r1 graph] p=%d cond=%d %s\n", p, conditional ? 1 : 0, what);
+    };
+    note("begin");
     cudaGraph_t g = nullptr;
     R1_CUDA(cudaGraphCreate(&g, 0));
     struct G {
@@ -400,6 +425,7 @@ cudaGraphExec_t capture_iteration(Work& w, HoscfDev& D, int p, bool conditional,
         cudaGraphNode_t cnode;
         R1_CUDA(cudaGraphAddNode(&cnode, g, nodes.data(), nn, &cp));
         body = cp.conditional.phGraph_out[0];
+        note("conditional node added");
     }
     const uint64_t l0 = w.ctx->launches;
     R1_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
@@ -413,10 +439,12 @@ cudaGraphExec_t capture_iteration(Work& w, HoscfDev& D, int p, bool conditional,
     }
     cudaGraph_t cap = nullptr;
     R1_CUDA(cudaStreamEndCapture(st, &cap));
+    note("body captured");
     *launches = w.ctx->launches - l0;
     w.ctx->launches = l0;  // counted per executed replay instead
     cudaGraphExec_t exec = nullptr;
     R1_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    note("instantiated");
     return exec;
 }
 
@@ -430,7 +458,8 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
     HoscfDev& D = *static_cast<HoscfDev*>(w.hd.get());
     D.ensure(o.max_iters);
     // parameters and state (pageable -> synchronous copies, before any capture)
-    IterParams prm{o.tol, o.scf_lambda_rtol, o.scf_angle_tol, o.max_iters, o.record_kkt, n};
+    IterParams prm{o.tol, o.scf_lambda_rtol, o.scf_angle_tol, o.max_iters, o.record_kkt, n,
+                   dev_env("R1_GRAPH_DEBUG") ? 1 : 0};
     IterState s0{0, 0};
     R1_CUDA(cudaMemcpyAsync(D.params, &prm, sizeof(prm), cudaMemcpyHostToDevice, st));
     R1_CUDA(cudaMemcpyAsync(D.state, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
@@ -438,10 +467,10 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
     // lambda0 and J(u0) (the reference's build_j before the loop, solvers.cpp:131-141)
     R1_CUDA(cudaMemcpyAsync(w.U, u0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
     split_stack(ctx, w.dims.data(), d, w.U, nullptr, w.Xhat, w.flags);
-    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 2);  // trace[0].t[2..3]: the initial sweep
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 2);  // trace[0].t[2..3]: the initial sweep
     check_launch(ctx, "stamp_kernel");
     w.sweep(w.U, w.J, w.fro2);
-    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, 3);
+    stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 3);
     check_launch(ctx, "stamp_kernel");
     unsigned long long t_init[2];
     R1_CUDA(cudaMemcpyAsync(t_init, &D.trace[0].t[2], sizeof(t_init), cudaMemcpyDeviceToHost, st));
@@ -456,8 +485,17 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
     rr.lambda0 = h[4];
     const double t_init_sweep = (t_init[1] - t_init[0]) * 1e-9;
 
-    // iterations 2.. : graph replays with the device stop test
+    // iterations 2..kEager: direct launches, one status read each (short solves
+    // never pay for a capture); then graph replays with the device stop test
     int done = hs->counter, status = hs->status;
+    constexpr int kEager = 3;
+    while (status == 0 && done < kEager) {
+        enqueue_hoscf_iteration(w, D, done & 1, true);
+        w.fetch(hs, D.state, 1);
+        w.sync();
+        done = hs->counter;
+        status = hs->status;
+    }
     if (status == 0) {
         bool graphs = true;
         static const char* nog = dev_env("R1_SOLVER_GRAPHS");  // development: 0 = direct launches
@@ -469,8 +507,10 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
                     cudaGraphExecDestroy(e);
                     e = nullptr;
                 }
-            D.conditional = true;
+            static const char* cenv = dev_env("R1_GRAPH_COND");  // development: 0 = plain graphs
+            D.conditional = !(cenv && std::atoi(cenv) == 0);
             try {
+                if (!D.conditional) throw Error(R1_ERR_CUDA, "conditional graphs disabled");
                 D.exec[1] = capture_iteration(w, D, 1, true, &per_iter);
                 D.exec[0] = capture_iteration(w, D, 0, true, &per_iter);
             } catch (const Error&) {
@@ -497,9 +537,17 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
             const int nb = std::min(batch, o.max_iters - k);
             for (int b = 0; b < nb; ++b, ++k) {
                 const int p = k & 1;  // iteration k+1 reads the buffers of parity k & 1
-                if (graphs)
+                if (graphs) {
                     R1_CUDA(cudaGraphLaunch(D.exec[p], st));
-                else
+                    static const bool sync_each = dev_env("R1_GRAPH_SYNC_EACH") != nullptr;
+                    if (sync_each) {
+                        cudaError_t e = cudaStreamSynchronize(st);
+                        if (e != cudaSuccess)
+                            fail(R1_ERR_CUDA, std::string("graph replay of iteration ") +
+                                                  std::to_string(k + 1) + " (parity " + std::to_string(p) +
+                                                  "): " + cudaGetErrorString(e));
+                    }
+                } else
                     enqueue_hoscf_iteration(w, D, p, true);
             }
             w.fetch(hs, D.state, 1);
@@ -508,7 +556,7 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
             done = hs->counter;
             status = hs->status;
             k = done;
-            batch = std::min(batch * 2, 32);
+            if (graphs && D.conditional) batch = std::min(batch * 2, 32);
         }
     }
     if (status == 5)
@@ -552,6 +600,9 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
         rec.n_sweeps = i == 0 ? 2 : 1;
         rec.lambda_pre_rqi = std::numeric_limits<double>::quiet_NaN();
         rec.factor_change = q.angle;
+        if (dev_env("R1_GRAPH_DEBUG") && i >= done - 30)
+            std::fprintf(stderr, "[r1 trace] k=%d lambda=%.17g dl/l=%.6e angle=%.3e\n", i + 1, q.lambda,
+                         q.pad, q.angle);
         rec.t_eig = (q.t[1] - q.t[0]) * 1e-9;
         rec.t_build_j = (q.t[3] - q.t[2]) * 1e-9 + (i == 0 ? t_init_sweep : 0.0);
         rec.t_other = (q.t[2] - q.t[1]) * 1e-9 + (q.t[4] - q.t[3]) * 1e-9;
@@ -1003,7 +1054,9 @@ static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* 
                                                    : Baseline::jacobi_asvd;
         auto go = [&](const std::vector<double>& u0) {
             if (baseline) return run_baseline(w, *opts, u0, bk);
-            return acc ? run(w, *opts, u0, true) : run_hoscf_dev(w, *opts, u0);
+            static const char* host_loop = dev_env("R1_HOSCF_HOST_LOOP");  // development A/B
+            if (acc || (host_loop && std::atoi(host_loop) != 0)) return run(w, *opts, u0, acc);
+            return run_hoscf_dev(w, *opts, u0);
         };
         try {
             rr = go(initial_factors(a, *opts));

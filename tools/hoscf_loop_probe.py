@@ -22,7 +22,8 @@ L = _lib.lib()
 for cfg, dims, kw in ((1, (100, 100, 100), dict(tol=1e-300, max_iters=500, init="provided",
                                                  scf_lambda_rtol=1e-12, record_kkt=False)),
                       (4, (60, 60, 60, 60, 60), dict(tol=1e-10, max_iters=100, seed=4)),
-                      (2, (1000, 1000, 1000), dict(tol=1e-10, max_iters=100, seed=2))):
+                      (2, (1000, 1000, 1000), dict(tol=1e-10, max_iters=100, seed=2)))[
+                          :int(os.environ.get("PROBE_NCFG", "3"))]:
     n = int(np.prod(dims))
     a = torch.empty(n + 2, dtype=torch.float64, device="cuda")
     t = r1.DeviceTensor.wrap(a.data_ptr(), dims, ctx, keepalive=a)
@@ -46,5 +47,8 @@ for cfg, dims, kw in ((1, (100, 100, 100), dict(tol=1e-300, max_iters=500, init=
                       "seconds": [round(x, 5) for x in runs], "t_eig": rep.wall_eig(),
                       "t_build_j": rep.wall_build_j(), "t_total_trace": rep.wall_total(),
                       "factor_change_last": rep.trace[-1].factor_change}), flush=True)
+    if os.environ.get("PROBE_TRACE"):
+        print(json.dumps({"cfg": cfg, "trace_lambda": [r.lambda_ for r in rep.trace][:40],
+                          "trace_eq11": [r.eq11_value for r in rep.trace][:40]}), flush=True)
     del t, a
     torch.cuda.empty_cache()
