@@ -230,7 +230,8 @@ def run_b200(args):
 
     import paper_2403_01778_b200 as r1
     from paper_2403_01778_b200 import _lib
-    from paper_2403_01778_b200.distributed import exchange, local_dims, slab_bounds
+    from paper_2403_01778_b200.distributed import (build_j_sharded, init_comm, local_dims,
+                                                   slab_bounds, solve_distributed)
 
     world, rank, local, dist = init_dist(args.gpus)
     torch.cuda.set_device(local)
@@ -253,20 +254,21 @@ def run_b200(args):
     gdims = _lib.dims_arr(dims)
     _lib.check(L.r1_generate_config(ctx.handle, t.handle, HEAD_CFG, HEAD_SEED, _lib.u64p(gdims), d,
                                     first))
-    # factors: the solver's uniform01 init (solvers.cpp:34-49), sliced for the slab
+    # factors: the solver's uniform01 init (solvers.cpp:34-49); a slab's sweep
+    # reads its slice of the global last factor in place
     fac_full = uniform01_factors(dims, seed=HEAD_SEED)
-    fl = np.concatenate(fac_full[:-1] + [fac_full[-1][lo:hi]])
+    fl = np.concatenate(fac_full)
     fac = torch.from_numpy(fl).cuda()
-    nb_local = int(sum(ldims[m] * ldims[k] for m in range(d) for k in range(m + 1, d)))
     nb = int(sum(dims[m] * dims[k] for m in range(d) for k in range(m + 1, d)))
-    lblocks = torch.empty(nb_local, dtype=torch.float64, device="cuda")
-    gblocks = torch.empty(nb, dtype=torch.float64, device="cuda") if world > 1 else lblocks
+    gblocks = torch.empty(nb, dtype=torch.float64, device="cuda")
+    comm = init_comm(ctx, dist, world, rank) if world > 1 else None
 
     def step():
-        _lib.check(L.r1_build_j_device(ctx.handle, t.handle, fac.data_ptr(), lblocks.data_ptr(),
-                                       None))
-        if world > 1:
-            exchange(lblocks, dims, world, rank, dist, gblocks)
+        if world > 1:  # slab sweep + one NCCL group (r1_build_j_sharded)
+            build_j_sharded(ctx, t, dims, fac.data_ptr(), gblocks.data_ptr())
+        else:
+            _lib.check(L.r1_build_j_device(ctx.handle, t.handle, fac.data_ptr(), gblocks.data_ptr(),
+                                           None))
 
     def barrier():
         if dist is not None:
@@ -325,8 +327,8 @@ def run_b200(args):
             step()
             blocks_host.copy_(gblocks, non_blocking=True)
             stream.synchronize()
-        e2e_path = ("per rank: pinned host slab H2D + factors H2D + slab sweep + NCCL exchange + "
-                    "blocks D2H per step")
+        e2e_path = ("per rank: pinned host slab H2D + factors H2D + r1_build_j_sharded (slab "
+                    "sweep + NCCL exchange) + blocks D2H per step")
 
     e2e_step()
     torch.cuda.synchronize()
@@ -363,7 +365,6 @@ def run_b200(args):
     # RQI / stopping test)
     ttc = None
     if not args.skip_solve:
-        from paper_2403_01778_b200.distributed import solve_distributed
         ttc = {}
 
         def ttc_one(alg):
@@ -376,7 +377,7 @@ def run_b200(args):
                 if world == 1:
                     rep = r1.solve(alg, t, o, ctx)
                 else:
-                    rep = solve_distributed(alg, t, dims, o, dist, world, rank, ctx)
+                    rep = solve_distributed(alg, t, dims, o, ctx)
                 torch.cuda.synchronize()
                 runs.append(max_over_ranks(time.perf_counter() - ts, dist))
             return {"seconds": round(statistics.median(runs[1:]), 6),
@@ -437,8 +438,9 @@ def run_b200(args):
             "data": "synthetic (BASELINE config 5, generated in HBM by the counter-based "
                     "generator; the reference arm generates the same config on the host)",
             "config": dict(head_config(),
-                           parallelism=(f"slab{world} along the slowest mode (NCCL all-reduce + "
-                                        "all-gather)") if world > 1 else "single GPU"),
+                           parallelism=(f"slab{world} along the slowest mode (r1_build_j_sharded: "
+                                        "NCCL all-reduce + all-gather in one group)")
+                           if world > 1 else "single GPU"),
             "roofline": {
                 "bound": "hbm",
                 "kernel": "the whole sweep: sweep3_box_kernel (fused top-level pass) + "
@@ -483,6 +485,8 @@ def run_b200(args):
         if cpu is not None:
             out["cpu_baseline"] = cpu
         emit(out)
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

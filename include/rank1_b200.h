@@ -55,6 +55,7 @@ extern "C" {
 
 typedef struct r1_context r1_context; /* device, stream, events, workspaces   */
 typedef struct r1_tensor r1_tensor;   /* a dense order-d tensor resident in HBM */
+typedef struct r1_comm r1_comm;       /* NCCL communicator of a sharded tensor's ranks */
 
 /* Mirrors rank1::SolveOptions (solvers.hpp:17-31), same defaults via
  * r1_solve_options_default().  `init_factors` is flat (sum I_k) or NULL. */
@@ -290,6 +291,38 @@ int r1_rank_one_expand(r1_context* ctx, double lambda, const double* factors_hos
 int r1_residual_norm(r1_context* ctx, const double* a_host, const uint64_t* dims, int order,
                      double lambda, const double* factors_host, uint64_t dense_threshold,
                      double* out_norm);
+
+/* ---- multi-GPU: slabs along the last (slowest) mode over NCCL ----------------
+ * SURVEY §8e.  Rank r of W holds the slab [lo_r, hi_r) of the last mode
+ * (sizes differ by at most one, larger first) as an ordinary r1_tensor of dims
+ * (I_0, ..., I_{d-2}, hi_r - lo_r).  Per sweep the partial blocks (m, n < d-1)
+ * are all-reduced and the blocks (m, d-1) gathered in place, all in one NCCL
+ * group; the eigen step / RQI / stopping test run replicated on identical
+ * bits.  NCCL is loaded at run time (libnccl.so.2). */
+#define R1_COMM_ID_BYTES 128
+/* A fresh NCCL unique id (rank 0 makes it; the caller ships it to the others). */
+int r1_comm_unique_id(void* id_out);
+/* One process (or thread) per GPU: join communicator `id` as `rank` of `nranks`
+ * and attach it to ctx. */
+int r1_comm_init(r1_context* ctx, int nranks, int rank, const void* id, r1_comm** out);
+/* One process for ndev GPUs: ctxs[i] on devices[i] (created by the caller);
+ * comms[i] attached to ctxs[i]. */
+int r1_comm_init_all(int ndev, const int* devices, r1_context** ctxs, r1_comm** comms);
+int r1_comm_destroy(r1_comm* c);
+int r1_comm_info(const r1_comm* c, int* world, int* rank);
+/* [lo, hi) of `rank`'s slab of an extent split over `world` ranks. */
+int r1_slab_bounds(uint64_t extent, int world, int rank, uint64_t* lo, uint64_t* hi);
+/* The sweep of a sharded tensor: `slab` is this rank's slab, `global_dims` the
+ * whole tensor's, factors_dev the GLOBAL flat factors, blocks_dev / fro2_dev
+ * the GLOBAL blocks (identical on every rank on return).  Needs the context's
+ * communicator (r1_comm_init*). */
+int r1_build_j_sharded(r1_context* ctx, const r1_tensor* slab, const uint64_t* global_dims, int order,
+                       const double* factors_dev, double* blocks_dev, double* fro2_dev);
+/* hoscf / ihoscf on a sharded tensor: every rank calls it with its slab; the
+ * reports (global factors, trace) are identical on all ranks. */
+int r1_solve_sharded(r1_context* ctx, const char* algorithm, const r1_tensor* slab,
+                     const uint64_t* global_dims, int order, const r1_solve_options* opts,
+                     r1_solve_report* report);
 
 /* ---- synthetic inputs ----------------------------------------------------------- */
 /* Fill `t` with elements [first, first + numel(t)) of BASELINE config `cfg`

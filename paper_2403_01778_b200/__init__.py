@@ -617,10 +617,14 @@ def _options_c(o: SolveOptions, dims):
     return c, keep
 
 
-def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None) -> SolveReport:
+def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None,
+          global_dims=None) -> SolveReport:
     """solvers.hpp:86: every solver of the reference on the device —
     hoscf | ihoscf (SCF on J(u)) and the baselines hopm | jacobi_hopm | asvd |
-    jacobi_asvd (solvers.cpp:299-447) on the same device sweep."""
+    jacobi_asvd (solvers.cpp:299-447) on the same device sweep.
+
+    global_dims: `a` is this rank's slab of a tensor sharded along its last mode
+    (r1_solve_sharded; the context needs a communicator, distributed.init_comm)."""
     ctx = ctx or default_context()
     if algorithm not in _SOLVERS:
         raise InvalidArgument("unknown solver: " + algorithm)
@@ -632,7 +636,7 @@ def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None) 
         t = owned
     else:
         t = a
-    dims = list(t.dims)
+    dims = list(t.dims) if global_dims is None else [int(v) for v in global_dims]
     c, keep = _options_c(opts, dims)
     n = sum(dims)
     fac = np.empty(n)
@@ -643,8 +647,13 @@ def solve(algorithm: str, a, opts: SolveOptions, ctx: Optional[Context] = None) 
     r.final_x = dptr(fx)
     r.trace = tr
     try:
-        check(lib().r1_solve(ctx.handle, algorithm.encode(), t.handle, ctypes.byref(c),
-                             ctypes.byref(r)))
+        if global_dims is None:
+            check(lib().r1_solve(ctx.handle, algorithm.encode(), t.handle, ctypes.byref(c),
+                                 ctypes.byref(r)))
+        else:
+            gd = _lib.dims_arr(dims)
+            check(lib().r1_solve_sharded(ctx.handle, algorithm.encode(), t.handle, _lib.u64p(gd),
+                                         len(dims), ctypes.byref(c), ctypes.byref(r)))
     finally:
         if owned is not None:
             owned.close()

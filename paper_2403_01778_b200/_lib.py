@@ -124,6 +124,16 @@ SIGNATURES = {
                                 ctypes.POINTER(SolveReportC)]),
     "r1_solve_host": (ctypes.c_int, [_vp, ctypes.c_char_p, _dp, _u64p, ctypes.c_int,
                                      ctypes.POINTER(SolveOptionsC), ctypes.POINTER(SolveReportC)]),
+    "r1_comm_unique_id": (ctypes.c_int, [_vp]),
+    "r1_comm_init": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
+    "r1_comm_init_all": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "r1_comm_destroy": (ctypes.c_int, [_vp]),
+    "r1_comm_info": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "r1_slab_bounds": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u64p, _u64p]),
+    "r1_build_j_sharded": (ctypes.c_int, [_vp, _vp, _u64p, ctypes.c_int, _vp, _vp, _vp]),
+    "r1_solve_sharded": (ctypes.c_int, [_vp, ctypes.c_char_p, _vp, _u64p, ctypes.c_int,
+                                        ctypes.POINTER(SolveOptionsC), ctypes.POINTER(SolveReportC)]),
     "r1_greedy_rank_r": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, ctypes.c_char_p,
                                         ctypes.POINTER(SolveOptionsC), ctypes.POINTER(GreedyReportC)]),
     "r1_rank_one_subtract": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _dp, _dp]),
@@ -154,6 +164,8 @@ EXTRA_SIGNATURES = {
                                            ctypes.POINTER(ctypes.c_int), _dp]),
     "r1x_sweep_plan_info": (ctypes.c_int, [_vp, _u64p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_int64)]),
+    "r1x_exchange_plan": (ctypes.c_int, [_u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     "r1x_solver_graph_mode": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     "r1x_eig_dense_lanczos": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp]),
     "r1x_ldlt": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.POINTER(ctypes.c_int), _dp, _dp,

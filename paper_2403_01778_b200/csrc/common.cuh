@@ -197,6 +197,14 @@ void configure_once(const void* key, int device, F&& f) {
 
 }  // namespace r1
 
+// An NCCL communicator of the ranks sharing a sharded tensor (comm.cu).
+struct r1_comm {
+    void* comm = nullptr;  // ncclComm_t
+    int world = 1;
+    int rank = 0;
+    bool owns = true;
+};
+
 struct r1_tensor {
     r1_context* ctx = nullptr;
     std::vector<uint64_t> dims;
@@ -225,9 +233,11 @@ struct r1_context {
     // host-buffer entry points (host_io.cu): device copy of the caller's
     // tensor, its view, factor / block buffers, pinned staging lanes
     r1::DeviceBuffer ws_upload;
+    r1::DeviceBuffer ws_xchg;    // local slab blocks of r1_build_j_sharded
     r1::DeviceBuffer ws_io;
     r1_tensor upload_view;
     r1::HostStaging staging;
+    r1_comm* comm = nullptr;  // attached communicator (sharded sweeps / solves)
     // diagnostics: how the last HOSCF solve drove its loop (0 direct launches,
     // 1 CUDA-graph replays, 2 graph replays behind conditional IF nodes)
     int solver_graph_mode = -1;
@@ -286,12 +296,25 @@ struct CtxLock {
 };
 
 // --------------------------------------------------------- component APIs --
+// comm.cu: slabs along the last mode and the per-sweep block exchange
+struct ExchangeOp {
+    int m, n;
+    uint64_t local_off, global_off, local_count, rows;
+    int gathered;  // 1: (m, d-1) columns gathered, 0: partial block all-reduced
+};
+void slab_bounds(uint64_t extent, int world, int rank, uint64_t* lo, uint64_t* hi);
+void exchange_plan(const uint64_t* gdims, int order, int world, int rank, std::vector<ExchangeOp>& ops);
+void exchange_blocks(r1_context* ctx, const double* lblocks, double* gblocks, const uint64_t* gdims,
+                     int order);
 // host_io.cu
 void h2d_bytes(r1_context* ctx, void* dst, const void* src, size_t bytes);
 const r1_tensor* upload_tensor(r1_context* ctx, const double* host, const uint64_t* dims, int order);
 // sweep.cu
+// last_factor (nullable): read the last mode's factor from there instead of
+// factors_dev + sum_{k<d-1} I_k (a slab of a tensor sharded along its last mode)
 void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int order,
-                  const double* factors_dev, double* blocks_dev);
+                  const double* factors_dev, double* blocks_dev,
+                  const double* last_factor = nullptr);
 // blockops.cu
 void sumsq_device(r1_context* ctx, const double* x, uint64_t n, double* out_dev);
 void block_matvec(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,

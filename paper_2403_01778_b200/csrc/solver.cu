@@ -108,11 +108,16 @@ struct Events {
 // Device working set of one solve.
 struct Work {
     r1_context* ctx;
-    const r1_tensor* A;
-    std::vector<uint64_t> dims;
+    const r1_tensor* A;         // the tensor, or this rank's slab of a sharded one
+    std::vector<uint64_t> dims; // GLOBAL dims (J, factors and all vectors use these)
     int d;
     int64_t n;     // sum I_k
     uint64_t nb;   // block entries
+    // sharded along the last mode (comm.cu): the slab [lo, hi) and its local blocks
+    bool sharded = false;
+    std::vector<uint64_t> ldims;
+    uint64_t lo = 0, hi = 0;
+    DeviceBuffer lblocks;
     DeviceBuffer mem;
     double *U, *Umid, *Urqi, *X, *Xprev, *Xhat, *XhatR, *Yr, *Y, *J, *Jmid, *S;
     double *fro2, *fro2mid, *mu, *post, *postmid, *dotv;
@@ -121,8 +126,24 @@ struct Work {
     std::shared_ptr<void> hd;  // HoscfDev (device-loop state), created on first use
     Events events;             // phase-timing events (iHOSCF / baselines), reused
 
-    Work(r1_context* c, const r1_tensor* a, bool dense)
+    Work(r1_context* c, const r1_tensor* a, bool dense, const uint64_t* gdims = nullptr)
         : ctx(c), A(a), dims(a->dims), d(static_cast<int>(a->dims.size())) {
+        if (gdims) {
+            sharded = true;
+            ldims = a->dims;
+            dims.assign(gdims, gdims + d);
+            const r1_comm* cm = c->comm;
+            if (dims[d - 1] < static_cast<uint64_t>(cm->world))
+                fail(R1_ERR_INVALID_ARGUMENT, "sharded solve: the last mode has fewer entries (" +
+                                                  std::to_string(dims[d - 1]) + ") than ranks (" +
+                                                  std::to_string(cm->world) + ")");
+            slab_bounds(dims[d - 1], cm->world, cm->rank, &lo, &hi);
+            if (hi - lo != ldims[d - 1])
+                fail(R1_ERR_INVALID_ARGUMENT, "sharded solve: slab extent does not match this rank's share");
+            for (int k = 0; k + 1 < d; ++k)
+                if (ldims[k] != dims[k]) fail(R1_ERR_INVALID_ARGUMENT, "sharded solve: slab dims mismatch");
+            lblocks.ensure((blocks_numel(ldims.data(), d) + 32) * sizeof(double));
+        }
         n = 0;
         for (auto v : dims) n += static_cast<int64_t>(v);
         nb = blocks_numel(dims.data(), d);
@@ -162,8 +183,16 @@ struct Work {
 
     cudaStream_t st() const { return ctx->stream; }
 
+    // J(u) of the whole tensor: one fused pass (sharded: over this rank's slab,
+    // reading its slice of the last factor, then the NCCL block exchange)
     void sweep(const double* u, double* jb, double* f2) {
-        sweep_blocks(ctx, A->dev, dims.data(), d, u, jb);
+        if (sharded) {
+            const double* last = u + (n - static_cast<int64_t>(dims[d - 1])) + lo;
+            sweep_blocks(ctx, A->dev, ldims.data(), d, u, lblocks.as<double>(), last);
+            exchange_blocks(ctx, lblocks.as<double>(), jb, dims.data(), d);
+        } else {
+            sweep_blocks(ctx, A->dev, dims.data(), d, u, jb);
+        }
         sumsq_device(ctx, jb, nb, f2);
     }
     // y = J xhat, then Eq.11 / KKT / lambda into out (see solver_ops.cu)
@@ -186,12 +215,17 @@ std::map<std::pair<r1_context*, std::vector<uint64_t>>, std::shared_ptr<Work>>& 
     return m;
 }
 
-Work& work_for(r1_context* ctx, const r1_tensor* a, bool dense) {
+Work& work_for(r1_context* ctx, const r1_tensor* a, bool dense, const uint64_t* gdims = nullptr) {
     std::vector<uint64_t> key = a->dims;
     key.push_back(dense ? 1 : 0);
+    if (gdims) {  // sharded: the global dims and the communicator shape are part of the key
+        key.insert(key.end(), gdims, gdims + a->dims.size());
+        key.push_back(static_cast<uint64_t>(ctx->comm->world));
+        key.push_back(static_cast<uint64_t>(ctx->comm->rank));
+    }
     std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& w = work_cache()[{ctx, key}];
-    if (!w) w = std::make_shared<Work>(ctx, a, dense);
+    if (!w) w = std::make_shared<Work>(ctx, a, dense, gdims);
     w->A = a;
     return *w;
 }
@@ -500,6 +534,7 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
         bool graphs = true;
         static const char* nog = dev_env("R1_SOLVER_GRAPHS");  // development: 0 = direct launches
         if (nog && std::atoi(nog) == 0) graphs = false;
+        if (w.sharded) graphs = false;  // NCCL exchange inside the iteration: direct launches
         uint64_t per_iter = 0;
         if (graphs) {
             for (auto& e : D.exec)
@@ -964,22 +999,22 @@ RunResult run_baseline(Work& w, const r1_solve_options& o, const std::vector<dou
     return rr;
 }
 
-std::vector<double> initial_factors(const r1_tensor* a, const r1_solve_options& o) {
-    const int d = static_cast<int>(a->dims.size());
+std::vector<double> initial_factors(const std::vector<uint64_t>& dims, const r1_solve_options& o) {
+    const int d = static_cast<int>(dims.size());
     if (o.init == R1_INIT_PROVIDED) {
         if (!o.init_factors) fail(R1_ERR_INVALID_ARGUMENT, "solver: provided init has wrong order");
         uint64_t n = 0;
-        for (auto v : a->dims) n += v;
+        for (auto v : dims) n += v;
         std::vector<double> f(o.init_factors, o.init_factors + n);
         uint64_t off = 0;
         for (int k = 0; k < d; ++k) {
-            if (normalize(f.data() + off, a->dims[k]) == 0.0)
+            if (normalize(f.data() + off, dims[k]) == 0.0)
                 fail(R1_ERR_INVALID_ARGUMENT, "solver: provided init factor is zero");
-            off += a->dims[k];
+            off += dims[k];
         }
         return f;
     }
-    return random_unit_factors(a->dims, o.seed, kStreamInit);
+    return random_unit_factors(dims, o.seed, kStreamInit);
 }
 
 }  // namespace
@@ -1001,7 +1036,8 @@ using namespace r1;
 extern "C" {
 
 static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* a,
-                       const r1_solve_options* opts, r1_solve_report* report);
+                       const r1_solve_options* opts, r1_solve_report* report,
+                       const uint64_t* gdims = nullptr);
 
 int r1_solve(r1_context* ctx, const char* algorithm, const r1_tensor* a,
              const r1_solve_options* opts, r1_solve_report* report) {
@@ -1028,10 +1064,53 @@ int r1_solve_host(r1_context* ctx, const char* algorithm, const double* a_host,
     });
 }
 
+int r1_solve_sharded(r1_context* ctx, const char* algorithm, const r1_tensor* slab,
+                     const uint64_t* global_dims, int order, const r1_solve_options* opts,
+                     r1_solve_report* report) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !slab || !global_dims) fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        if (!ctx->comm) fail(R1_ERR_INVALID_ARGUMENT, "sharded solve: no communicator attached");
+        if (order != static_cast<int>(slab->dims.size()))
+            fail(R1_ERR_INVALID_ARGUMENT, "sharded solve: order mismatch");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        solve_impl(ctx, algorithm, slab, opts, report, global_dims);
+    });
+}
+
+int r1_build_j_sharded(r1_context* ctx, const r1_tensor* slab, const uint64_t* global_dims, int order,
+                       const double* factors_dev, double* blocks_dev, double* fro2_dev) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || !slab || !global_dims || !factors_dev || !blocks_dev)
+            fail(R1_ERR_INVALID_ARGUMENT, "null argument");
+        if (!ctx->comm) fail(R1_ERR_INVALID_ARGUMENT, "sharded sweep: no communicator attached");
+        if (order < 2 || order != static_cast<int>(slab->dims.size()))
+            fail(R1_ERR_INVALID_ARGUMENT, "sharded sweep: order mismatch");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        if (global_dims[order - 1] < static_cast<uint64_t>(ctx->comm->world))
+            fail(R1_ERR_INVALID_ARGUMENT, "sharded sweep: the last mode has fewer entries than ranks");
+        uint64_t lo, hi;
+        slab_bounds(global_dims[order - 1], ctx->comm->world, ctx->comm->rank, &lo, &hi);
+        if (hi - lo != slab->dims[order - 1])
+            fail(R1_ERR_INVALID_ARGUMENT, "sharded sweep: slab extent does not match this rank's share");
+        // local blocks in the context's sweep-exchange buffer
+        const uint64_t lnb = blocks_numel(slab->dims.data(), order);
+        ctx->ws_xchg.ensure((lnb + 32) * sizeof(double));
+        uint64_t off = 0;
+        for (int k = 0; k + 1 < order; ++k) off += global_dims[k];
+        sweep_blocks(ctx, slab->dev, slab->dims.data(), order, factors_dev, ctx->ws_xchg.as<double>(),
+                     factors_dev + off + lo);
+        exchange_blocks(ctx, ctx->ws_xchg.as<double>(), blocks_dev, global_dims, order);
+        if (fro2_dev) sumsq_device(ctx, blocks_dev, blocks_numel(global_dims, order), fro2_dev);
+    });
+}
+
 }  // extern "C"
 
 static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* a,
-                       const r1_solve_options* opts, r1_solve_report* report) {
+                       const r1_solve_options* opts, r1_solve_report* report,
+                       const uint64_t* gdims) {
     {
         const std::string alg = algorithm ? algorithm : "";
         const bool baseline =
@@ -1045,7 +1124,9 @@ static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* 
         if (opts->max_iters < 1) fail(R1_ERR_INVALID_ARGUMENT, "solver: max_iters must be >= 1");
         const bool acc = alg == "ihoscf";
         auto t0 = std::chrono::steady_clock::now();
-        Work& w = work_for(ctx, a, acc);
+        if (gdims && baseline)
+            fail(R1_ERR_INVALID_ARGUMENT, "sharded solves support hoscf and ihoscf: " + alg);
+        Work& w = work_for(ctx, a, acc, gdims);
         RunResult rr;
         bool restarted = false;
         const Baseline bk = alg == "hopm"          ? Baseline::hopm
@@ -1059,10 +1140,10 @@ static void solve_impl(r1_context* ctx, const char* algorithm, const r1_tensor* 
             return run_hoscf_dev(w, *opts, u0);
         };
         try {
-            rr = go(initial_factors(a, *opts));
+            rr = go(initial_factors(w.dims, *opts));
         } catch (const Degenerate&) {
             try {
-                rr = go(random_unit_factors(a->dims, opts->seed, kStreamRestart));
+                rr = go(random_unit_factors(w.dims, opts->seed, kStreamRestart));
                 restarted = true;
             } catch (const Degenerate& e) {
                 fail(R1_ERR_RUNTIME, std::string("solver failed after restart: ") + e.what());

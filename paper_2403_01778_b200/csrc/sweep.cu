@@ -1505,7 +1505,7 @@ int grid_for(int64_t n, int threads, int num_sms) {
 }  // namespace
 
 void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int order,
-                  const double* factors_dev, double* blocks_dev) {
+                  const double* factors_dev, double* blocks_dev, const double* last_factor) {
     if (order < 2 || order > kMaxOrder) fail(R1_ERR_INVALID_ARGUMENT, "sweep: unsupported order");
     const uint64_t n = numel_of(dims, order);
     if (order == 2) {
@@ -1521,6 +1521,11 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
     uint64_t foff[kMaxOrder + 1];
     foff[0] = 0;
     for (int k = 0; k < order; ++k) foff[k + 1] = foff[k] + dims[k];
+    // factor of mode k; a slab of a sharded tensor reads its slice of the
+    // global last factor in place (last_factor)
+    auto fac = [&](int k) -> const double* {
+        return (k == order - 1 && last_factor) ? last_factor : factors_dev + foff[k];
+    };
 
     auto resolve = [&](const Ref& r) -> double* {
         switch (r.where) {
@@ -1539,7 +1544,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         oa.nout = L.order - 2;
         for (int k = 2; k < L.order; ++k) {
             oa.dims[k - 2] = L.dims[k];
-            oa.u[k - 2] = factors_dev + foff[L.modes[k]];
+            oa.u[k - 2] = fac(L.modes[k]);
         }
         oa.O = L.O;
         oa.W = resolve(L.w);
@@ -1559,8 +1564,8 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.K = L.K;
         s.MI0 = L.MI0;
         s.MI1 = L.MI1;
-        s.u0 = factors_dev + foff[L.modes[0]];
-        s.u1 = factors_dev + foff[L.modes[1]];
+        s.u0 = fac(L.modes[0]);
+        s.u1 = fac(L.modes[1]);
         s.W = Wsrc;
         s.r0 = L.r0;
         s.t1 = L.t1;

@@ -1,8 +1,9 @@
 """The N > 1 path on CPU: world_size-2 (and 3, uneven slabs) gloo process
-groups run the real slab exchange (paper_2403_01778_b200.distributed.exchange:
-all-reduce of partial blocks, all-gather of blocks touching the sharded mode)
-on per-rank local blocks computed by the oracle for each rank's slab; the
-assembled blocks must equal the oracle's blocks of the whole tensor."""
+groups execute the library's exchange plan (r1x_exchange_plan, csrc/comm.cu —
+the same all-reduces and per-root column-run broadcasts the library issues
+through NCCL) on per-rank local blocks computed by the oracle for each rank's
+slab; the assembled blocks must equal the oracle's blocks of the whole tensor,
+bit-identical on every rank."""
 import os
 import socket
 
@@ -25,7 +26,7 @@ def _worker(rank, world, port, dims, seed, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import rank1_oracle as O
-        from paper_2403_01778_b200.distributed import exchange, local_dims, slab_bounds
+        from paper_2403_01778_b200.distributed import exchange_torch, local_dims, slab_bounds
         a = O.oracle_random_tensor(dims, seed).reshape(dims, order="F")
         f = O.oracle_random_unit_factors(dims, seed + 1)
         lo, hi = slab_bounds(dims[-1], world, rank)
@@ -35,7 +36,7 @@ def _worker(rank, world, port, dims, seed, q):
         local = torch.from_numpy(O.build_j_numpy(slab, ld, fl))
         nb = sum(dims[m] * dims[n] for m in range(len(dims)) for n in range(m + 1, len(dims)))
         out = torch.zeros(nb, dtype=torch.float64)
-        exchange(local, dims, world, rank, dist, out)
+        exchange_torch(local, dims, world, rank, dist, out)
         q.put((rank, out.numpy()))
     finally:
         dist.destroy_process_group()
@@ -91,11 +92,33 @@ def test_exchange_numpy_reference():
                                O.build_j_numpy(a.reshape(-1, order="F"), dims, f), rtol=1e-12, atol=1e-12)
 
 
-def test_driver_init_factors_match_reference():
-    """The distributed driver's uniform01 init (solvers.cpp:34-49) equals the
-    oracle's (pinned to the reference)."""
-    from oracle import rank1_oracle as O
-    from paper_2403_01778_b200.distributed import random_unit_factors
-    for dims, seed in [((4, 5, 6), 3), ((10, 2), 0)]:
-        for a, b in zip(random_unit_factors(dims, seed, 2), O.random_unit_factors(dims, seed, 2)):
-            np.testing.assert_allclose(a, b, rtol=1e-15)
+def test_slab_bounds_match_library():
+    import ctypes
+
+    from paper_2403_01778_b200 import _lib
+    from paper_2403_01778_b200.distributed import slab_bounds
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    for extent in (3, 60, 125, 4000):
+        for world in (1, 2, 3, 8):
+            for r in range(world):
+                _lib.check(_lib.lib().r1_slab_bounds(extent, world, r, ctypes.byref(lo), ctypes.byref(hi)))
+                assert (lo.value, hi.value) == slab_bounds(extent, world, r)
+
+
+def test_exchange_plan_layout():
+    """Local offsets follow the slab's own pair order, global offsets the whole
+    tensor's; gathered blocks are exactly the pairs (m, d-1)."""
+    from paper_2403_01778_b200.distributed import exchange_plan, local_dims, pairs, slab_bounds
+    dims = (4, 3, 5, 11)
+    for world in (1, 2, 4):
+        for r in range(world):
+            lo, hi = slab_bounds(dims[-1], world, r)
+            ld = local_dims(dims, lo, hi)
+            ops = exchange_plan(dims, world, r)
+            loff = goff = 0
+            for op, (m, n) in zip(ops, pairs(4)):
+                assert (op.m, op.n) == (m, n) and op.gathered == (n == 3)
+                assert op.local_off == loff and op.global_off == goff
+                assert op.local_count == ld[m] * ld[n]
+                loff += ld[m] * ld[n]
+                goff += dims[m] * dims[n]
