@@ -522,7 +522,7 @@ RunResult run_hoscf_dev(Work& w, const r1_solve_options& o, const std::vector<do
     // iterations 2..kEager: direct launches, one status read each (short solves
     // never pay for a capture); then graph replays with the device stop test
     int done = hs->counter, status = hs->status;
-    constexpr int kEager = 3;
+    constexpr int kEager = 6;
     while (status == 0 && done < kEager) {
         enqueue_hoscf_iteration(w, D, done & 1, true);
         w.fetch(hs, D.state, 1);

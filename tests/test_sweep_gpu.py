@@ -120,7 +120,7 @@ MERGE_SHAPES = [(20, 8, 5), (200, 10, 7), (500, 8, 3), (60, 60, 9), (1000, 4, 3)
 def test_build_j_merged_classes_forced():
     """Every merged-alignment-class configuration (R1_SWEEP_MERGE=2 forces the
     merged view whenever legal, including tiles holding up to 4 classes) in a
-    fresh process, against the oracle."""
+    fresh process on the development build, against the oracle."""
     import os
     import subprocess
     import sys
@@ -142,7 +142,11 @@ for dims in {MERGE_SHAPES!r}:
     assert err <= 1e-13, (dims, err)
 print("ok")
 """
-    env = dict(os.environ, R1_SWEEP_MERGE="2")
+    dev_lib = os.path.join(root, "paper_2403_01778_b200", "librank1_b200_dev.so")
+    if not os.path.exists(dev_lib):
+        pytest.skip("development build not present (build.py --dev)")
+    # the switch exists only in the development build
+    env = dict(os.environ, R1_SWEEP_MERGE="2", R1_LIB_PATH=dev_lib)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
