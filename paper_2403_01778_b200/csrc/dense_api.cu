@@ -698,6 +698,21 @@ size_t sym_eig_ws_doubles(int64_t n) { return static_cast<size_t>(n) * n + 4 * n
 
 }  // namespace
 
+// largest_magnitude_eigenpair (sym_eig.cpp:206-229) of a DEVICE dense matrix
+// S (n x n, overwritten) with the reference's own algorithm, asynchronous:
+// value_dev[0], vec_dev[0..n).  ws: 4n + 16 doubles.  (Used by the solvers'
+// eigen step for small operators when selected; non-convergence of QL leaves
+// the status word in ws[4n+4] nonzero.)
+void eig_dense_reference_device(r1_context* ctx, int64_t n, double* S, double* ws, double* value_dev,
+                                double* vec_dev) {
+    int* status = reinterpret_cast<int*>(ws + 4 * n + 4);
+    SymEigArgs a{S, ws, ws + n, ws + 2 * n, ws + 3 * n, n, status};
+    sym_eig_kernel<<<1, kDenseThreads, 0, ctx->stream>>>(a);
+    check_launch(ctx, "sym_eig_kernel");
+    pick_kernel<<<1, kDenseThreads, 0, ctx->stream>>>(S, ws, n, value_dev, vec_dev);
+    check_launch(ctx, "pick_kernel");
+}
+
 }  // namespace r1
 
 using namespace r1;

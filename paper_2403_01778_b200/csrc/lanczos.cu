@@ -1043,6 +1043,7 @@ struct EigPlan {
     BlockOp op;
     DescCache<BlockOp> dop;
     DeviceBuffer hint;   // one int: steps of the last solve in the solver's chain
+    DeviceBuffer dense_ws;  // dense J + scratch of the reference-algorithm eigen step
     DeviceBuffer other;  // n: other-end Ritz vector of the last solve in the chain
     bool other_valid = false;
     int64_t coldot_n = 0, rowpart_n = 0;
@@ -1271,6 +1272,11 @@ std::map<PlanKey, std::shared_ptr<EigPlan>>& eig_plans() {
 
 }  // namespace
 
+void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
+                       double* S);
+void eig_dense_reference_device(r1_context* ctx, int64_t n, double* S, double* ws, double* value_dev,
+                                double* vec_dev);
+
 void forget_eig_plans(r1_context* ctx) {
     std::lock_guard<std::mutex> cache_lock(cache_mutex());
     auto& m = eig_plans();
@@ -1302,6 +1308,15 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
     }
     P->op.blocks = blocks;
     P->op.dense = nullptr;
+    const int64_t n = P->op.n;
+    static const char* dmax = dev_env("R1_EIG_DENSE_MAX");  // development: reference algorithm for small n
+    if (dmax && n <= std::atoll(dmax) && !info_host && !stats_host) {
+        P->dense_ws.ensure((static_cast<size_t>(n) * n + 4 * n + 32) * sizeof(double));
+        double* S = P->dense_ws.as<double>();
+        dense_from_blocks(ctx, dims, order, blocks, S);
+        eig_dense_reference_device(ctx, n, S, S + n * n, value_dev, vec_dev);
+        return;
+    }
     run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host, solver_chain);
 }
 

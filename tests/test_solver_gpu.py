@@ -118,14 +118,14 @@ SOLVE_CASES = [
     ("ihoscf", (20, 20, 20), "c1", 1e-10, 1),
 ]
 
-# iHOSCF on a tensor whose iteration stagnates near the tolerance: the RQI
-# accept/reject decision (|rho_y| > |lambda_mid|) is a near-tie there and flips
-# with last-bit rounding (the C/numpy oracle flips the same decisions against
-# the compiled reference), so the iteration count is only pinned to +-6 (any
-# change of summation grouping in the sweep moves it by a few iterations).
+# iHOSCF on tensors whose iteration stagnates near the tolerance: the RQI
+# accept test |rho_y| > |rho_mid| compares two Rayleigh quotients equal to the
+# last ulp there, so the iteration count is sensitive to rounding — in the
+# reference itself (test_reference_sensitivity below: 1-ulp input
+# perturbations move it over 118-122 and 41-45).  The device path still meets
+# the north star's +-1 on the unperturbed inputs; test_chaotic_distribution
+# checks it against the reference's own spread.
 CHAOTIC = {("ihoscf", (20, 20, 20), "c1"), ("ihoscf", (7, 5, 9), "gauss")}
-# (7,5,9): the traces agree to ~1e-15 through iteration 29; at iteration 30 the
-# accept test compares two Rayleigh quotients equal to the last ulp (tools/chaos_probe.py)
 
 
 def _input(oracle, ref, dims, kind):
@@ -147,8 +147,7 @@ def test_solver_matches_reference(gpu_ctx, oracle, ref, alg, dims, kind, tol, se
     want = ref.solve(alg, a, dims, tol=tol, max_iters=500, seed=seed)
     got = r1.solve(alg, r1.DenseTensor(dims, a), r1.SolveOptions(tol=tol, max_iters=500, seed=seed))
     assert got.converged == want["converged"]
-    slack = 6 if (alg, dims, kind) in CHAOTIC else 1
-    assert abs(got.iterations - want["iterations"]) <= slack, (got.iterations, want["iterations"])
+    assert abs(got.iterations - want["iterations"]) <= 1, (got.iterations, want["iterations"])
     assert abs(got.result.lambda_ - want["lam"]) <= 1e-10 * abs(want["lam"]), (got.result.lambda_, want["lam"])
     if got.iterations == want["iterations"]:
         for u, v in zip(got.result.factors, want["factors"]):
@@ -169,3 +168,28 @@ def test_solver_validation(gpu_ctx):
         r1.solve("nope", a, r1.SolveOptions())
     with pytest.raises(ValueError, match="tol must be > 0"):
         r1.solve("hopm", a, r1.SolveOptions(tol=0.0))
+
+
+def _perturbed(a, t, rng):
+    return a.copy() if t == 0 else a * (1 + rng.choice([-1, 0, 1], size=a.size) * 2.0 ** -52)
+
+
+@pytest.mark.parametrize("case", sorted(CHAOTIC))
+def test_chaotic_distribution(gpu_ctx, oracle, ref, case):
+    """Over the input and 11 one-ulp perturbations of it, the device iteration
+    counts of a stagnating iHOSCF case stay inside the reference's own range
+    widened by its spread, and the medians agree within that spread."""
+    import paper_2403_01778_b200 as r1
+    alg, dims, kind = case
+    a = _input(oracle, ref, dims, kind)
+    rng = np.random.default_rng(0)
+    ref_its, gpu_its = [], []
+    for t in range(12):
+        b = _perturbed(a, t, rng)
+        ref_its.append(ref.solve(alg, b, dims, tol=1e-10, max_iters=500, seed=1)["iterations"])
+        gpu_its.append(r1.solve(alg, r1.DenseTensor(dims, b),
+                                r1.SolveOptions(tol=1e-10, max_iters=500, seed=1)).iterations)
+    spread = max(ref_its) - min(ref_its)
+    assert spread >= 2  # the case is genuinely rounding-sensitive in the reference
+    assert min(ref_its) - spread <= min(gpu_its) and max(gpu_its) <= max(ref_its) + spread, (ref_its, gpu_its)
+    assert abs(np.median(gpu_its) - np.median(ref_its)) <= spread, (ref_its, gpu_its)
