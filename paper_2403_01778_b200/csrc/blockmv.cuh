@@ -178,89 +178,6 @@ __device__ inline void blockop_phase_a(const BlockOp& op, const double* __restri
     }
 }
 
-// Phase A for the persistent Lanczos kernel (round 2): each block byte is read
-// ONCE per matvec.  Tasks (pair, 32-column chunk, row chunk) of a CHUNKED
-// layout whose row chunks are sized so all tasks move about the same bytes;
-// thread = row: it loads its 32 entries (two batches of 16 in flight) and
-// forms both the row partial (B x_n)[i] and its contributions to the 32
-// column dots (B' x_m)[j]; the column dots are reduced by a 31-shuffle
-// transposing butterfly (lane l ends with column l) and then over the warps
-// in warp order (fixed order: deterministic).  The blocks are loaded with an
-// L2 evict_last policy: a Lanczos run reads the same blocks every step.
-__device__ inline void blockop_phase_a_fused(const BlockOp& op, const double* __restrict__ x,
-                                             double xscale) {
-    constexpr int kH = 16;  // columns per half pass (registers: 16 loads + 16 column sums)
-    __shared__ double cred[32][kMvCols + 1];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    for (int t = blockIdx.x; t < op.ntasks; t += gridDim.x) {
-        int p = 0;
-        while (t >= op.task_first[p + 1]) ++p;
-        const int local = t - op.task_first[p];
-        const int c = local / op.nrc[p];
-        const int rc = local - c * op.nrc[p];
-        const int m = op.pm[p], n = op.pn[p];
-        const int64_t rows = op.dims[m], cols = op.dims[n];
-        const int64_t i0 = static_cast<int64_t>(rc) * op.rows_per_task;
-        const int64_t i1 = rows - i0 < op.rows_per_task ? rows : i0 + op.rows_per_task;
-        const double* B = op.blocks + op.boff[p];
-        const int64_t j0 = static_cast<int64_t>(c) * kMvCols;
-        const int nc = static_cast<int>(cols - j0 < kMvCols ? cols - j0 : kMvCols);
-        const double* xm = x + op.offs[m];
-        const double* xn = x + op.offs[n] + j0;
-        double* rp = op.rowpart + op.rp_off[p] + static_cast<int64_t>(c) * rows;
-#pragma unroll 1
-        for (int h = 0; h < kMvCols; h += kH) {
-            double ca[kH];
-#pragma unroll
-            for (int j = 0; j < kH; ++j) ca[j] = 0.0;
-            for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-                const double* bi = B + i + (j0 + h) * rows;
-                const double xi = xm[i];
-                double bv[kH];
-#pragma unroll
-                for (int j = 0; j < kH; ++j) {
-                    bv[j] = 0.0;
-                    if (h + j < nc)
-                        asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;"
-                                     : "=d"(bv[j])
-                                     : "l"(bi + j * rows), "l"(pol));
-                }
-                double s = h == 0 ? 0.0 : rp[i];  // the row partial continues across the halves
-#pragma unroll
-                for (int j = 0; j < kH; ++j) {
-                    s = fma(bv[j], h + j < nc ? xn[h + j] * xscale : 0.0, s);
-                    ca[j] = fma(bv[j], xi, ca[j]);
-                }
-                rp[i] = s;
-            }
-            // transposing butterfly over the 16 column sums: lanes with bit s set
-            // keep the upper half of their range; lane l ends with column l & 15
-#pragma unroll
-            for (int sft = kH / 2; sft >= 1; sft >>= 1) {
-                const bool up = (lane & sft) != 0;
-#pragma unroll
-                for (int k = 0; k < sft; ++k) {
-                    const double send = up ? ca[k] : ca[k + sft];
-                    const double keep = up ? ca[k + sft] : ca[k];
-                    ca[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
-                }
-            }
-            // lanes l and l ^ 16 hold the same column: fold them (fixed order)
-            const double v = ca[0] + __shfl_xor_sync(0xffffffffu, ca[0], 16);
-            if (lane < kH) cred[warp][h + lane] = v;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double sum = 0.0;
-            for (int w = 0; w < nw; ++w) sum += cred[w][lane];
-            if (lane < nc) op.coldot[op.cd_off[p] + rc * cols + j0 + lane] = sum * xscale;
-        }
-        __syncthreads();
-    }
-}
-
 // Phase B: y[t] for t in [start, end) step stride (end < 0: n).
 template <bool CHUNKED = true>
 __device__ inline void blockop_phase_b(const BlockOp& op, double* __restrict__ y, int64_t start,

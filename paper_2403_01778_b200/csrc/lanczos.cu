@@ -524,14 +524,10 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     for (;;) {
         // [A] matvec partials of v_j
         mark(7);
-        if (op.dense) {
-            if (j == 0)
-                blockop_phase_a<false>(op, a.V);
-            else
-                blockop_phase_a<false>(op, a.w, inv_beta);
-        } else {
-            blockop_phase_a_fused(op, j == 0 ? a.V : a.w, j == 0 ? 1.0 : inv_beta);
-        }
+        if (j == 0)
+            blockop_phase_a<false>(op, a.V);
+        else
+            blockop_phase_a<false>(op, a.w, inv_beta);
         mark(0);
         gsync();
         mark(1);
@@ -541,7 +537,7 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
             for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) vj[t] = a.w[t] * inv_beta;
             __syncthreads();
         }
-        blockop_phase_b<true>(op, a.w, r0 + threadIdx.x, blockDim.x, r1);
+        blockop_phase_b<false>(op, a.w, r0 + threadIdx.x, blockDim.x, r1);
         __syncthreads();
         mark(2);
         cgs2(j);
@@ -1305,9 +1301,8 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
         auto& slot = eig_plans()[{ctx, std::vector<uint64_t>(dims, dims + order)}];
         if (!slot) {
             slot = std::make_shared<EigPlan>();
-            // row chunks of <= 512 rows (one row per thread in the fused phase A):
-            // tasks of ~128 KB, balanced over the grid
-            blockop_layout(slot->op, dims, order, &slot->coldot_n, &slot->rowpart_n, 512);
+            blockop_layout(slot->op, dims, order, &slot->coldot_n, &slot->rowpart_n,
+                           int64_t(1) << 40);
         }
         P = slot;
     }
