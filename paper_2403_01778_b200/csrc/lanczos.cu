@@ -78,6 +78,7 @@ struct EigArgs {
     double* other_out; // this solve's other-end Ritz vector (unit), or null
     int debug_text;    // development: print the phase split of t_extremes
     double warm_noise; // weight of the random component of a warm start vector
+    double decide_tol; // relative Ritz residual at which the non-picked end counts as decided
 };
 
 __device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
@@ -346,11 +347,15 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
         const double scale = fmax(fabs(theta[0]), fabs(theta[1]));
         const int pick = fabs(theta[0]) > fabs(theta[1]) * (1.0 + 1e-12) ? 0 : 1;
         // The picked end must be converged to tol.  The other end matters only
-        // through the pick rule: it is enough that it is an accurate Ritz value
-        // (<= 1e-6 relative) whose magnitude is clearly on the losing side.
+        // through the pick rule: it is enough that it is a Ritz value with a
+        // small residual (decide_tol = 1e-4 relative; the warm start carries the
+        // previous iteration's vector of that end, so it is not a stray Ritz
+        // value) whose magnitude is on the losing side by a 100-residual margin
+        // (close calls keep iterating).  1e-6 took C1's eigen step 40 Lanczos
+        // steps instead of ~24 for a decision the margin already settles.
         const double rp = pick ? res_hi : res_lo, ro = pick ? res_lo : res_hi;
         const double tp = fabs(theta[pick]), to = fabs(theta[1 - pick]);
-        const bool decided = ro <= 1e-6 * scale && to + 100.0 * ro < tp * (1.0 - 1e-6);
+        const bool decided = ro <= a.decide_tol * scale && to + 100.0 * ro < tp * (1.0 - 1e-6);
         const bool conv = exact || (rp <= a.tol * scale && (ro <= a.tol * scale || decided));
         a.stats[0] = theta[0];
         a.stats[1] = theta[1];
@@ -1143,6 +1148,8 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     // 1e-6 (was 1e-3): the previous Ritz vectors are good to ~1e-5 or better,
     // a 1e-3 random component only had to be filtered out again (C1 eigen -6%)
     a.warm_noise = wn ? std::atof(wn) : 1e-6;
+    static const char* dt = dev_env("R1_EIG_DECIDE_TOL");  // development
+    a.decide_tol = dt ? std::atof(dt) : 1e-4;
     if (solver_chain) {
         if (!P.hint.ptr) {
             P.hint.ensure(sizeof(int));
