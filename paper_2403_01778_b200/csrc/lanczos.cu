@@ -348,11 +348,14 @@ __device__ void t_extremes(const EigArgs& a, int m, double beta_last, bool exact
         const int pick = fabs(theta[0]) > fabs(theta[1]) * (1.0 + 1e-12) ? 0 : 1;
         // The picked end must be converged to tol.  The other end matters only
         // through the pick rule: it is enough that it is a Ritz value with a
-        // small residual (decide_tol = 1e-4 relative; the warm start carries the
-        // previous iteration's vector of that end, so it is not a stray Ritz
-        // value) whose magnitude is on the losing side by a 100-residual margin
-        // (close calls keep iterating).  1e-6 took C1's eigen step 40 Lanczos
-        // steps instead of ~24 for a decision the margin already settles.
+        // small residual (decide_tol relative: 1e-6 by default, 1e-4 in the
+        // HOSCF chain, where the warm start carries the previous iteration's
+        // vector of that end, so it is not a stray Ritz value) whose magnitude
+        // is on the losing side by a 100-residual margin (close calls keep
+        // iterating).  At 1e-6 C1's eigen step took 40 Lanczos steps for a
+        // decision the margin settles at ~24.  iHOSCF keeps 1e-6: its RQI
+        // accept test compares Rayleigh quotients equal to the last ulp, and
+        // the tighter eigen step keeps its trajectory closest to the reference.
         const double rp = pick ? res_hi : res_lo, ro = pick ? res_lo : res_hi;
         const double tp = fabs(theta[pick]), to = fabs(theta[1 - pick]);
         const bool decided = ro <= a.decide_tol * scale && to + 100.0 * ro < tp * (1.0 - 1e-6);
@@ -1097,7 +1100,8 @@ void finish_lanczos(r1_context* ctx, const EigArgs& a, int* info_host, double* s
 }
 
 void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_dev,
-                 double* vec_dev, int* info_host, double* stats_host, bool solver_chain = false) {
+                 double* vec_dev, int* info_host, double* stats_host, bool solver_chain = false,
+                 double decide_tol = 1e-6) {
     const int64_t n = P.op.n;
     const int maxm = static_cast<int>(std::min<int64_t>(n, 320));
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
@@ -1149,7 +1153,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     // a 1e-3 random component only had to be filtered out again (C1 eigen -6%)
     a.warm_noise = wn ? std::atof(wn) : 1e-6;
     static const char* dt = dev_env("R1_EIG_DECIDE_TOL");  // development
-    a.decide_tol = dt ? std::atof(dt) : 1e-4;
+    a.decide_tol = dt ? std::atof(dt) : decide_tol;
     if (solver_chain) {
         if (!P.hint.ptr) {
             P.hint.ensure(sizeof(int));
@@ -1300,7 +1304,7 @@ void forget_eig_plans(r1_context* ctx) {
 // res_lo, res_hi, value].
 void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                 const double* x0, double* value_dev, double* vec_dev, int* info_host,
-                double* stats_host, bool solver_chain) {
+                double* stats_host, bool solver_chain, double decide_tol) {
     if (order < 2 || order > 16) fail(R1_ERR_INVALID_ARGUMENT, "eig: unsupported order");
     std::shared_ptr<EigPlan> P;
     {
@@ -1324,7 +1328,7 @@ void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* 
         eig_dense_reference_device(ctx, n, S, S + n * n, value_dev, vec_dev);
         return;
     }
-    run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host, solver_chain);
+    run_lanczos(ctx, *P, x0, value_dev, vec_dev, info_host, stats_host, solver_chain, decide_tol);
 }
 
 // Same on a dense symmetric n x n matrix S (device, column-major).

@@ -257,6 +257,10 @@ struct RunResult {
 // graphs are replayed one per status read; without graphs the same kernels are
 // launched directly.
 
+// Lanczos: the non-picked spectral end counts as decided at this relative
+// Ritz residual in the HOSCF chain (lanczos.cu t_extremes; iHOSCF keeps 1e-6)
+constexpr double kHoscfDecideTol = 1e-4;
+
 struct DevRecord {
     double lambda, stop_value, eq11, kkt, angle, pad;
     unsigned long long t[5];  // globaltimer: start, after eig, after split, after sweep, end
@@ -403,7 +407,7 @@ void enqueue_hoscf_iteration(Work& w, HoscfDev& D, int p, bool warm) {
     check_launch(ctx, "stamp_kernel");
     note("eig");
     eig_blocks(ctx, w.dims.data(), w.d, Jb[p], warm ? w.Xprev : nullptr, w.mu, w.X, nullptr, nullptr,
-               true);
+               true, kHoscfDecideTol);
     stamp_kernel<<<1, 1, 0, st>>>(D.state, D.trace, D.cap, 1);
     check_launch(ctx, "stamp_kernel");
     note("split");

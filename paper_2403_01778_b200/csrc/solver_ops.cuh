@@ -26,9 +26,11 @@ void dense_from_blocks(r1_context* ctx, const uint64_t* dims, int order, const d
 bool rqi_step(r1_context* ctx, int64_t n, const double* S, const double* x, double* y);
 // solver_chain: x0 is the previous eigenvector of the same operator inside one
 // solve (nullptr on its first iteration): the step-count hint is used / reset.
+// decide_tol: relative Ritz residual at which the non-picked spectral end
+// counts as decided (lanczos.cu t_extremes)
 void eig_blocks(r1_context* ctx, const uint64_t* dims, int order, const double* blocks,
                 const double* x0, double* value_dev, double* vec_dev, int* info_host,
-                double* stats_host, bool solver_chain = false);
+                double* stats_host, bool solver_chain = false, double decide_tol = 1e-6);
 void eig_dense(r1_context* ctx, int64_t n, const double* S, const double* x0, double* value_dev,
                double* vec_dev, int* info_host, double* stats_host);
 void dot_device(r1_context* ctx, const double* x, const double* y, uint64_t n, double* out_dev);
