@@ -1643,7 +1643,9 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
             const int64_t total = f.n_b01 + f.n_c0 + f.n_c1;
             const int grid = static_cast<int>(
                 std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, int64_t(32) * ctx->num_sms)));
-            if (total < (int64_t(1) << 31))
+            // 32-bit indices only while the grid-stride loop cannot step past
+            // 2^31 (e + gridDim.x * 256 must stay representable)
+            if (total + static_cast<int64_t>(grid) * 256 < (int64_t(1) << 31))
                 finish_kernel<int><<<grid, 256, 0, ctx->stream>>>(f);
             else
                 finish_kernel<int64_t><<<grid, 256, 0, ctx->stream>>>(f);
@@ -1668,6 +1670,7 @@ void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* 
     info[9] = L.nra;
     info[10] = L.K;
     info[11] = L.KO;
+    info[12] = L.ndyn;
 }
 
 }  // namespace r1

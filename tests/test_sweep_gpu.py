@@ -96,6 +96,26 @@ def test_build_j_deterministic_box_kernel(gpu_ctx, oracle, dims):
         assert np.array_equal(r1.build_j(t, r1.FactorSet(0.0, f)).blocks, b0)
 
 
+def test_dynamic_tail_and_merged_classes_deterministic(gpu_ctx, oracle):
+    """A shape that really takes the scheduled dynamic tail (>= 64 panels per
+    CTA) and the merged alignment classes (I0 = 136: K = 2, I1 / K = 240), as
+    the plan reports it: repeated sweeps bit-identical, and equal to the oracle
+    within the contraction bound."""
+    import paper_2403_01778_b200 as r1
+    dims = (136, 480, 800)
+    info = gpu_ctx.sweep_plan_info(dims)
+    assert info["K"] > 1 and info["ndyn"] > 0, info
+    a = oracle.oracle_random_tensor(dims, 17)
+    f = oracle.oracle_random_unit_factors(dims, 18)
+    t = r1.DenseTensor(dims, a)
+    b0 = r1.build_j(t, r1.FactorSet(0.0, f)).blocks
+    for _ in range(3):
+        assert np.array_equal(r1.build_j(t, r1.FactorSet(0.0, f)).blocks, b0)
+    want = oracle.build_j(a, dims, f)
+    scale = oracle.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
+    assert np.all(np.abs(b0 - want) <= 1e-13 * scale + 1e-300)
+
+
 def test_build_j_errors(gpu_ctx, oracle):
     """nepv.cpp:24-41 / test_nepv.cpp:104-107, 227-232."""
     import paper_2403_01778_b200 as r1
