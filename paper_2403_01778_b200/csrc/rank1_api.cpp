@@ -14,12 +14,14 @@
 #include <functional>
 #include <numbers>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "rank1/generators.hpp"
 #include "rank1/greedy.hpp"
@@ -759,6 +761,44 @@ SolveReport from_c(const std::string& algorithm, const DenseTensor& a, const Rep
 
 }  // namespace
 
+namespace {
+
+// Several GPUs of the node for the SCF solvers (opt-in: R1_NUM_GPUS = N):
+// one context per device, one NCCL communicator set (r1_comm_init_all), the
+// tensor split into slabs along its last mode and one host thread per GPU
+// running the sharded solver (SURVEY §8b threading: "one thread per GPU").
+struct MultiGpu {
+    std::vector<r1_context*> ctxs;
+    std::vector<r1_comm*> comms;
+};
+
+MultiGpu* multi_gpu() {
+    static std::once_flag once;
+    static MultiGpu* m = nullptr;
+    std::call_once(once, [] {
+        const char* env = std::getenv("R1_NUM_GPUS");
+        if (!env) return;  // default: the process context on device 0
+        const int want = std::atoi(env);
+        int have = 0;
+        if (want < 1 || r1_device_count(&have) != R1_OK || have < 1) return;
+        const int ndev = std::min(want, have);  // 1 is allowed: the sharded path on one GPU
+        auto* mg = new MultiGpu();
+        std::vector<int> devs(ndev);
+        for (int i = 0; i < ndev; ++i) {
+            devs[i] = i;
+            r1_context* c = nullptr;
+            raise(r1_context_create(i, &c));
+            mg->ctxs.push_back(c);
+        }
+        mg->comms.resize(ndev);
+        raise(r1_comm_init_all(ndev, devs.data(), mg->ctxs.data(), mg->comms.data()));
+        m = mg;
+    });
+    return m;
+}
+
+}  // namespace
+
 SolveReport solve(const std::string& algorithm, const DenseTensor& a, const SolveOptions& opts) {
     if (algorithm != "hoscf" && algorithm != "ihoscf" && algorithm != "hopm" &&
         algorithm != "jacobi_hopm" && algorithm != "asvd" && algorithm != "jacobi_asvd")
@@ -768,6 +808,42 @@ SolveReport solve(const std::string& algorithm, const DenseTensor& a, const Solv
     r1_solve_options o = c_options(a, opts, init);
     const auto dims = u64(a.dims());
     const std::size_t n = std::accumulate(a.dims().begin(), a.dims().end(), std::size_t{0});
+    const int d = static_cast<int>(a.order());
+    MultiGpu* mg = (algorithm == "hoscf" || algorithm == "ihoscf") ? multi_gpu() : nullptr;
+    if (mg && dims[d - 1] >= mg->ctxs.size()) {
+        // slabs of the last (slowest) mode are contiguous runs of the host array
+        const int W = static_cast<int>(mg->ctxs.size());
+        uint64_t prefix = 1;
+        for (int k = 0; k + 1 < d; ++k) prefix *= dims[k];
+        std::vector<std::unique_ptr<ReportBuffers>> bufs;
+        for (int r = 0; r < W; ++r) bufs.push_back(std::make_unique<ReportBuffers>(n, opts.max_iters));
+        std::vector<int> rcs(W, R1_OK);
+        std::vector<std::string> msgs(W);
+        auto rank_fn = [&](int r) {
+            uint64_t lo = 0, hi = 0;
+            r1_slab_bounds(dims[d - 1], W, r, &lo, &hi);
+            std::vector<uint64_t> ld(dims);
+            ld[d - 1] = hi - lo;
+            r1_tensor* slab = nullptr;
+            int rc = r1_tensor_from_host(mg->ctxs[r], a.data() + prefix * lo, ld.data(), d, &slab);
+            if (rc == R1_OK)
+                rc = r1_solve_sharded(mg->ctxs[r], algorithm.c_str(), slab, dims.data(), d, &o,
+                                      &bufs[r]->r);
+            if (rc != R1_OK) msgs[r] = r1_last_error();  // thread-local message
+            if (slab) r1_tensor_destroy(slab);
+            rcs[r] = rc;
+        };
+        std::vector<std::thread> th;
+        for (int r = 1; r < W; ++r) th.emplace_back(rank_fn, r);
+        rank_fn(0);
+        for (auto& t : th) t.join();
+        for (int r = 0; r < W; ++r)
+            if (rcs[r] != R1_OK) {
+                if (rcs[r] == R1_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msgs[r]);
+                throw std::runtime_error(msgs[r]);
+            }
+        return from_c(algorithm, a, *bufs[0]);
+    }
     ReportBuffers b(n, opts.max_iters);
     raise(r1_solve_host(ctx(), algorithm.c_str(), a.data(), dims.data(), static_cast<int>(a.order()),
                         &o, &b.r));

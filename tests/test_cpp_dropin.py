@@ -36,3 +36,34 @@ def test_cpp_dropin_runs_on_b200(gpu_ctx):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
+
+
+MULTI = os.path.join(ROOT, "tests", "cpp", "test_multi_gpu.cpp")
+
+
+def _compile_multi():
+    out = os.path.join(ROOT, "tests", "cpp", "test_multi_gpu")
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), MULTI, "-o", out,
+           os.path.join(PKG, "librank1_b200.so"), f"-Wl,-rpath,{PKG}"]
+    subprocess.run(cmd, check=True)
+    return out
+
+
+def test_cpp_multi_gpu_program_compiles():
+    assert os.path.exists(_compile_multi())
+
+
+@pytest.mark.gpu
+def test_cpp_multi_gpu_path_matches_single(gpu_ctx):
+    """R1_NUM_GPUS=1 takes the sharded C++ path (slab upload, r1_comm_init_all,
+    r1_solve_sharded on a thread per GPU) on this one-GPU box: bit-identical to
+    the default single-context path."""
+    exe = _compile_multi()
+    env0 = {k: v for k, v in os.environ.items() if k != "R1_NUM_GPUS"}
+    one = subprocess.run([exe], capture_output=True, text=True, timeout=300, env=env0)
+    multi = subprocess.run([exe], capture_output=True, text=True, timeout=300,
+                           env=dict(env0, R1_NUM_GPUS="1"))
+    assert one.returncode == 0, one.stderr
+    assert multi.returncode == 0, multi.stderr
+    assert one.stdout == multi.stdout
+    assert one.stdout.count("hoscf") == 2
