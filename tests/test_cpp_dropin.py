@@ -65,5 +65,7 @@ def test_cpp_multi_gpu_path_matches_single(gpu_ctx):
                            env=dict(env0, R1_NUM_GPUS="1"))
     assert one.returncode == 0, one.stderr
     assert multi.returncode == 0, multi.stderr
-    assert one.stdout == multi.stdout
+    # ncclCommInitAll prints its version banner on stdout
+    body = lambda out: [ln for ln in out.splitlines() if not ln.startswith("NCCL")]  # noqa: E731
+    assert body(one.stdout) == body(multi.stdout)
     assert one.stdout.count("hoscf") == 2
