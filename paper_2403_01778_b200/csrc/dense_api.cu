@@ -871,6 +871,17 @@ int r1_ttvc(r1_context* ctx, const double* a_host, const uint64_t* dims, int ord
         R1_CUDA(cudaSetDevice(ctx->device));
         if (order < 1 || order > 16 || nmodes < 1 || nmodes > order)
             fail(R1_ERR_INVALID_ARGUMENT, "ttvc: mode out of range");
+        if (full ? nmodes != order : nmodes >= order)
+            fail(R1_ERR_INVALID_ARGUMENT, full ? "ttvc_scalar: all modes must be contracted"
+                                               : "ttvc: contracting all modes yields a scalar, use ttvc_scalar");
+        {
+            std::vector<bool> seen(order, false);
+            for (int i = 0; i < nmodes; ++i) {
+                if (modes[i] < 0 || modes[i] >= order) fail(R1_ERR_INVALID_ARGUMENT, "ttvc: mode out of range");
+                if (seen[modes[i]]) fail(R1_ERR_INVALID_ARGUMENT, "ttvc: duplicate mode");
+                seen[modes[i]] = true;
+            }
+        }
         // vector offsets in the caller's order, then the descending contraction order
         std::vector<int64_t> voff(nmodes + 1, 0);
         for (int i = 0; i < nmodes; ++i) voff[i + 1] = voff[i] + static_cast<int64_t>(dims[modes[i]]);
