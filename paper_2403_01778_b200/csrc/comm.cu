@@ -169,7 +169,9 @@ void exchange_blocks(r1_context* ctx, const double* lblocks, double* gblocks,
 }
 
 void comm_destroy(r1_comm* c) {
-    if (c && c->comm && c->owns) nccl().CommDestroy(static_cast<ncclComm_t>(c->comm));
+    if (!c) return;
+    if (c->ctx && c->ctx->comm == c) c->ctx->comm = nullptr;
+    if (c->comm && c->owns) nccl().CommDestroy(static_cast<ncclComm_t>(c->comm));
     delete c;
 }
 
@@ -206,6 +208,7 @@ int r1_comm_init(r1_context* ctx, int nranks, int rank, const void* id, r1_comm*
             delete c;
             nccl_check(r, "ncclCommInitRank");
         }
+        c->ctx = ctx;
         ctx->comm = c;
         *out = c;
     });
@@ -224,6 +227,7 @@ int r1_comm_init_all(int ndev, const int* devices, r1_context** ctxs, r1_comm** 
             c->rank = i;
             c->owns = true;
             c->comm = reinterpret_cast<void*>(cs[i]);
+            c->ctx = ctxs[i];
             ctxs[i]->comm = c;
             comms[i] = c;
         }

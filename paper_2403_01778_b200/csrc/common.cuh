@@ -203,6 +203,7 @@ struct r1_comm {
     int world = 1;
     int rank = 0;
     bool owns = true;
+    r1_context* ctx = nullptr;  // the context it is attached to (detached on destroy)
 };
 
 struct r1_tensor {
