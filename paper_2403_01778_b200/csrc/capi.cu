@@ -166,6 +166,7 @@ int r1_context_destroy(r1_context* ctx) {
         forget_solver_handles(ctx);
         forget_solver_work(ctx);
         ctx->plans.clear();
+        if (ctx->comm) ctx->comm->ctx = nullptr;  // the communicator outlives its context
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
         delete ctx;
     });
