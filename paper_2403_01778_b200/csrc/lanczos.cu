@@ -34,8 +34,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <string>
 #include <vector>
 
 namespace cg = cooperative_groups;
@@ -79,6 +82,7 @@ struct EigArgs {
     int debug_text;    // development: print the phase split of t_extremes
     double warm_noise; // weight of the random component of a warm start vector
     double decide_tol; // relative Ritz residual at which the non-picked end counts as decided
+    const struct LzTiles* tl;  // tiled matvec plan (TILED grid kernel), device
 };
 
 __device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
@@ -389,6 +393,245 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// ---------------------------------------------------------------------------
+// Tiled block matvec of the grid kernel (block operators, n > kSmallN).
+//
+// Every block B(p) (I_m x I_n, column-major) is cut into row chunks of
+// Rc <= 32 * kLzNQ rows; the (pair, row chunk, column) units are split into
+// gridDim contiguous ranges of equal cost, one per CTA ("segments": the part
+// of a range inside one row chunk).  A warp takes a column of its segment,
+// lane l the rows l + 32 q: ONE read of each block entry (L2 evict_last, so
+// the 88 MB of C5's blocks stay on chip across the Lanczos steps) feeds both
+// the column dot (B' x_m)[c] over the chunk (warp-reduced, complete) and the
+// lane's row accumulators (B x_n)[i] (summed over the warps in shared memory
+// into one row partial per segment).  The CGS pass-1 dots V' (J x) are folded
+// into the same phase from the partials (every contribution to J x lives in
+// exactly one CTA), so a Lanczos step needs three grid barriers, not four.
+// The plan is fixed per operator shape: every sum has a fixed order.
+constexpr int kLzNQ = 4;     // rows per lane (row chunk <= 128)
+constexpr int kLzWarps = kEigThreads / 32;
+
+struct LzSeg {
+    int p, rc, c0, c1;  // pair, row chunk, columns [c0, c1)
+    long long rp;       // row-partial slot (rows of the chunk)
+};
+
+struct LzTiles {
+    int nrc[kMvMaxPairs] = {};
+    int Rc[kMvMaxPairs] = {};
+    int rcseg_off[kMvMaxPairs] = {};  // index of (p, 0) in rc_first
+    int64_t cd_off[kMvMaxPairs] = {}; // column dots of pair p: [rc][I_n]
+    unsigned char v2[kMvMaxPairs] = {};  // pair p's columns are 16-B aligned (double2 loads)
+    const LzSeg* segs = nullptr;
+    const int* cta_seg = nullptr;     // [G + 1]
+    // phase-B metadata, one int array: rc_first[nrcf + 1] (first segment of
+    // each (p, rc) + sentinel), then seg_rp[nseg] (row-partial slot of each
+    // segment); copied to shared memory when it fits kLzMetaInts
+    const int* meta = nullptr;
+    int nrcf = 0, nseg = 0;
+    double* coldot = nullptr;
+    double* rowpart = nullptr;
+};
+
+constexpr int kLzMetaInts = 6144;  // 24 KB of shared memory for the phase-B metadata
+constexpr size_t kLzDynSmem = sizeof(double) * 14 * kMaxKrylov + sizeof(int) * kLzMetaInts;
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ double2 ld_keep2(const double* p, uint64_t pol) {
+    double2 v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(p), "l"(pol));
+    return v;
+}
+
+// Phase A of the tiled matvec on x (= V[:, kmax]) plus the CGS pass-1 dot
+// partials pdot[blockIdx.x * ld + k] = sum over this CTA's contributions c to
+// J x (unscaled) of V[row(c), k] c, k <= kmax.  red: kLzWarps * 32 kLzNQ
+// doubles, rps: 32 kLzNQ, dacc: kmax + 1 (shared memory).
+__device__ __noinline__ void lz_phase_a(const BlockOp& op, const LzTiles& tl, const double* __restrict__ x,
+                           const double* __restrict__ V, int64_t n, int kmax, double* pdot, int ld,
+                           double* red, double* rps, double* dacc) {
+    constexpr int RMAX = 32 * kLzNQ;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t pol = policy_evict_last();
+    for (int k = threadIdx.x; k <= kmax; k += blockDim.x) dacc[k] = 0.0;
+    const int s_end = tl.cta_seg[blockIdx.x + 1];
+    for (int s = tl.cta_seg[blockIdx.x]; s < s_end; ++s) {
+        const LzSeg sg = tl.segs[s];
+        const int p = sg.p, m = op.pm[p], nn = op.pn[p];
+        const int64_t rows = op.dims[m], cols = op.dims[nn];
+        const int64_t i0 = static_cast<int64_t>(sg.rc) * tl.Rc[p];
+        const int nr = static_cast<int>(min(static_cast<int64_t>(tl.Rc[p]), rows - i0));
+        const double* B = op.blocks + op.boff[p] + i0;
+        const double* xm = x + op.offs[m] + i0;
+        const double* xn = x + op.offs[nn];
+        double* cd = tl.coldot + tl.cd_off[p] + static_cast<int64_t>(sg.rc) * cols;
+        // lane rows: r(q) = 64 (q / 2) + 2 lane + (q & 1) — two consecutive
+        // rows per lane and pair of q, so aligned columns load as double2
+        double xr[kLzNQ], racc[kLzNQ];
+#pragma unroll
+        for (int q = 0; q < kLzNQ; ++q) {
+            const int r = 64 * (q >> 1) + 2 * lane + (q & 1);
+            xr[q] = r < nr ? xm[r] : 0.0;
+            racc[q] = 0.0;
+        }
+        auto column_dot = [&](const double (&b)[kLzNQ], double xc) {
+            double dd = 0.0;
+#pragma unroll
+            for (int q = 0; q < kLzNQ; ++q) {
+                racc[q] = fma(b[q], xc, racc[q]);
+                dd = fma(b[q], xr[q], dd);
+            }
+            return dd;
+        };
+        auto load_col = [&](double (&b)[kLzNQ], const double* col, bool v2) {
+            if (v2) {
+#pragma unroll
+                for (int h = 0; h < kLzNQ / 2; ++h) {
+                    const int r = 64 * h + 2 * lane;
+                    double2 v = make_double2(0.0, 0.0);
+                    if (r + 1 < nr) {
+                        v = ld_keep2(col + r, pol);
+                    } else if (r < nr) {
+                        v.x = ld_keep(col + r, pol);
+                    }
+                    b[2 * h] = v.x;
+                    b[2 * h + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kLzNQ; ++q) {
+                    const int r = 64 * (q >> 1) + 2 * lane + (q & 1);
+                    b[q] = r < nr ? ld_keep(col + r, pol) : 0.0;
+                }
+            }
+        };
+        const bool v2 = tl.v2[p] != 0;
+        // four columns per iteration: 4 * kLzNQ doubles in flight per lane
+        constexpr int CU = 4;
+        int c = sg.c0 + warp;
+        for (; c + (CU - 1) * kLzWarps < sg.c1; c += CU * kLzWarps) {
+            double b[CU][kLzNQ];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) load_col(b[u], B + static_cast<int64_t>(c + u * kLzWarps) * rows, v2);
+            double dd[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) dd[u] = column_dot(b[u], xn[c + u * kLzWarps]);
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+                for (int u = 0; u < CU; ++u) dd[u] += __shfl_xor_sync(0xffffffffu, dd[u], off);
+            if (lane == 0)
+#pragma unroll
+                for (int u = 0; u < CU; ++u) cd[c + u * kLzWarps] = dd[u];
+        }
+        for (; c < sg.c1; c += kLzWarps) {
+            double b[kLzNQ];
+            load_col(b, B + static_cast<int64_t>(c) * rows, v2);
+            double dd = column_dot(b, xn[c]);
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, off);
+            if (lane == 0) cd[c] = dd;
+        }
+        // row partial of the segment: the warps' accumulators in warp order
+#pragma unroll
+        for (int q = 0; q < kLzNQ; ++q) red[warp * RMAX + 64 * (q >> 1) + 2 * lane + (q & 1)] = racc[q];
+        __syncthreads();
+        for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < kLzWarps; ++w) v += red[w * RMAX + r];
+            rps[r] = v;
+            tl.rowpart[sg.rp + r] = v;
+        }
+        __syncthreads();
+        // CGS pass-1 dot partials of this segment's contributions (warp per k)
+        const double* vm = V + op.offs[m] + i0;
+        const double* vn = V + op.offs[nn];
+        for (int k = warp; k <= kmax; k += kLzWarps) {
+            const int64_t ko = static_cast<int64_t>(k) * n;
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < kLzNQ; ++q) {  // rows: all loads issued together
+                const int r = lane + 32 * q;
+                t = fma(r < nr ? vm[ko + r] : 0.0, r < nr ? rps[r] : 0.0, t);
+            }
+            int cc = sg.c0 + lane;
+            for (; cc + 7 * 32 < sg.c1; cc += 8 * 32) {
+                double vv[8], cv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    vv[u] = vn[ko + cc + 32 * u];
+                    cv[u] = cd[cc + 32 * u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t = fma(vv[u], cv[u], t);
+            }
+            for (; cc < sg.c1; cc += 32) t = fma(vn[ko + cc], cd[cc], t);
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            if (lane == 0) dacc[k] += t;
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k <= kmax; k += blockDim.x) pdot[static_cast<int64_t>(blockIdx.x) * ld + k] = dacc[k];
+}
+
+// (J x)[t] / scale for one row t, summed by an 8-lane group (sub-lane sl):
+// the column dots of the pairs (k, m), k < m (one per row chunk) and the row
+// partials of the pairs (m, n), n > m (one per segment of the row's chunk),
+// strided over the group in a fixed enumeration, then a fixed shuffle tree.
+// All 32 lanes must call (shuffles); the result is in every lane of the group.
+__device__ double lz_row_sum8(const BlockOp& op, const LzTiles& tl, const int* meta, int64_t t, int sl) {
+    const int d = op.d;
+    int m = 0;
+    while (t >= op.offs[m + 1]) ++m;
+    const int64_t i = t - op.offs[m];
+    const int* rc_first = meta;
+    const int* seg_rp = meta + tl.nrcf + 1;
+    double s = 0.0;
+    int base = 0;  // enumeration index of the next contribution
+    for (int k = 0; k < m; ++k) {
+        const int p = pair_index(k, m, d);
+        const int cnt = tl.nrc[p];
+        for (int e = (sl - base) & 7; e < cnt; e += 8)
+            s += tl.coldot[tl.cd_off[p] + static_cast<int64_t>(e) * op.dims[m] + i];
+        base += cnt;
+    }
+    for (int nn = m + 1; nn < d; ++nn) {
+        const int p = pair_index(m, nn, d);
+        const int rc = static_cast<int>(i / tl.Rc[p]);
+        const int64_t r = i - static_cast<int64_t>(rc) * tl.Rc[p];
+        const int sf = rc_first[tl.rcseg_off[p] + rc], se = rc_first[tl.rcseg_off[p] + rc + 1];
+        const int cnt = se - sf;
+        for (int e = (sl - base) & 7; e < cnt; e += 8) s += tl.rowpart[seg_rp[sf + e] + r];
+        base += cnt;
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+}
+
+// TILED = false: the round-1 kernel (dense operators; development switch
+// R1_EIG_TILED=0 for block operators) — phase A partials, phase B, CGS2 with
+// its own passes, four grid barriers per step.
+// TILED = true (block operators): lz_phase_a (single read, CGS pass 1 folded),
+// then own rows y -> w1 = y - V h1 with the pass-2 dots and ||w1||^2, then
+// v_{j+1} = (w1 - V h2) / beta with beta^2 = ||w1||^2 - ||h2||^2: three
+// grid barriers per step.
+template <bool TILED>
 __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a) {
     cg::grid_group grid = cg::this_grid();
     // one-CTA launches (small operators) synchronise with the CTA barrier
@@ -409,10 +652,28 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
         tlast = t;
     };
     __shared__ BlockOp op;
+    __shared__ LzTiles tls;
     __shared__ double red[32];
     __shared__ double hsh[kMaxKrylov + 1];
-    if (threadIdx.x == 0) op = *a.op;
+    if (threadIdx.x == 0) {
+        op = *a.op;
+        if (TILED) tls = *a.tl;
+    }
     __syncthreads();
+    // phase-B metadata of the tiled matvec: shared memory when it fits
+    const int* lzmeta = nullptr;
+    if constexpr (TILED) {
+        extern __shared__ double dsm[];
+        const int cnt = tls.nrcf + 1 + tls.nseg;
+        if (cnt <= kLzMetaInts) {
+            int* sm = reinterpret_cast<int*>(dsm + 14 * kMaxKrylov);
+            for (int e = threadIdx.x; e < cnt; e += blockDim.x) sm[e] = tls.meta[e];
+            lzmeta = sm;
+            __syncthreads();
+        } else {
+            lzmeta = tls.meta;
+        }
+    }
     const int64_t n = a.n;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -530,6 +791,116 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     double anorm = 0.0;
     double inv_beta = 1.0;  // V[:,j] = w * inv_beta for j > 0 (materialised in phase B)
     for (;;) {
+        if constexpr (TILED) {
+            extern __shared__ double dsm[];
+            // [A] J v_j partials (single read of the blocks) + CGS pass-1 dot partials
+            mark(7);
+            lz_phase_a(op, tls, a.V + static_cast<int64_t>(j) * n, a.V, n, j, a.pdot1, ld, dsm,
+                       dsm + kLzWarps * 32 * kLzNQ, dsm + (kLzWarps + 1) * 32 * kLzNQ);
+            mark(0);
+            gsync();
+            mark(1);
+            // [B] own rows: y = J v_j, w1 = y - V h1; pass-2 dot and ||w1||^2 partials
+            reduce_dots(a.pdot1, j);  // hsh = h1 / scale
+            const double sc = op.scale;
+            // an 8-lane group per row
+            for (int64_t tb = r0 + 4 * warp; tb < r1; tb += 4 * nw) {
+                const int64_t t = tb + (lane >> 3);
+                const bool ok = t < r1;
+                const int sl = lane & 7;
+                const double y = lz_row_sum8(op, tls, lzmeta, ok ? t : r0, sl) * sc;
+                double s = 0.0;
+                if (ok)
+                    for (int k = sl; k <= j; k += 8) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k] * sc, s);
+#pragma unroll
+                for (int off = 4; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (ok && sl == 0) a.w[t] = y - s;
+            }
+            __syncthreads();
+            partial_dots(a.pdot2, j);
+            {
+                double ss = 0.0;
+                for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) ss = fma(a.w[t], a.w[t], ss);
+                ss = cta_sum(ss, red);
+                if (threadIdx.x == 0) a.part[blockIdx.x] = ss;
+            }
+            mark(2);
+            gsync();
+            mark(3);
+            const double h1j = hsh[j] * sc;
+            __syncthreads();
+            reduce_dots(a.pdot2, j);  // hsh = h2
+            double h2sq = 0.0;
+            for (int k = 0; k <= j; ++k) h2sq = fma(hsh[k], hsh[k], h2sq);
+            const double w1sq = grid_sum(a.part, 0);
+            const double alpha = h1j + hsh[j];
+            // ||w1 - V h2||^2 = ||w1||^2 - ||h2||^2 (V orthonormal, h2 = V' w1)
+            double nrm = sqrt(fmax(w1sq - h2sq, 0.0));
+            anorm = fmax(anorm, fabs(alpha) + nrm + (j > 0 ? a.beta[j - 1] : 0.0));
+            if (j == 0 && restarts == 0 && anorm == 0.0) {
+                zero_op = true;  // J == 0 (see below)
+                break;
+            }
+            const bool space_full = (j + 1 == n);
+            const bool breakdown = !space_full && nrm <= 1e-13 * anorm;
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.alpha[j] = alpha;
+                a.beta[j] = breakdown ? 0.0 : nrm;
+            }
+            double* vnext = a.V + static_cast<int64_t>(j + 1) * n;
+            if (breakdown) {
+                ++breakdowns;
+                for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x)
+                    a.w[t] = hash_unit(static_cast<uint64_t>(t), 0xb00ull + breakdowns);
+                __syncthreads();
+                cgs2(j);
+                nrm = sqrt(grid_sum(a.part, 0));
+                for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) vnext[t] = a.w[t] / nrm;
+            } else if (!space_full) {
+                const double ib = 1.0 / nrm;
+                for (int64_t tb = r0 + 4 * warp; tb < r1; tb += 4 * nw) {
+                    const int64_t t = tb + (lane >> 3);
+                    const bool ok = t < r1;
+                    const int sl = lane & 7;
+                    double s = 0.0;
+                    if (ok)
+                        for (int k = sl; k <= j; k += 8) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k], s);
+#pragma unroll
+                    for (int off = 4; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                    if (ok && sl == 0) vnext[t] = (a.w[t] - s) * ib;
+                }
+            }
+            ++j;
+            const bool size_limit = (j == a.maxm) || space_full;
+            const bool check = ((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit;
+            mark(4);
+            if (check && blockIdx.x == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts, dsm, kMaxKrylov);
+            mark(5);
+            gsync();
+            mark(6);
+            if (check) {
+                if (a.ctl[0]) break;
+                if (size_limit) {
+                    if (restarts >= a.max_restarts) break;
+                    ++restarts;
+                    first_check = a.min_steps;
+                    for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
+                        double s0 = 0.0, s1 = 0.0;
+                        for (int k = 0; k < j; ++k) {
+                            const double v = a.V[t + static_cast<int64_t>(k) * n];
+                            s0 = fma(v, a.sT[k], s0);
+                            s1 = fma(v, a.sT[kMaxKrylov + k], s1);
+                        }
+                        a.w[t] = s0 + s1;
+                    }
+                    gsync();
+                    set_v0_from_w();
+                    j = 0;
+                    anorm = 0.0;
+                }
+            }
+            continue;
+        }
         // [A] matvec partials of v_j
         mark(7);
         if (j == 0)
@@ -1055,7 +1426,94 @@ struct EigPlan {
     DeviceBuffer other;  // n: other-end Ritz vector of the last solve in the chain
     bool other_valid = false;
     int64_t coldot_n = 0, rowpart_n = 0;
+    // tiled matvec plan of the grid kernel (built for tl_G CTAs)
+    LzTiles tl;
+    DeviceBuffer tl_meta;
+    DescCache<LzTiles> dtl;
+    int tl_G = 0;
+    int64_t tl_coldot_n = 0, tl_rowpart_n = 0;
 };
+
+// Split the (pair, row chunk, column) units of the blocks into G contiguous
+// ranges of equal cost (rows of the chunk + a per-column overhead) and cut
+// them into segments (one row chunk each).
+void build_tiles(EigPlan& P, int G) {
+    const BlockOp& op = P.op;
+    LzTiles& tl = P.tl;
+    tl = LzTiles{};
+    std::vector<LzSeg> segs;
+    std::vector<int> cta_seg(G + 1, 0), rc_first;
+    double total = 0.0;
+    int64_t cdo = 0;
+    const int group = 1;
+    for (int p = 0; p < op.npairs; ++p) {
+        const int64_t rows = op.dims[op.pm[p]], cols = op.dims[op.pn[p]];
+        int nrc = static_cast<int>((rows + 32 * kLzNQ - 1) / (32 * kLzNQ));
+        int rc_rows = static_cast<int>((rows + nrc - 1) / nrc);
+        tl.nrc[p] = nrc;
+        tl.Rc[p] = rc_rows;
+        // double2 loads: even rows and an even block offset keep every column
+        // and every (even) row chunk 16-B aligned
+        tl.v2[p] = (rows % 2 == 0 && op.boff[p] % 2 == 0) ? 1 : 0;
+        if (tl.v2[p] && tl.Rc[p] % 2) ++tl.Rc[p];
+        tl.cd_off[p] = cdo;
+        cdo += static_cast<int64_t>(nrc) * cols;
+        for (int rc = 0; rc < nrc; ++rc) {
+            const int64_t nr = std::min<int64_t>(tl.Rc[p], rows - static_cast<int64_t>(rc) * tl.Rc[p]);
+            total += static_cast<double>(cols) * static_cast<double>(nr + 16);
+        }
+    }
+    const double per = total / G;
+    double x = 0.0;
+    int cur = 0;
+    long long rp = 0;
+    for (int p = 0; p < op.npairs; ++p) {
+        const int64_t rows = op.dims[op.pm[p]], cols = op.dims[op.pn[p]];
+        tl.rcseg_off[p] = static_cast<int>(rc_first.size());
+        for (int rc = 0; rc < tl.nrc[p]; ++rc) {
+            const int64_t nr = std::min<int64_t>(tl.Rc[p], rows - static_cast<int64_t>(rc) * tl.Rc[p]);
+            const double c = static_cast<double>(nr + 16);
+            rc_first.push_back(static_cast<int>(segs.size()));
+            bool open = false;
+            for (int64_t col = 0; col < cols; col += group) {
+                const int64_t ce = std::min<int64_t>(cols, col + group);
+                const double cg = c * static_cast<double>(ce - col);
+                const int target = std::min(G - 1, static_cast<int>((x + 0.5 * cg) / per));
+                if (!open || target != cur) {
+                    while (cur < target) cta_seg[++cur] = static_cast<int>(segs.size());
+                    segs.push_back(LzSeg{p, rc, static_cast<int>(col), static_cast<int>(ce), rp});
+                    rp += nr;
+                    open = true;
+                } else {
+                    segs.back().c1 = static_cast<int>(ce);
+                }
+                x += cg;
+            }
+        }
+    }
+    while (cur < G) cta_seg[++cur] = static_cast<int>(segs.size());
+    rc_first.push_back(static_cast<int>(segs.size()));
+    if (rp >= (1ll << 31)) fail(R1_ERR_INVALID_ARGUMENT, "eig: operator too large for the tiled matvec");
+    tl.nrcf = static_cast<int>(rc_first.size()) - 1;
+    tl.nseg = static_cast<int>(segs.size());
+    for (const LzSeg& sg : segs) rc_first.push_back(static_cast<int>(sg.rp));  // meta = rc_first ++ seg_rp
+    const size_t seg_bytes = segs.size() * sizeof(LzSeg);
+    const size_t cta_bytes = cta_seg.size() * sizeof(int);
+    const size_t rcf_bytes = rc_first.size() * sizeof(int);
+    const size_t off_cta = (seg_bytes + 15) & ~size_t(15);
+    const size_t off_rcf = off_cta + ((cta_bytes + 15) & ~size_t(15));
+    P.tl_meta.ensure(off_rcf + rcf_bytes + 16);
+    char* base = P.tl_meta.as<char>();
+    R1_CUDA(cudaMemcpy(base, segs.data(), seg_bytes, cudaMemcpyHostToDevice));
+    R1_CUDA(cudaMemcpy(base + off_cta, cta_seg.data(), cta_bytes, cudaMemcpyHostToDevice));
+    R1_CUDA(cudaMemcpy(base + off_rcf, rc_first.data(), rcf_bytes, cudaMemcpyHostToDevice));
+    tl.segs = reinterpret_cast<const LzSeg*>(base);
+    tl.cta_seg = reinterpret_cast<const int*>(base + off_cta);
+    tl.meta = reinterpret_cast<const int*>(base + off_rcf);
+    P.tl_coldot_n = cdo;
+    P.tl_rowpart_n = rp;
+    P.tl_G = G;
+}
 
 }  // namespace
 
@@ -1104,9 +1562,18 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
                  double decide_tol = 1e-6) {
     const int64_t n = P.op.n;
     const int maxm = static_cast<int>(std::min<int64_t>(n, 320));
+    static const char* gs = dev_env("R1_EIG_GRID");
+    static const char* gc = dev_env("R1_EIG_CLUSTER");
+    static const char* gsm = dev_env("R1_EIG_SMALL");
+    static const char* tz = dev_env("R1_EIG_TILED");  // development: 0 = the round-1 grid kernel
+    const int grid_ctas = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs))) : ctx->num_sms;
+    const int cl_size = gc ? std::max(0, std::min(16, std::atoi(gc))) : 0;
+    const bool tiled = !P.op.dense && n > kSmallN && !(cl_size > 1 && !gs) && !(tz && std::atoi(tz) == 0);
+    if (tiled && P.tl_G != grid_ctas) build_tiles(P, grid_ctas);
+    const int64_t tl_n = tiled ? P.tl_coldot_n + P.tl_rowpart_n + 16 : 0;
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
                          2 * static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 8) +
-                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 256 +
+                         2 * kMaxKrylov + P.coldot_n + P.rowpart_n + 256 + tl_n +
                          (n <= kSmallN ? (n + 16) * n : 0);
     ctx->ws_eig.ensure(need * sizeof(double));
     double* base = ctx->ws_eig.as<double>();
@@ -1144,6 +1611,12 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     op.coldot = take(std::max<int64_t>(P.coldot_n, 1));
     op.rowpart = take(std::max<int64_t>(P.rowpart_n, 1));
     a.op = P.dop.get(op, ctx->stream);
+    if (tiled) {
+        LzTiles tl = P.tl;
+        tl.coldot = take(std::max<int64_t>(P.tl_coldot_n, 1));
+        tl.rowpart = take(std::max<int64_t>(P.tl_rowpart_n, 1));
+        a.tl = P.dtl.get(tl, ctx->stream);
+    }
     a.out_value = value_dev;
     a.out_vec = vec_dev;
     static const bool dbg_text = dev_env("R1_DEBUG_EIG_TEXT") != nullptr;
@@ -1169,9 +1642,6 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     }
 
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
-    static const char* gs = dev_env("R1_EIG_GRID");
-    static const char* gc = dev_env("R1_EIG_CLUSTER");
-    static const char* gsm = dev_env("R1_EIG_SMALL");
     if (n <= kSmallN && !gs && !gc && !(gsm && std::atoi(gsm) == 0)) {
         // one thread-block cluster, rows of J / V / w on chip
         const int G = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (n + 15) / 16)));
@@ -1236,19 +1706,19 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
             return;
         }
     }
-    configure_once(reinterpret_cast<const void*>(lanczos_kernel), ctx->device, [&] {
-        R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kEigDynSmem)));
-        R1_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    auto kern = tiled ? lanczos_kernel<true> : lanczos_kernel<false>;
+    const size_t dyn_smem = tiled ? kLzDynSmem : kEigDynSmem;
+    configure_once(reinterpret_cast<const void*>(kern), ctx->device, [&] {
+        R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(dyn_smem)));
+        R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     });
     int per_sm = 0;
-    R1_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_kernel, kEigThreads,
-                                                          kEigDynSmem));
+    R1_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEigThreads, dyn_smem));
     if (per_sm < 1) fail(R1_ERR_CUDA, "lanczos kernel cannot be resident");
     void* args[] = {&a};
     // (small operators took the cluster kernel above; R1_EIG_CLUSTER / R1_EIG_GRID
     // are development overrides for this grid kernel)
-    const int cl_size = gc ? std::max(0, std::min(16, std::atoi(gc))) : 0;
     if (cl_size > 1 && !gs) {
         // the whole Lanczos run on ONE thread-block cluster: cluster barriers
         // instead of cooperative grid syncs
@@ -1265,11 +1735,10 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        R1_CUDA(cudaLaunchKernelEx(&cfg, lanczos_kernel, a));
+        R1_CUDA(cudaLaunchKernelEx(&cfg, lanczos_kernel<false>, a));
     } else {
-        const int grid = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs))) : ctx->num_sms;
-        R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_kernel), dim3(grid),
-                                            dim3(kEigThreads), args, kEigDynSmem, ctx->stream));
+        R1_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid_ctas),
+                                            dim3(kEigThreads), args, dyn_smem, ctx->stream));
     }
     check_launch(ctx, "lanczos_kernel");
     finish_lanczos(ctx, a, info_host, stats_host);

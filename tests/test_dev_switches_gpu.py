@@ -30,7 +30,7 @@ for n in (40, 333, 700):
     if y is not None:
         assert min(np.max(np.abs(y - yr)), np.max(np.abs(y + yr))) <= 1e-8, n
 # eigen step on block operators (small n: cluster or grid kernel) against numpy
-for dims in ((3, 4, 2), (20, 30, 25), (60, 60, 60)):
+for dims in ((3, 4, 2), (20, 30, 25), (60, 60, 60), (500, 600, 50)):
     rng = np.random.default_rng(sum(dims))
     a = rng.standard_normal(int(np.prod(dims)))
     f = [rng.standard_normal(k) for k in dims]
@@ -62,7 +62,7 @@ DEV_LIB = os.path.join(ROOT, "paper_2403_01778_b200", "librank1_b200_dev.so")
 
 
 @pytest.mark.parametrize("env", [{"R1_SOLVER_GRAPHS": "0"}, {"R1_BK_GRID_SOLVE": "1"},
-                                 {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"},
+                                 {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"}, {"R1_EIG_TILED": "0"},
                                  {"R1_SWEEP_NRA8": "0"}, {"R1_SWEEP_MERGE": "0"}])
 def test_switch_paths(gpu_ctx, env):
     if not os.path.exists(DEV_LIB):

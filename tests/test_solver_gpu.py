@@ -19,7 +19,12 @@ def _blocks(oracle, dims, seed):
                                   (20, 20, 20, 20),
                                   # n = 301 (odd), 1024 (largest single-cluster
                                   # kernel: J rows in L2), 1025 (grid kernel)
-                                  (101, 100, 100), (400, 324, 300), (400, 325, 300)])
+                                  (101, 100, 100), (400, 324, 300), (400, 325, 300),
+                                  # tiled grid kernel (n > 1024): d = 2, a 2-row mode
+                                  # (row chunks of 2), d = 4, odd extents, rows over
+                                  # several 256-row chunks
+                                  (500, 600), (2, 3, 1100), (300, 300, 250, 200), (257, 513, 301),
+                                  (1100, 60, 7)])
 def test_eig_blocks_matches_reference(gpu_ctx, oracle, ref, dims):
     import paper_2403_01778_b200 as r1
     a, f, blocks = _blocks(oracle, dims, 31)
