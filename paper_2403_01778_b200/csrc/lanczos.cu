@@ -83,6 +83,7 @@ struct EigArgs {
     double warm_noise; // weight of the random component of a warm start vector
     double decide_tol; // relative Ritz residual at which the non-picked end counts as decided
     const struct LzTiles* tl;  // tiled matvec plan (TILED grid kernel), device
+    unsigned long long* lzt;   // diagnostics (R1_DEBUG_EIG): CTA 1's phase-A split, ns
 };
 
 __device__ __forceinline__ double hash_unit(uint64_t i, uint64_t salt) {
@@ -462,7 +463,17 @@ __device__ __forceinline__ double2 ld_keep2(const double* p, uint64_t pol) {
 // doubles, rps: 32 kLzNQ, dacc: kmax + 1 (shared memory).
 __device__ __noinline__ void lz_phase_a(const BlockOp& op, const LzTiles& tl, const double* __restrict__ x,
                            const double* __restrict__ V, int64_t n, int kmax, double* pdot, int ld,
-                           double* red, double* rps, double* dacc) {
+                           double* red, double* rps, double* dacc, unsigned long long* tdbg) {
+    unsigned long long tq0 = 0, tq1 = 0, tq2 = 0;
+    auto tmark = [&](int slot, unsigned long long& last) {
+        if (tdbg && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (slot >= 0) tdbg[slot] += t - last;
+            last = t;
+        }
+    };
+    tmark(-1, tq0);
     constexpr int RMAX = 32 * kLzNQ;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t pol = policy_evict_last();
@@ -520,6 +531,8 @@ __device__ __noinline__ void lz_phase_a(const BlockOp& op, const LzTiles& tl, co
         };
         const bool v2 = tl.v2[p] != 0;
         // four columns per iteration: 4 * kLzNQ doubles in flight per lane
+        // (software-pipelining two such sets measured slower: branches and
+        // register pressure at the 128-register cap)
         constexpr int CU = 4;
         int c = sg.c0 + warp;
         for (; c + (CU - 1) * kLzWarps < sg.c1; c += CU * kLzWarps) {
@@ -545,6 +558,8 @@ __device__ __noinline__ void lz_phase_a(const BlockOp& op, const LzTiles& tl, co
             for (int off = 16; off >= 1; off >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, off);
             if (lane == 0) cd[c] = dd;
         }
+        tq1 = tq0;
+        tmark(0, tq1);  // column loop (thread 0's view)
         // row partial of the segment: the warps' accumulators in warp order
 #pragma unroll
         for (int q = 0; q < kLzNQ; ++q) red[warp * RMAX + 64 * (q >> 1) + 2 * lane + (q & 1)] = racc[q];
@@ -557,6 +572,8 @@ __device__ __noinline__ void lz_phase_a(const BlockOp& op, const LzTiles& tl, co
             tl.rowpart[sg.rp + r] = v;
         }
         __syncthreads();
+        tq2 = tq1;
+        tmark(1, tq2);
         // CGS pass-1 dot partials of this segment's contributions (warp per k)
         const double* vm = V + op.offs[m] + i0;
         const double* vn = V + op.offs[nn];
@@ -585,6 +602,8 @@ __device__ __noinline__ void lz_phase_a(const BlockOp& op, const LzTiles& tl, co
             if (lane == 0) dacc[k] += t;
         }
         __syncthreads();
+        tq0 = tq2;
+        tmark(2, tq0);
     }
     for (int k = threadIdx.x; k <= kmax; k += blockDim.x) pdot[static_cast<int64_t>(blockIdx.x) * ld + k] = dacc[k];
 }
@@ -790,39 +809,115 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
     bool zero_op = false;
     double anorm = 0.0;
     double inv_beta = 1.0;  // V[:,j] = w * inv_beta for j > 0 (materialised in phase B)
+    // TILED: a convergence check decided at the end of a step, run by CTA 0
+    // during the next step's matvec
+    bool pend_check = false, pend_full = false, pend_limit = false;
+    double pend_beta = 0.0;
     for (;;) {
         if constexpr (TILED) {
             extern __shared__ double dsm[];
-            // [A] J v_j partials (single read of the blocks) + CGS pass-1 dot partials
+            // [A] J v_j partials (single read of the blocks) + CGS pass-1 dot
+            // partials.  CTA 0 has no matvec share (build_tiles): it runs the
+            // convergence check of the previous step meanwhile; the decision
+            // is read after the barrier (an unneeded step's partials are
+            // simply dropped).
             mark(7);
+            if (pend_check && blockIdx.x == 0)
+                t_extremes(a, j, pend_beta, pend_full, restarts, dsm, kMaxKrylov);
+            mark(5);
             lz_phase_a(op, tls, a.V + static_cast<int64_t>(j) * n, a.V, n, j, a.pdot1, ld, dsm,
-                       dsm + kLzWarps * 32 * kLzNQ, dsm + (kLzWarps + 1) * 32 * kLzNQ);
+                       dsm + kLzWarps * 32 * kLzNQ, dsm + (kLzWarps + 1) * 32 * kLzNQ,
+                       blockIdx.x == 1 ? a.lzt : nullptr);
             mark(0);
             gsync();
             mark(1);
-            // [B] own rows: y = J v_j, w1 = y - V h1; pass-2 dot and ||w1||^2 partials
+            if (pend_check) {
+                pend_check = false;
+                if (a.ctl[0]) break;
+                if (pend_limit) {
+                    if (restarts >= a.max_restarts) break;  // best effort: ctl[0] stays 0
+                    // restart from (x_lo + x_hi): both ends stay represented
+                    ++restarts;
+                    first_check = a.min_steps;
+                    for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
+                        double s0 = 0.0, s1 = 0.0;
+                        for (int k = 0; k < j; ++k) {
+                            const double v = a.V[t + static_cast<int64_t>(k) * n];
+                            s0 = fma(v, a.sT[k], s0);
+                            s1 = fma(v, a.sT[kMaxKrylov + k], s1);
+                        }
+                        a.w[t] = s0 + s1;
+                    }
+                    gsync();
+                    set_v0_from_w();
+                    j = 0;
+                    anorm = 0.0;
+                    continue;
+                }
+            }
+            // [B] own rows, an 8-lane group per row (group g = 4 warp + lane / 8,
+            // rows r0 + g + 64 round): y = J v_j, w1 = y - V h1 (h1 from the
+            // folded partials), the pass-2 dots V' w1 and ||w1||^2.  Round 0
+            // keeps w1 and its V entries k = sl + 8u < 32 in registers for the
+            // update after the next barrier.
             reduce_dots(a.pdot1, j);  // hsh = h1 / scale
             const double sc = op.scale;
-            // an 8-lane group per row
-            for (int64_t tb = r0 + 4 * warp; tb < r1; tb += 4 * nw) {
-                const int64_t t = tb + (lane >> 3);
+            const int g = 4 * warp + (lane >> 3), sl = lane & 7;
+            double w1r = 0.0, vr[4] = {0.0, 0.0, 0.0, 0.0}, acc2[4] = {0.0, 0.0, 0.0, 0.0}, ssq = 0.0;
+            for (int64_t tb = r0; tb < r1; tb += 64) {
+                const int64_t t = tb + g;
                 const bool ok = t < r1;
-                const int sl = lane & 7;
                 const double y = lz_row_sum8(op, tls, lzmeta, ok ? t : r0, sl) * sc;
+                double v4[4];
                 double s = 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = sl + 8 * u;
+                    v4[u] = (ok && k <= j) ? a.V[t + static_cast<int64_t>(k) * n] : 0.0;
+                    s = fma(v4[u], k <= j ? hsh[k] * sc : 0.0, s);
+                }
                 if (ok)
-                    for (int k = sl; k <= j; k += 8) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k] * sc, s);
+                    for (int k = sl + 32; k <= j; k += 8) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k] * sc, s);
 #pragma unroll
                 for (int off = 4; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                if (ok && sl == 0) a.w[t] = y - s;
+                const double w1 = ok ? y - s : 0.0;
+                if (ok && sl == 0) a.w[t] = w1;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc2[u] = fma(v4[u], w1, acc2[u]);
+                if (sl == 0) ssq = fma(w1, w1, ssq);
+                if (tb == r0) {
+                    w1r = w1;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) vr[u] = v4[u];
+                }
             }
-            __syncthreads();
-            partial_dots(a.pdot2, j);
+            // pass-2 dot partials k < 32 in a fixed order: groups, then the CTA
             {
-                double ss = 0.0;
-                for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) ss = fma(a.w[t], a.w[t], ss);
-                ss = cta_sum(ss, red);
-                if (threadIdx.x == 0) a.part[blockIdx.x] = ss;
+                double* d2 = dsm;  // [64 groups][32 k] + [64] norms (phase-A scratch, free here)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) d2[g * 32 + sl + 8 * u] = acc2[u];
+                if (sl == 0) d2[64 * 32 + g] = ssq;
+                __syncthreads();
+                if (threadIdx.x <= min(j, 31)) {
+                    double v = 0.0;
+                    for (int q = 0; q < 64; ++q) v += d2[q * 32 + threadIdx.x];
+                    a.pdot2[static_cast<int64_t>(blockIdx.x) * ld + threadIdx.x] = v;
+                }
+                if (threadIdx.x == 32) {
+                    double v = 0.0;
+                    for (int q = 0; q < 64; ++q) v += d2[64 * 32 + q];
+                    a.part[blockIdx.x] = v;
+                }
+                if (j >= 32) {  // long Krylov spaces (cold starts): k >= 32 from memory
+                    for (int k = 32 + warp; k <= j; k += nw) {
+                        const double* vk = a.V + static_cast<int64_t>(k) * n;
+                        double t2 = 0.0;
+                        for (int64_t t = r0 + lane; t < r1; t += 32) t2 = fma(vk[t], a.w[t], t2);
+#pragma unroll
+                        for (int off = 16; off >= 1; off >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, off);
+                        if (lane == 0) a.pdot2[static_cast<int64_t>(blockIdx.x) * ld + k] = t2;
+                    }
+                }
             }
             mark(2);
             gsync();
@@ -857,48 +952,42 @@ __global__ void __launch_bounds__(kEigThreads, 1) lanczos_kernel(const EigArgs a
                 nrm = sqrt(grid_sum(a.part, 0));
                 for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) vnext[t] = a.w[t] / nrm;
             } else if (!space_full) {
+                // v_{j+1} = (w1 - V h2) / beta: round 0 from registers
                 const double ib = 1.0 / nrm;
-                for (int64_t tb = r0 + 4 * warp; tb < r1; tb += 4 * nw) {
-                    const int64_t t = tb + (lane >> 3);
+                for (int64_t tb = r0; tb < r1; tb += 64) {
+                    const int64_t t = tb + g;
                     const bool ok = t < r1;
-                    const int sl = lane & 7;
-                    double s = 0.0;
+                    double s = 0.0, w1 = w1r;
+                    if (tb == r0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int k = sl + 8 * u;
+                            s = fma(vr[u], k <= j ? hsh[k] : 0.0, s);
+                        }
+                    } else {
+                        w1 = ok ? a.w[t] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int k = sl + 8 * u;
+                            if (ok && k <= j) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k], s);
+                        }
+                    }
                     if (ok)
-                        for (int k = sl; k <= j; k += 8) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k], s);
+                        for (int k = sl + 32; k <= j; k += 8) s = fma(a.V[t + static_cast<int64_t>(k) * n], hsh[k], s);
 #pragma unroll
                     for (int off = 4; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                    if (ok && sl == 0) vnext[t] = (a.w[t] - s) * ib;
+                    if (ok && sl == 0) vnext[t] = (w1 - s) * ib;
                 }
             }
             ++j;
             const bool size_limit = (j == a.maxm) || space_full;
-            const bool check = ((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit;
+            pend_check = ((j >= first_check && j % a.check_every == 0) && !breakdown) || size_limit;
+            pend_beta = breakdown ? 0.0 : nrm;
+            pend_full = space_full;
+            pend_limit = size_limit;
             mark(4);
-            if (check && blockIdx.x == 0) t_extremes(a, j, breakdown ? 0.0 : nrm, space_full, restarts, dsm, kMaxKrylov);
-            mark(5);
             gsync();
             mark(6);
-            if (check) {
-                if (a.ctl[0]) break;
-                if (size_limit) {
-                    if (restarts >= a.max_restarts) break;
-                    ++restarts;
-                    first_check = a.min_steps;
-                    for (int64_t t = r0 + threadIdx.x; t < r1; t += blockDim.x) {
-                        double s0 = 0.0, s1 = 0.0;
-                        for (int k = 0; k < j; ++k) {
-                            const double v = a.V[t + static_cast<int64_t>(k) * n];
-                            s0 = fma(v, a.sT[k], s0);
-                            s1 = fma(v, a.sT[kMaxKrylov + k], s1);
-                        }
-                        a.w[t] = s0 + s1;
-                    }
-                    gsync();
-                    set_v0_from_w();
-                    j = 0;
-                    anorm = 0.0;
-                }
-            }
             continue;
         }
         // [A] matvec partials of v_j
@@ -1463,9 +1552,11 @@ void build_tiles(EigPlan& P, int G) {
             total += static_cast<double>(cols) * static_cast<double>(nr + 16);
         }
     }
-    const double per = total / G;
+    // CTA 0 runs the convergence checks while the others do the matvec
+    const int first = G > 1 ? 1 : 0;
+    const double per = total / (G - first);
     double x = 0.0;
-    int cur = 0;
+    int cur = first;
     long long rp = 0;
     for (int p = 0; p < op.npairs; ++p) {
         const int64_t rows = op.dims[op.pm[p]], cols = op.dims[op.pn[p]];
@@ -1478,7 +1569,7 @@ void build_tiles(EigPlan& P, int G) {
             for (int64_t col = 0; col < cols; col += group) {
                 const int64_t ce = std::min<int64_t>(cols, col + group);
                 const double cg = c * static_cast<double>(ce - col);
-                const int target = std::min(G - 1, static_cast<int>((x + 0.5 * cg) / per));
+                const int target = first + std::min(G - 1 - first, static_cast<int>((x + 0.5 * cg) / per));
                 if (!open || target != cur) {
                     while (cur < target) cta_seg[++cur] = static_cast<int>(segs.size());
                     segs.push_back(LzSeg{p, rc, static_cast<int>(col), static_cast<int>(ce), rp});
@@ -1543,6 +1634,10 @@ void finish_lanczos(r1_context* ctx, const EigArgs& a, int* info_host, double* s
                      static_cast<long long>(n), ctl[0], ctl[1], ctl[2], ctl[3], ctl[4], st[0], st[1],
                      st[2], st[3], st[8] * 1e-3, st[9] * 1e-3, st[10] * 1e-3, st[11] * 1e-3,
                      st[12] * 1e-3, st[13] * 1e-3, st[14] * 1e-3, st[15] * 1e-3);
+        unsigned long long lz[3] = {0, 0, 0};
+        if (a.lzt) R1_CUDA(cudaMemcpy(lz, a.lzt, sizeof(lz), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[r1 eig] CTA 1 phase A: columns %.1f us, row partials %.1f us, pass-1 dots %.1f us\n",
+                     lz[0] * 1e-3, lz[1] * 1e-3, lz[2] * 1e-3);
     }
     if (info_host || stats_host) {
         int ctl[5];
@@ -1588,10 +1683,12 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.maxm = maxm;
     static const char* ce = dev_env("R1_EIG_CHECK");
     static const char* ms = dev_env("R1_EIG_MIN_STEPS");
-    a.check_every = n <= 64 ? 1 : (ce ? std::max(1, std::atoi(ce)) : 8);
+    // the tiled grid kernel hides a check behind the next step's matvec:
+    // check every 2 steps from step 4 (warm C5 solves: 8 -> 6 steps)
+    a.check_every = n <= 64 ? 1 : (ce ? std::max(1, std::atoi(ce)) : (tiled ? 2 : 8));
     // the warm start (previous eigenvector) converges the picked end within a
     // few steps; the first check comes after 8 (C2 solve 0.87 -> 0.33 ms)
-    a.min_steps = static_cast<int>(std::min<int64_t>(n, ms ? std::max(1, std::atoi(ms)) : 8));
+    a.min_steps = static_cast<int>(std::min<int64_t>(n, ms ? std::max(1, std::atoi(ms)) : (tiled ? 4 : 8)));
     a.max_restarts = 6;
     a.tol = 1e-13;
     a.x0 = x0;
@@ -1606,6 +1703,12 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     a.pdot2 = take(static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 1));
     a.sT = take(2 * kMaxKrylov);
     a.stats = take(16);
+    static const bool dbg_eig = dev_env("R1_DEBUG_EIG") != nullptr;
+    a.lzt = reinterpret_cast<unsigned long long*>(take(4));
+    if (dbg_eig)
+        R1_CUDA(cudaMemsetAsync(a.lzt, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    else
+        a.lzt = nullptr;
     a.ctl = reinterpret_cast<int*>(take(4));
     BlockOp op = P.op;
     op.coldot = take(std::max<int64_t>(P.coldot_n, 1));
