@@ -1216,6 +1216,8 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
     // 4 (was 16): the small recursion levels (60^3 at C4) ran on one CTA
     const int64_t min_panels = mp_env ? std::max(1, std::atoi(mp_env)) : 4;
     int64_t ncta = std::min<int64_t>(num_sms, std::max<int64_t>(1, npanels / min_panels));
+    static const char* nc_env = dev_env("R1_SWEEP_NCTA");  // development: cap the grid
+    if (nc_env) ncta = std::max<int64_t>(1, std::min<int64_t>(ncta, std::atoi(nc_env)));
     L.ncta = static_cast<int>(ncta);
     std::vector<Seg> segs;
     std::vector<int> cta_seg(L.ncta + 1, 0);
