@@ -23,7 +23,7 @@ def _blocks(oracle, dims, seed):
                                   # tiled grid kernel (n > 1024): d = 2, a 2-row mode
                                   # (row chunks of 2), d = 4, odd extents, rows over
                                   # several 256-row chunks
-                                  (500, 600), (2, 3, 1100), (300, 300, 250, 200), (257, 513, 301),
+                                  (500, 600), (2, 3, 1100), (800, 200, 20, 10), (257, 513, 301),
                                   (1100, 60, 7)])
 def test_eig_blocks_matches_reference(gpu_ctx, oracle, ref, dims):
     import paper_2403_01778_b200 as r1
