@@ -985,28 +985,51 @@ __global__ void finish_kernel(const FinishArgs f) {
 }
 
 // B01 when tiles hold many segments (deep o ranges split over many CTAs, e.g.
-// a single 60 x 60 face tile): a warp per element, lanes over the segments,
-// then a fixed-pattern butterfly — still one fixed summation order.
-__global__ void finish_b01_warp_kernel(const FinishArgs f) {
-    const int lane = threadIdx.x & 31;
+// a single 60 x 60 face tile): a CTA takes 32 consecutive offsets of one
+// tile's partial slots (lanes, coalesced) and its 16 warps take 16 equal
+// slices of the tile's segments (8 loads in flight per lane); the slices are
+// combined in warp order through shared memory — one fixed summation order.
+constexpr int kB01Warps = 16;
+__global__ void __launch_bounds__(kB01Warps * 32) finish_b01_seg_kernel(const FinishArgs f) {
+    __shared__ double red[kB01Warps][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t tile_elems = static_cast<int64_t>(f.r0) * f.t1;
-    const int K = f.K;
-    for (int64_t e = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-         e < f.n_b01; e += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-        const int64_t i1 = e / f.I0, i0 = e - i1 * f.I0;
-        const int64_t p = i1 & (K - 1), c = i1 >> f.lgK;
-        const int64_t r = p * f.I0 + i0;
-        const int g0 = static_cast<int>(r / f.r0), g1 = static_cast<int>(c / f.t1);
-        const int tile = g0 + f.G0 * g1;
-        const double* src = f.P01 + (c - static_cast<int64_t>(g1) * f.t1) * f.r0 +
-                            (r - static_cast<int64_t>(g0) * f.r0);
+    const int64_t per_tile = (tile_elems + 31) / 32;
+    const int ntiles = f.G0 * f.G1;
+    const int64_t units = static_cast<int64_t>(ntiles) * per_tile;
+    const int64_t MI0 = static_cast<int64_t>(f.K) * f.I0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tile = static_cast<int>(u / per_tile);
+        const int64_t off = (u - static_cast<int64_t>(tile) * per_tile) * 32 + lane;
+        const int g0 = tile % f.G0, g1 = tile / f.G0;
+        const int64_t j = off / f.r0, i = off - j * f.r0;
+        const int64_t r = static_cast<int64_t>(g0) * f.r0 + i, c = static_cast<int64_t>(g1) * f.t1 + j;
+        const bool valid = off < tile_elems && i < f.r0 && r < MI0 && c < f.MI1;
         const int sb = __ldg(f.tile_seg + tile), se = __ldg(f.tile_seg + tile + 1);
+        const int per = (se - sb + kB01Warps - 1) / kB01Warps;
+        const int k0 = sb + warp * per, k1 = min(se, k0 + per);
+        const double* src = f.P01 + (valid ? off : 0);
         double s = 0.0;
-#pragma unroll 4
-        for (int k = sb + lane; k < se; k += 32) s += __ldcs(src + k * tile_elems);
+        int k = k0;
+        for (; k + 8 <= k1; k += 8) {
+            double v[8];
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) f.b01[e] = s;
+            for (int q = 0; q < 8; ++q) v[q] = valid ? __ldcs(src + (k + q) * tile_elems) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += v[q];
+        }
+        for (; k < k1; ++k) s += valid ? __ldcs(src + k * tile_elems) : 0.0;
+        red[warp][lane] = s;
+        __syncthreads();
+        if (warp == 0 && valid) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kB01Warps; ++w) t += red[w][lane];
+            // merged row r = p I0 + i0 of merged column c: B01[i0 + I0 (K c + p)]
+            const int64_t pcl = r / f.I0, i0 = r - pcl * f.I0;
+            f.b01[i0 + f.I0 * (f.K * c + pcl)] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -1631,12 +1654,11 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         fastdiv_init(L.r0, f.m_r0, f.s_r0);
         fastdiv_init(L.t1, f.m_t1, f.s_t1);
         if (L.nseg >= 64 * L.ntiles) {
-            // many segments per tile: B01 by warps, C0/C1 (if any) below
-            const int64_t warps = f.n_b01;
-            const int grid = static_cast<int>(std::max<int64_t>(
-                1, std::min<int64_t>((warps * 32 + 255) / 256, int64_t(32) * ctx->num_sms)));
-            finish_b01_warp_kernel<<<grid, 256, 0, ctx->stream>>>(f);
-            check_launch(ctx, "finish_b01_warp_kernel");
+            // many segments per tile: B01 by segment slices, C0/C1 (if any) below
+            const int64_t units = static_cast<int64_t>(L.ntiles) * ((static_cast<int64_t>(L.r0) * L.t1 + 31) / 32);
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(4) * ctx->num_sms)));
+            finish_b01_seg_kernel<<<grid, kB01Warps * 32, 0, ctx->stream>>>(f);
+            check_launch(ctx, "finish_b01_seg_kernel");
             f.b01 = nullptr;
             f.n_b01 = 0;
             if (f.n_c0 + f.n_c1 == 0) continue;
