@@ -1667,7 +1667,9 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     static const char* tz = dev_env("R1_EIG_TILED");  // development: 0 = the round-1 grid kernel
     const int grid_ctas = gs ? std::max(1, std::min(ctx->num_sms, std::atoi(gs))) : ctx->num_sms;
     const int cl_size = gc ? std::max(0, std::min(16, std::atoi(gc))) : 0;
-    const bool tiled = !P.op.dense && n > kSmallN && !(cl_size > 1 && !gs) && !(tz && std::atoi(tz) == 0);
+    // small operators take the single-cluster kernel below (unless overridden)
+    const bool small_pref = n <= kSmallN && !gs && !gc && !(gsm && std::atoi(gsm) == 0);
+    const bool tiled = !P.op.dense && !small_pref && !(cl_size > 1 && !gs) && !(tz && std::atoi(tz) == 0);
     if (tiled && P.tl_G != grid_ctas) build_tiles(P, grid_ctas);
     const int64_t tl_n = tiled ? P.tl_coldot_n + P.tl_rowpart_n + 16 : 0;
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
@@ -1749,7 +1751,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     }
 
     R1_CUDA(cudaMemsetAsync(a.ctl, 0, 4 * sizeof(int), ctx->stream));
-    if (n <= kSmallN && !gs && !gc && !(gsm && std::atoi(gsm) == 0)) {
+    if (small_pref) {
         // one thread-block cluster, rows of J / V / w on chip
         const int G = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (n + 15) / 16)));
         const int64_t R = (n + G - 1) / G;
