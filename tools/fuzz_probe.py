@@ -16,7 +16,8 @@ from oracle import ref  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
-solves_only = len(sys.argv) > 3 and sys.argv[3] == "solves"  # skip the sweep checks, iHOSCF every case
+mode = sys.argv[3] if len(sys.argv) > 3 else ""  # "solves" / "hoscf": skip the sweep checks, solve every case
+solves_only = mode in ("solves", "hoscf")
 O.build()
 t0 = time.time()
 nb = ns = 0
@@ -38,7 +39,7 @@ while time.time() - t0 < budget:
             bad.append(("build_j", dims))
         nb += 1
     if d >= 3 and np.prod(dims) <= 2e5 and min(dims) >= 2 and (solves_only or rng.random() < 0.25):
-        alg = "ihoscf" if solves_only or rng.random() < 0.5 else "hoscf"
+        alg = "hoscf" if mode == "hoscf" else ("ihoscf" if solves_only or rng.random() < 0.5 else "hoscf")
         seed = int(rng.integers(100))
         rep = r1.solve(alg, r1.DenseTensor(dims, a), r1.SolveOptions(tol=1e-10, max_iters=300, seed=seed))
         w = ref.solve(alg, a, dims, tol=1e-10, max_iters=300, seed=seed)
