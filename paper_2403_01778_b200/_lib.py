@@ -170,6 +170,7 @@ EXTRA_SIGNATURES = {
     "r1x_eig_dense_lanczos": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, _dp, _dp]),
     "r1x_ldlt": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.POINTER(ctypes.c_int), _dp, _dp,
                                 ctypes.POINTER(ctypes.c_int), _dp]),
+    "r1x_ldlt_time": (ctypes.c_int, [_vp, ctypes.c_int64, _dp, ctypes.c_int, _dp]),
 }
 
 _lib = None

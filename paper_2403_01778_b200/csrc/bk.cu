@@ -108,6 +108,15 @@ __global__ void bk_init_kernel(int* perm, char* ps, int64_t n) {
     }
 }
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialisation attribute may start while its predecessor runs; it
+// lets its own dependents launch at once and waits for the predecessor's
+// completion (and memory flush) before touching any data.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ void argmax_merge(double& v, int64_t& i, double v2, int64_t i2) {
     if (v2 > v || (v2 == v && i2 < i)) {
         v = v2;
@@ -141,6 +150,7 @@ __global__ void __launch_bounds__(kBkThreads) bk_panel_kernel(const BkArgs a) {
     __shared__ double sv[32];
     __shared__ int64_t si[32];
     __shared__ double Lr[kBkW];  // row k (then imax) of the panel's L columns
+    pdl_enter();
     const int64_t n = a.n;
     const int64_t k0 = a.ctl[0];
     if (k0 >= n) return;
@@ -369,24 +379,37 @@ __device__ __forceinline__ double l_entry(const double* wrow, const StepCoef* cf
     return 0.0;
 }
 
-// (|v|, index) arg-max, first index on ties; v < 0 marks "no candidate"
-__device__ __forceinline__ void amax_merge(double& v, int& i, double& s, double v2, int i2, double s2) {
-    if (v2 > v || (v2 == v && i2 < i)) {
-        v = v2;
-        i = i2;
-        s = s2;
-    }
-}
-
-__device__ __forceinline__ void warp_amax(double& v, int& i, double& s) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1)
-        amax_merge(v, i, s, __shfl_xor_sync(0xffffffffu, v, off), __shfl_xor_sync(0xffffffffu, i, off),
-                   __shfl_xor_sync(0xffffffffu, s, off));
-}
-
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+// Magnitude keys for the warp reductions: for v >= 0 the IEEE bit pattern
+// orders like the value, so key = bits(v) + 1 (0 = no candidate / NaN) and a
+// max / arg-max is three (two) redux.sync instead of a five-level butterfly.
+// Same result as the (|v|, index) merge rule: largest value, then the first
+// index; NaN never wins (as `fabs(x) > best` never holds for NaN).
+__device__ __forceinline__ unsigned long long mag_key(double v) {
+    return v >= 0.0 ? static_cast<unsigned long long>(__double_as_longlong(fabs(v))) + 1ull : 0ull;
+}
+
+__device__ __forceinline__ double key_mag(unsigned long long key, double none) {
+    return key ? __longlong_as_double(static_cast<long long>(key - 1ull)) : none;
+}
+
+// warp arg-max of (key, idx): max key, then min idx among the max keys
+__device__ __forceinline__ void warp_key_argmax(unsigned long long& key, unsigned& idx) {
+    const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    idx = __reduce_min_sync(0xffffffffu, hi == mh && lo == ml ? idx : 0xffffffffu);
+    key = (static_cast<unsigned long long>(mh) << 32) | ml;
+}
+
+__device__ __forceinline__ unsigned long long warp_key_max(unsigned long long key) {
+    const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return (static_cast<unsigned long long>(mh) << 32) | ml;
 }
 
 // NT threads per CTA; TRACE compiles the phase timers in (their register
@@ -396,12 +419,13 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
     static_assert((NT & (NT - 1)) == 0, "row mapping uses a mask");
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double dsm[];
+    pdl_enter();
     double* Ws = dsm;                 // [rcap][kBkW] this CTA's rows of W
     double* Cs = Ws + rcap * kBkW;    // [rcap] updated column k
     double* Cis = Cs + rcap;          // [rcap] updated column imax
     double* Raw = Cis + rcap;         // [2 pairs][2][rcap] raw stored columns (k, k+1)
-    __shared__ double sv[NT / 32], ss[NT / 32];
-    __shared__ int si[NT / 32];
+    __shared__ unsigned long long skey[NT / 32];  // per-warp reduction keys
+    __shared__ unsigned sidx[NT / 32];
     __shared__ double Lr[kBkW], Wim[kBkW];  // L row being applied; W row of imax
     __shared__ double pend[2][kBkW];
     __shared__ int pend_row[2], pend_n[2];
@@ -530,26 +554,29 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
                 if (i == k + 1) own[1] = sacc;
             }
         }
-        warp_amax(bv, bi, bs);
-        if ((tid & 31) == 0) {
-            sv[tid >> 5] = bv;
-            si[tid >> 5] = bi;
-            ss[tid >> 5] = bs;
+        {
+            unsigned long long key = mag_key(bv);
+            unsigned idx = key ? static_cast<unsigned>(bi) : 0xffffffffu;
+            warp_key_argmax(key, idx);
+            if ((tid & 31) == 0) {
+                skey[tid >> 5] = key;
+                sidx[tid >> 5] = idx;
+            }
         }
         __syncthreads();
-        if (tid < kBkMsg * G) {
-            // CAND record of this CTA -> CTA tid / 4
-            const int f = tid & 3;
-            double v = 0.0;
-            if (f < 2) {
-                double cv = -1.0, cs = 0.0;
-                int ci = n;
-                for (int w = 0; w < NT / 32; ++w) amax_merge(cv, ci, cs, sv[w], si[w], ss[w]);
-                v = f == 0 ? static_cast<double>(ci) : cs;
-            } else {
-                v = own[f - 2];
+        if (tid < 32) {
+            // CAND record of this CTA (arg-max index and signed value, or n / 0
+            // without a candidate; c_k(k), c_k(k+1)) -> every CTA; warp 0 sends
+            unsigned long long key = tid < NT / 32 ? skey[tid] : 0ull;
+            unsigned idx = tid < NT / 32 ? sidx[tid] : 0xffffffffu;
+            warp_key_argmax(key, idx);
+            const double ci = key ? static_cast<double>(idx) : static_cast<double>(n);
+            const double cs = key ? Cs[static_cast<int>(idx) - lo] : 0.0;
+            for (int e = tid; e < kBkMsg * G; e += 32) {
+                const int f = e & 3;
+                const double v = f == 0 ? ci : (f == 1 ? cs : own[f - 2]);
+                send8(&candm[b][me][f], v, &bars[b], e >> 2);
             }
-            send8(&candm[b][me][f], v, &bars[b], tid >> 2);
         }
         mark(2);
         if (tid == 0) expect_bytes(&bars[b], static_cast<uint32_t>(G * kBkMsg * 8));
@@ -559,17 +586,21 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         int imax;
         {
             const int lane = tid & 31;
-            int ii = lane < G ? static_cast<int>(candm[b][lane][0]) : n;
-            double sg = lane < G ? candm[b][lane][1] : 0.0;
-            double v = ii < n ? fabs(sg) : -1.0;
-            warp_amax(v, ii, sg);
-            colmax = v;
-            imax = ii;
-            ckimax = sg;
-        }
-        if (colmax < 0.0) {
-            colmax = 0.0;
-            imax = k;
+            const int ii = lane < G ? static_cast<int>(candm[b][lane][0]) : n;
+            const double sg = lane < G ? candm[b][lane][1] : 0.0;
+            unsigned long long key = ii < n ? mag_key(fabs(sg)) : 0ull;
+            unsigned idx = key ? static_cast<unsigned>(ii) : 0xffffffffu;
+            warp_key_argmax(key, idx);
+            if (key) {
+                colmax = key_mag(key, 0.0);
+                imax = static_cast<int>(idx);
+                const unsigned wl = __ballot_sync(0xffffffffu, ii == imax);
+                ckimax = __shfl_sync(0xffffffffu, sg, __ffs(wl) - 1);
+            } else {
+                colmax = 0.0;
+                imax = k;
+                ckimax = 0.0;
+            }
         }
         const double ckk = candm[b][owner(k)][2];
         const double ckk1 = k + 1 < n ? candm[b][owner(k + 1)][3] : 0.0;
@@ -627,30 +658,27 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
                 if (i == k) own[3] = sacc;
                 if (i == k + 1) own[4] = sacc;
             }
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) rv = fmax(rv, __shfl_xor_sync(0xffffffffu, rv, off));
-            if ((tid & 31) == 0) sv[tid >> 5] = rv;
+            {
+                const unsigned long long key = warp_key_max(mag_key(rv));
+                if ((tid & 31) == 0) skey[tid >> 5] = key;
+            }
             __syncthreads();
             const int rb = 2 + (rstep & 1);
-            if (tid < kBkMsg * G) {
-                const int f = tid & 3;
-                double v;
-                if (f == 0) {
-                    v = -1.0;
-                    for (int w = 0; w < NT / 32; ++w) v = fmax(v, sv[w]);
-                } else {
-                    v = own[f + 1];
+            if (tid < 32) {
+                // RMAX record (row-max partial or -1, c_imax(imax), c_imax(k),
+                // c_imax(k+1)) -> every CTA; warp 0 sends
+                const double rmx = key_mag(warp_key_max(tid < NT / 32 ? skey[tid] : 0ull), -1.0);
+                for (int e = tid; e < kBkMsg * G; e += 32) {
+                    const int f = e & 3;
+                    send8(&rmaxm[rstep & 1][me][f], f == 0 ? rmx : own[f + 1], &bars[rb], e >> 2);
                 }
-                send8(&rmaxm[rstep & 1][me][f], v, &bars[rb], tid >> 2);
             }
             mark(4);
             if (tid == 0) expect_bytes(&bars[rb], static_cast<uint32_t>(G * kBkMsg * 8));
             wait_parity(&bars[rb], (rstep >> 1) & 1);
             mark(5);
-            double v = (tid & 31) < G ? rmaxm[rstep & 1][tid & 31][0] : 0.0;
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
-            const double rowmax = fmax(v, 0.0);
+            const double rowmax =
+                key_mag(warp_key_max((tid & 31) < G ? mag_key(rmaxm[rstep & 1][tid & 31][0]) : 0ull), 0.0);
             cimax = rmaxm[rstep & 1][oi][1];
             cik = rmaxm[rstep & 1][owner(k)][2];
             cik1 = k + 1 < n ? rmaxm[rstep & 1][owner(k + 1)][3] : 0.0;
@@ -884,6 +912,7 @@ __global__ void __launch_bounds__(kBkThreads, 2) bk_update_tc_kernel(const BkArg
     extern __shared__ __align__(16) double usm[];
     double* Ws = usm;                      // [kBkUpdK][kBkUpdLd]  W(i0 + r, t)
     double* Ls = usm + kBkUpdK * kBkUpdLd;  // [kBkUpdK][kLdL]      L(j0 + c, t)
+    pdl_enter();
     const int64_t n = a.n;
     const int64_t k0 = a.ctl[2];
     const int jp = a.ctl[3];
@@ -1564,8 +1593,26 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
     // 256 threads even when a CTA owns 2 rows per thread (n = 6500): 512 was
     // measured 2% slower there (16-warp reductions and barriers)
     auto panel_fn = trace ? bk_panel_smem_kernel<kBkThreads, true> : bk_panel_smem_kernel<kBkThreads, false>;
+    // panels and trailing updates alternate as programmatic dependent launches:
+    // each kernel is launched while its predecessor runs and waits for it on
+    // the device (griddepcontrol.wait), so launch latency leaves the chain
+    static const char* pdl_env = dev_env("R1_BK_PDL");  // development: 0 = plain stream order
+    const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
+    cudaLaunchAttribute pattr[2];
+    pattr[0] = attr[0];
+    pattr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pattr[1].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t pcfg = cfg;
     pcfg.dynamicSmemBytes = psmem;
+    pcfg.attrs = pattr;
+    pcfg.numAttrs = pdl ? 2 : 1;
+    cudaLaunchConfig_t ucfg{};
+    ucfg.gridDim = dim3(2 * ctx->num_sms);
+    ucfg.blockDim = dim3(kBkThreads);
+    ucfg.dynamicSmemBytes = kBkUpdTcSmem;
+    ucfg.stream = ctx->stream;
+    ucfg.attrs = pattr + 1;
+    ucfg.numAttrs = pdl ? 1 : 0;
     // each panel factors >= kBkNb columns (or the rest); extra launches exit at once
     const int64_t panels = (n + kBkNb - 1) / kBkNb;
     for (int64_t p = 0; p < panels; ++p) {
@@ -1574,7 +1621,7 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         else
             R1_CUDA(cudaLaunchKernelEx(&cfg, bk_panel_kernel, a));
         check_launch(ctx, "bk_panel_kernel");
-        bk_update_tc_kernel<<<2 * ctx->num_sms, kBkThreads, kBkUpdTcSmem, ctx->stream>>>(a);
+        R1_CUDA(cudaLaunchKernelEx(&ucfg, bk_update_tc_kernel, a));
         check_launch(ctx, "bk_update_tc_kernel");
     }
     bk_condition_kernel<<<1, 1024, 0, ctx->stream>>>(A, n, L.ctl, L.ps, cond_dev);
@@ -1685,6 +1732,39 @@ int r1x_ldlt(r1_context* ctx, int64_t n, const double* s_host, int* ipiv, double
             }
         }
         *singular = ctl[1];
+    });
+}
+
+// Diagnostics: upload S once, then time `reps` factorisations of fresh copies
+// with CUDA events on the context's stream (the device-to-device restore is
+// outside the timed region); ms[r] = factorisation r.
+int r1x_ldlt_time(r1_context* ctx, int64_t n, const double* s_host, int reps, double* ms) {
+    return abi_guard([&] {
+        CtxLock lk_(ctx);
+        if (!ctx || reps < 1) fail(R1_ERR_INVALID_ARGUMENT, "r1x_ldlt_time: bad arguments");
+        R1_CUDA(cudaSetDevice(ctx->device));
+        const size_t bytes = static_cast<size_t>(n) * n * sizeof(double);
+        DeviceBuffer S, A, ws, c;
+        S.ensure(bytes);
+        A.ensure(bytes);
+        ws.ensure(bk_workspace_bytes(n, ctx->num_sms));
+        c.ensure(64);
+        R1_CUDA(cudaMemcpyAsync(S.ptr, s_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        cudaEvent_t e0, e1;
+        R1_CUDA(cudaEventCreate(&e0));
+        R1_CUDA(cudaEventCreate(&e1));
+        for (int r = 0; r < reps; ++r) {
+            R1_CUDA(cudaMemcpyAsync(A.ptr, S.ptr, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+            R1_CUDA(cudaEventRecord(e0, ctx->stream));
+            bk_factor(ctx, n, A.as<double>(), ws.ptr, c.as<double>());
+            R1_CUDA(cudaEventRecord(e1, ctx->stream));
+            R1_CUDA(cudaEventSynchronize(e1));
+            float t = 0.0f;
+            R1_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            ms[r] = t;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
     });
 }
 

@@ -1,0 +1,7 @@
+#!/bin/bash
+# BK panel change check: output hashes (compare with the previous build's) and device time
+mkdir -p gpurun_out
+python tools/bk_hash_probe.py
+python tools/bk_time_probe.py 600 1500 3000 6500
+if [ -n "$BK_TRACE" ]; then R1_LIB_PATH=$PWD/paper_2403_01778_b200/librank1_b200_dev.so R1_BK_TRACE=1 REPS=1 python tools/bk_time_probe.py 600 3000 6500 2>&1; fi
+if [ -n "$BK_TESTS" ]; then timeout 900 python -m pytest tests/test_bk_gpu.py -q -x 2>&1 | tail -2; fi
