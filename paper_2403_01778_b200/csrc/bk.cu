@@ -59,7 +59,8 @@ struct BkArgs {
     double* red;  // 4 * gridDim partials
     int* perm;    // panel start columns (ctl[4] of them), for the panel-wise solve
     char* ps;     // 0: 1x1 pivot, 1 / 2: first / second column of a 2x2 pivot
-    unsigned long long* trace;  // diagnostics: per-phase globaltimer sums (CTA 0), or null
+    unsigned long long* trace;  // diagnostics: per-phase cycle sums of CTA trace_cta, or null
+    int trace_cta;
 };
 
 // Workspace layout (bytes from bk_workspace_bytes).
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
     auto raw = [&](int pair, int slot) { return Raw + (2 * pair + slot) * rcap; };
     // diagnostics (R1_BK_TRACE): per-phase cycles of CTA 0 thread 0, kept in
     // registers (constant indices after inlining) and written once at the end
-    const bool tr = TRACE && a.trace && me == 0 && tid == 0;
+    const bool tr = TRACE && a.trace && me == min(a.trace_cta, G - 1) && tid == 0;
     long long tprev = 0;
     unsigned long long tacc[16] = {};
     auto mark = [&](int ph) {
@@ -701,22 +702,11 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         const double* rkk = raw(cp, kks);
         const double* w_kk = nx + kks * kBkW;  // W row kk (NEXT of the previous step)
         mark(10);
-        // ---- pivot coefficients (every CTA), new W column(s), pending W rows
-        double d = 0.0, r1 = 0.0, d11 = 0.0, d22 = 0.0, d21t = 0.0;
-        bool zero = false;
+        // ---- NEXT (W needs no division: the pivot coefficients come after
+        // it), pivot coefficients (every CTA), new W column(s), pending W rows
         const bool same = kp == k + 1;
-        if (kstep == 1) {
-            d = kp == k ? ckk : cimax;
-            zero = d == 0.0;
-            r1 = zero ? 0.0 : 1.0 / d;
-        } else {
-            const double d21 = same ? ckk1 : ckimax;
-            d11 = cimax / d21;
-            d22 = ckk / d21;
-            const double tt = 1.0 / (d11 * d22 - 1.0);
-            d21t = tt / d21;
-        }
-        mark(12);
+        const double d = kstep == 1 ? (kp == k ? ckk : cimax) : 0.0;
+        const bool zero = kstep == 1 && d == 0.0;
         auto new_w = [&](int r, int i, double& x0, double& x1) {
             if (kstep == 1) {
                 const double v = kp == k ? Cs[r] : (i == k ? cimax : (i == kp ? cik : Cis[r]));
@@ -742,11 +732,12 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
                     const double* old = swap && q == kp ? w_kk : Ws + (q - lo) * kBkW;
                     double x0, x1;
                     new_w(q - lo, q, x0, x1);
-                    for (int e = tid; e < G * jn; e += NT) {
-                        const int dst = e / jn, t = e - dst * jn;
-                        const double v = t < jp ? old[t] : (t == jp ? x0 : x1);
-                        send8(&nextm[b][s * kBkW + t], v, &bars[4 + b], dst);
-                    }
+                    // warp w -> CTAs w, w + NT/32, ...; lane -> entries lane, lane + 32
+                    for (int dst = tid >> 5; dst < G; dst += NT / 32)
+                        for (int t = tid & 31; t < jn; t += 32) {
+                            const double v = t < jp ? old[t] : (t == jp ? x0 : x1);
+                            send8(&nextm[b][s * kBkW + t], v, &bars[4 + b], dst);
+                        }
                 }
                 if (swap && q <= kp) {
                     if (okp == me) next_bytes += 8u;
@@ -756,6 +747,18 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
                 }
             }
         }
+        mark(6);
+        double r1 = 0.0, d11 = 0.0, d22 = 0.0, d21t = 0.0;
+        if (kstep == 1) {
+            r1 = zero ? 0.0 : 1.0 / d;
+        } else {
+            const double d21 = same ? ckk1 : ckimax;
+            d11 = cimax / d21;
+            d22 = ckk / d21;
+            const double tt = 1.0 / (d11 * d22 - 1.0);
+            d21t = tt / d21;
+        }
+        mark(12);
         if (swap) {
             if (kk >= lo && kk < hi && tid < jp) pend[0][tid] = Wim[tid];
             if (kp >= lo && kp < hi && tid < jp) pend[1][tid] = w_kk[tid];
@@ -793,7 +796,6 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         mark(13);
         __syncthreads();
         mark(14);
-        mark(6);
         // prefetch the raw columns kn, kn+1 (patched at the top of the next
         // step), issued after NEXT so they stream during the stores
         if (more) {
@@ -809,12 +811,16 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         // ---- global stores (stream out behind NEXT): L / D of the new
         // column(s), interchange moves, interchanged rows of earlier L columns
         if (swap) {
-            for (int e = gtid; e < 2 * jp; e += G * NT) {
+            // interchanged rows of the earlier L columns: by the CTAs after
+            // CTA 0 (which sends NEXT and owns the panel's first rows)
+            const int ns = G > 1 ? G - 1 : 1, sg = G > 1 ? me - 1 : 0;
+            for (int e = sg >= 0 ? sg + ns * tid : 2 * jp; e < 2 * jp; e += ns * NT) {
                 const int t = e >> 1;
                 if (e & 1) col(k0 + t)[kp] = l_entry(w_kk, coef, t);
                 else col(k0 + t)[kk] = l_entry(Wim, coef, t);
             }
         }
+        mark(15);
         double* ck = col(k);
         double* ck1 = col(k + 1 < n ? k + 1 : k);
         double* ckp = col(kp);
@@ -1561,7 +1567,9 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         R1_CUDA(cudaMemsetAsync(tbuf.ptr, 0, 16 * sizeof(unsigned long long), ctx->stream));
     }
     BkArgs a{n, A, L.Wp, L.ipiv, L.ctl, L.Ck, L.Ci, L.red, L.perm, L.ps,
-             trace ? tbuf.as<unsigned long long>() : nullptr};
+             trace ? tbuf.as<unsigned long long>() : nullptr,
+             0};
+    if (const char* tenv = dev_env("R1_BK_TRACE")) a.trace_cta = std::max(0, std::atoi(tenv) - 1);
     // the panel grid is one cluster (<= 16 CTAs, non-portable size when the
     // device allows it): enough SMs for the column updates, hardware barriers
     const int gp = panel_cluster_size(ctx, n);
@@ -1634,10 +1642,10 @@ void bk_factor(r1_context* ctx, int64_t n, double* A, void* ws, double* cond_dev
         std::fprintf(stderr,
                      "[r1 bk] n=%lld cols=%llu imax-path=%llu cycles/col: wait_next %.0f top %.0f step1 %.0f "
                      "wait_cand %.0f imax %.0f wait_rmax %.0f elim %.0f (decide %.0f prefetch %.0f coef %.0f "
-                     "neww %.0f bar %.0f sends %.0f) stores %.0f\n",
+                     "neww %.0f bar %.0f sends %.0f) swapL %.0f stores %.0f\n",
                      static_cast<long long>(n), h[9], h[8], h[0] / c, h[1] / c, h[2] / c, h[3] / c,
                      h[4] / c, h[5] / c, (h[10] + h[11] + h[12] + h[13] + h[14] + h[6]) / c, h[10] / c,
-                     h[11] / c, h[12] / c, h[13] / c, h[14] / c, h[6] / c, h[7] / c);
+                     h[11] / c, h[12] / c, h[13] / c, h[14] / c, h[6] / c, h[15] / c, h[7] / c);
     }
 }
 
