@@ -413,6 +413,24 @@ __device__ __forceinline__ unsigned long long warp_key_max(unsigned long long ke
     return (static_cast<unsigned long long>(mh) << 32) | ml;
 }
 
+// Updated entry of one row: s0 - W(row, 0:jp) . Lr in the fixed order (groups
+// of four into s0..s3, the tail into s0).  Rolled loops: the panel kernel's
+// code stays small (a step runs through most of it once).
+__device__ __forceinline__ double row_update(const double* w, const double* Lr, int jp, double s0) {
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int t = 0;
+#pragma unroll 1
+    for (; t + 4 <= jp; t += 4) {
+        s0 -= w[t] * Lr[t];
+        s1 -= w[t + 1] * Lr[t + 1];
+        s2 -= w[t + 2] * Lr[t + 2];
+        s3 -= w[t + 3] * Lr[t + 3];
+    }
+#pragma unroll 1
+    for (; t < jp; ++t) s0 -= w[t] * Lr[t];
+    return (s0 + s1) + (s2 + s3);
+}
+
 // NT threads per CTA; TRACE compiles the phase timers in (their register
 // array doubles the register count).
 template <int NT, bool TRACE>
@@ -486,6 +504,7 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
         const int c = k0 + s;
         if (c >= n) break;
         const double* src = col(c);
+#pragma unroll 1
         for (int r = first_row(c); r < R; r += NT) cp_async8(raw(0, s) + r, src + lo + r);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -534,17 +553,7 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
             const double* rk = raw(cp, 0);
             for (int r = first_row(k); r < R; r += NT) {
                 const int i = lo + r;
-                const double* w = Ws + r * kBkW;
-                double s0 = rk[r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                int t = 0;
-                for (; t + 4 <= jp; t += 4) {
-                    s0 -= w[t] * Lr[t];
-                    s1 -= w[t + 1] * Lr[t + 1];
-                    s2 -= w[t + 2] * Lr[t + 2];
-                    s3 -= w[t + 3] * Lr[t + 3];
-                }
-                for (; t < jp; ++t) s0 -= w[t] * Lr[t];
-                const double sacc = (s0 + s1) + (s2 + s3);
+                const double sacc = row_update(Ws + r * kBkW, Lr, jp, rk[r]);
                 Cs[r] = sacc;
                 if (i > k && (fabs(sacc) > bv || (fabs(sacc) == bv && i < bi))) {
                     bv = fabs(sacc);
@@ -637,22 +646,13 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
             }
             __syncthreads();
             double rv = -1.0;
-#pragma unroll
+#pragma unroll 1
             for (int q = 0; q < kBkMaxRowsPerThread; ++q) {
                 const int r = rfirst + q * NT;
                 if (r >= R) break;
                 const int i = lo + r;
-                const double* w = Ws + r * kBkW;
-                double s0 = araw[q], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                int t = 0;
-                for (; t + 4 <= jp; t += 4) {
-                    s0 -= w[t] * Lr[t];
-                    s1 -= w[t + 1] * Lr[t + 1];
-                    s2 -= w[t + 2] * Lr[t + 2];
-                    s3 -= w[t + 3] * Lr[t + 3];
-                }
-                for (; t < jp; ++t) s0 -= w[t] * Lr[t];
-                const double sacc = (s0 + s1) + (s2 + s3);
+                const double a0 = q == 0 ? araw[0] : (q == 1 ? araw[1] : araw[2]);
+                const double sacc = row_update(Ws + r * kBkW, Lr, jp, a0);
                 Cis[r] = sacc;
                 if (i != imax) rv = fmax(rv, fabs(sacc));
                 if (i == imax) own[2] = sacc;
@@ -803,6 +803,7 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
                 const int c = kn + s;
                 if (c >= n) break;
                 const double* src = col(c);
+#pragma unroll 1
                 for (int r = first_row(c); r < R; r += NT) cp_async8(raw(cp ^ 1, s) + r, src + lo + r);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
@@ -877,6 +878,7 @@ __global__ void __launch_bounds__(NT) bk_panel_smem_kernel(const BkArgs a, int r
     __syncthreads();
     // the panel's W rows of this CTA -> global, for the trailing update
     for (int t = 0; t < jp; ++t)
+#pragma unroll 1
         for (int r = tid; r < R; r += NT) a.Wp[(lo + r) + static_cast<size_t>(t) * n] = Ws[r * kBkW + t];
     if (tr)
         for (int q = 0; q < 16; ++q) a.trace[q] += tacc[q];
