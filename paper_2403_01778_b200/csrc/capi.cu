@@ -152,6 +152,8 @@ int r1_context_create(int device, r1_context** out) {
         ctx->smem_optin = prop.sharedMemPerBlockOptin;
         R1_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
+        R1_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->ev_sweep) R1_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *out = ctx;
     });
 }
@@ -168,6 +170,12 @@ int r1_context_destroy(r1_context* ctx) {
         ctx->plans.clear();
         if (ctx->comm) ctx->comm->ctx = nullptr;  // the communicator outlives its context
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        if (ctx->side_stream) {
+            cudaStreamSynchronize(ctx->side_stream);
+            cudaStreamDestroy(ctx->side_stream);
+        }
+        for (auto e : ctx->ev_sweep)
+            if (e) cudaEventDestroy(e);
         delete ctx;
     });
 }

@@ -220,6 +220,10 @@ struct r1_context {
     size_t smem_optin = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    // second lane of a sweep (sweep.cu): independent subtrees of the recursion
+    // and the B01 second stage run beside the main stream, joined by events
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t ev_sweep[3] = {nullptr, nullptr, nullptr};  // root box done, root C1 done, side joined
     uint64_t launches = 0;
     unsigned long long* dbg_sweep_trace = nullptr;  // diagnostics: per-CTA timing of level 0
     // diagnostics: CUDA events around every top-level sweep kernel launch

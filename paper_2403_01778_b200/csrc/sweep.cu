@@ -47,6 +47,7 @@ constexpr int kThreads = (kNWC + 1) * 32;  // + one producer warp
 constexpr int kMaxOrder = 16;
 constexpr int kBoxNWC = 15;  // consumer warps of the TMA box kernel (+1 producer = 16 warps)
 constexpr int kBoxNCB = 4;   // columns per consumer warp (box = 32*NRA x 60)
+constexpr int kWideDefault = 13;  // wide consumer shapes for all three row-tile heights (tile_level)
 constexpr int kMaxStages = 16;          // mbarrier slots of the box kernel ring
 constexpr double kDynFrac = 0.25;       // share of the work scheduled dynamically
 constexpr double kDynMinChunk = 8.0;    // guided chunks: remaining/(2*ncta), >= 8 panels
@@ -533,13 +534,15 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
         const int q = pc - 1, slot = q & 1;
         if (warp * 32 < pend_r0e) {
             mbar_wait(&red_full[slot], (q >> 1) & 1);
-            const int i = threadIdx.x;
-            if (i < pend_r0e) {
-                const double* rr = red + slot * NWC * RMAX + i;
-                double sum = 0.0;
 #pragma unroll
-                for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX];
-                pend_dst[i] = sum;
+            for (int i = threadIdx.x; i < RMAX; i += NWC * 32) {
+                if (i < pend_r0e) {
+                    const double* rr = red + slot * NWC * RMAX + i;
+                    double sum = 0.0;
+#pragma unroll
+                    for (int w = 0; w < NWC; ++w) sum += rr[w * RMAX];
+                    pend_dst[i] = sum;
+                }
             }
         }
         __syncwarp();
@@ -665,7 +668,6 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             }
 
             {
-                static_assert(NRA <= NWC, "one C0 row per consumer thread");
                 const int slot = pc & 1;
                 mbar_wait(&red_empty[slot], ((pc >> 1) & 1) ^ 1);
                 double2* rb =
@@ -1018,7 +1020,15 @@ __global__ void __launch_bounds__(kB01Warps * 32) finish_b01_seg_kernel(const Fi
 #pragma unroll
             for (int q = 0; q < 8; ++q) s += v[q];
         }
-        for (; k < k1; ++k) s += valid ? __ldcs(src + k * tile_elems) : 0.0;
+        if (k < k1) {  // the rest as one predicated batch (loads in flight together)
+            const int r = k1 - k;
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = (valid && q < r) ? __ldcs(src + (k + q) * tile_elems) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < r) s += v[q];
+        }
         red[warp][lane] = s;
         __syncthreads();
         if (warp == 0 && valid) {
@@ -1086,6 +1096,7 @@ struct Level {
     // outputs
     Ref out_b01, out_c0, out_c1;
     Ref w, p01, p0, p1;
+    int lane = 0;  // 1: in the root's C1 subtree (runs on the side stream)
 };
 
 }  // namespace
@@ -1163,6 +1174,30 @@ void tile_level(Level& L, int num_sms) {
             L.nra = 8;
             L.ncb = 2;
         }
+        // Wide shapes (round 2): 32 elements per consumer thread instead of 16,
+        // on fewer warps — the per-panel fixed work (barrier waits, the C1
+        // butterfly, the C0 block reduction) is paid per 32 elements: 3.8
+        // instead of 5.5 static instructions per DFMA in the 128-row loop.
+        // Same-box A/B: C5 5.44-5.55 -> 5.31 ms (sustained 600 sweeps under the
+        // power cap 5.72 -> 5.39), C2 1.39 -> 1.35, C4 1.14 -> 1.12 and C3 2.50 ->
+        // 2.22 ms (11 warps x 4 columns also cut its column tiles from 7 to 5).
+        // Measured and left out: 7 warps x 4 columns for the 256-row tiles (C3
+        // 2.56 ms) and 11 warps x 8 columns for the 128-row ones (C5 5.45 ms:
+        // 168-register cap, two 86-KB stages).  R1_SWEEP_WIDE=0 (development
+        // build) restores the 15-warp shapes; bits 1 / 4 / 8 select the 128- /
+        // 64- / 256-row shapes.
+        static const char* wide_env = dev_env("R1_SWEEP_WIDE");
+        const int wide = wide_env ? std::atoi(wide_env) : kWideDefault;
+        if ((wide & 1) && L.nra == 4) {
+            L.nwc = 7;  // 128 x 56
+            L.ncb = 8;
+        } else if ((wide & 8) && L.nra == 8) {
+            L.nwc = 11;  // 256 x 44
+            L.ncb = 4;
+        } else if ((wide & 4) && L.nra == 2) {
+            L.nwc = 8;  // 64 x 64
+            L.ncb = 8;
+        }
         const int rm = 32 * L.nra, cm = L.nwc * L.ncb;
         L.G0 = static_cast<int>((L.MI0 + rm - 1) / rm);
         L.r0 = static_cast<int>((L.MI0 + L.G0 - 1) / L.G0);
@@ -1187,7 +1222,8 @@ void tile_level(Level& L, int num_sms) {
         // reductions (C4: 60 x 60 faces)
         L.KO = 1;
         static const char* ko_env = dev_env("R1_SWEEP_KO");
-        const int ko_max = ko_env ? std::atoi(ko_env) : 2;  // measured: 2 beats 4 on C4
+        int ko_max = ko_env ? std::atoi(ko_env) : 2;  // measured: 2 beats 4 on C4
+        if (L.nwc == 8) ko_max = std::min(ko_max, 2);   // the 64 x 64 shape has KO <= 2
         if (L.ntiles == 1 && L.r0 * L.t1 <= 64 * 64 && L.nra == 2)
             for (int ko = ko_max; ko > 1; ko >>= 1)
                 if (L.O % ko == 0) {
@@ -1331,8 +1367,10 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
 // Recursively lay out the levels for a sub-problem of order `order` (>= 3).
 // need_all: also produce the blocks among modes >= 2 of this sub-problem.
 void plan_rec(SweepPlan& P, const uint64_t* full_dims, int full_order, int order,
-              const int64_t* dims, const int* modes, Ref input, bool need_all, int num_sms) {
+              const int64_t* dims, const int* modes, Ref input, bool need_all, int num_sms,
+              int lane = 0) {
     Level L;
+    L.lane = lane;
     L.order = order;
     for (int k = 0; k < order; ++k) {
         L.dims[k] = dims[k];
@@ -1384,11 +1422,14 @@ void plan_rec(SweepPlan& P, const uint64_t* full_dims, int full_order, int order
             m0[k - 1] = modes[k];
         }
         const Ref c0 = L.out_c0, c1 = L.out_c1;
-        plan_rec(P, full_dims, full_order, order - 1, d0, m0, c0, need_all, num_sms);
+        plan_rec(P, full_dims, full_order, order - 1, d0, m0, c0, need_all, num_sms, lane);
         if (need_c1) {
             d0[0] = dims[1];
             m0[0] = modes[1];
-            plan_rec(P, full_dims, full_order, order - 1, d0, m0, c1, false, num_sms);
+            // the root's C1 subtree shares nothing with its C0 subtree (disjoint
+            // work regions, disjoint final blocks): second lane
+            plan_rec(P, full_dims, full_order, order - 1, d0, m0, c1, false, num_sms,
+                     order == full_order ? 1 : lane);
         }
     }
 }
@@ -1499,9 +1540,17 @@ void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
     if (L.tma) {
         static const char* sr = dev_env("R1_SWEEP_STAGE_REGS");
         const bool stage_regs = sr ? std::atoi(sr) != 0 : true;
-        if (L.nra == 8) {
+        if (L.nra == 8 && L.nwc == 11) {
+            launch_box<8, false, 1, 4, 11>(ctx, L, a);
+        } else if (L.nra == 2 && L.nwc == 8) {
+            if (L.KO == 2) launch_box<2, false, 2, 8, 8>(ctx, L, a);
+            else launch_box<2, false, 1, 8, 8>(ctx, L, a);
+        } else if (L.nra == 8) {
             if (stage_regs) launch_box<8, true, 1, 2>(ctx, L, a);
             else launch_box<8, false, 1, 2>(ctx, L, a);
+        } else if (L.nra == 4 && L.nwc == 7) {
+            if (stage_regs) launch_box<4, true, 1, 8, 7>(ctx, L, a);
+            else launch_box<4, false, 1, 8, 7>(ctx, L, a);
         } else if (L.nra == 4) {
             if (stage_regs) launch_box<4, true, 1>(ctx, L, a);
             else launch_box<4, false, 1>(ctx, L, a);
@@ -1562,8 +1611,34 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
     };
 
     R1_CUDA(cudaMemsetAsync(P->counters.ptr, 0, P->levels.size() * 64, ctx->stream));
+    // Two lanes.  The children of the root need only its C0 / C1, not B01, and
+    // its two subtrees are independent: the root's B01 second stage and its C1
+    // subtree run on the side stream beside the C0 / C1 second stage and the C0
+    // subtree (C4: 18 small kernels of ~190 us in a chain become two chains of
+    // ~70 us).  Forked after the root's box kernel, joined at the end — inside
+    // a stream capture the side stream joins the capture the same way.
+    static const char* fork_env = dev_env("R1_SWEEP_FORK");
+    const int fork_mode = fork_env ? std::atoi(fork_env) : 1;  // 0 never, 1 large tensors, 2 always
+    const Level& root = P->levels.front();
+    const bool root_seg = root.nseg >= 64 * root.ntiles;
+    const bool fork = ctx->side_stream && fork_mode != 0 && (fork_mode == 2 || n >= (uint64_t(1) << 22)) &&
+                      (P->levels.size() > 1 && (root_seg || P->levels.back().lane == 1));
+    cudaStream_t const main_stream = ctx->stream;
+    struct StreamGuard {
+        r1_context* c;
+        cudaStream_t s;
+        ~StreamGuard() { c->stream = s; }
+    } guard{ctx, main_stream};
+    bool side_used = false, side_has_c1 = false;
     int level_idx = 0;
     for (const Level& L : P->levels) {
+        const bool on_side = fork && L.lane == 1;
+        if (on_side && !side_has_c1) {
+            R1_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sweep[1], 0));
+            side_has_c1 = side_used = true;
+        }
+        ctx->stream = on_side ? ctx->side_stream : main_stream;
+        const bool is_root = &L == &root;
         // outer weights
         OuterArgs oa{};
         oa.nout = L.order - 2;
@@ -1653,15 +1728,29 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         fastdiv_init(L.I1, f.m_I1, f.s_I1);
         fastdiv_init(L.r0, f.m_r0, f.s_r0);
         fastdiv_init(L.t1, f.m_t1, f.s_t1);
+        // the root's children wait for its C0 / C1 only (event 1, recorded below)
+        auto root_outputs_done = [&]() {
+            if (is_root && fork) R1_CUDA(cudaEventRecord(ctx->ev_sweep[1], main_stream));
+        };
         if (L.nseg >= 64 * L.ntiles) {
             // many segments per tile: B01 by segment slices, C0/C1 (if any) below
             const int64_t units = static_cast<int64_t>(L.ntiles) * ((static_cast<int64_t>(L.r0) * L.t1 + 31) / 32);
             const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(4) * ctx->num_sms)));
-            finish_b01_seg_kernel<<<grid, kB01Warps * 32, 0, ctx->stream>>>(f);
+            cudaStream_t bs = ctx->stream;
+            if (is_root && fork) {
+                R1_CUDA(cudaEventRecord(ctx->ev_sweep[0], main_stream));
+                R1_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sweep[0], 0));
+                bs = ctx->side_stream;
+                side_used = true;
+            }
+            finish_b01_seg_kernel<<<grid, kB01Warps * 32, 0, bs>>>(f);
             check_launch(ctx, "finish_b01_seg_kernel");
             f.b01 = nullptr;
             f.n_b01 = 0;
-            if (f.n_c0 + f.n_c1 == 0) continue;
+            if (f.n_c0 + f.n_c1 == 0) {
+                root_outputs_done();
+                continue;
+            }
         }
         {
             const int64_t total = f.n_b01 + f.n_c0 + f.n_c1;
@@ -1675,6 +1764,12 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
                 finish_kernel<int64_t><<<grid, 256, 0, ctx->stream>>>(f);
         }
         check_launch(ctx, "finish_kernel");
+        root_outputs_done();
+    }
+    ctx->stream = main_stream;
+    if (side_used) {
+        R1_CUDA(cudaEventRecord(ctx->ev_sweep[2], ctx->side_stream));
+        R1_CUDA(cudaStreamWaitEvent(main_stream, ctx->ev_sweep[2], 0));
     }
 }
 
