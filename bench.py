@@ -91,7 +91,7 @@ def fp64_peak():
 def profile_traffic():
     """DRAM read+write bytes of one C5 sweep (all its kernels) from the
     committed ncu --set full capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "r02_sweep_c5_ncu_summary.json")
+    p = os.path.join(ROOT, "profiles", "r02_sweep_c5_wide_ncu_summary.json")
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
@@ -453,7 +453,7 @@ def run_b200(args):
                 "algorithmic_bytes_per_sweep": sweep_bytes(ldims),
                 "sweep_ms": round(sweep_ms, 6),
                 "traffic": traffic,
-                "traffic_source": "profiles/r02_sweep_c5_ncu_summary.json (ncu --set full, "
+                "traffic_source": "profiles/r02_sweep_c5_wide_ncu_summary.json (ncu --set full, "
                                   "dram__bytes_read.sum + dram__bytes_write.sum over the "
                                   "sweep's kernels)" if traffic else None,
                 "level0_kernel": {
