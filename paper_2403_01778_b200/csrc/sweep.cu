@@ -122,6 +122,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
+// Programmatic dependent launch: every sweep kernel lets its successor in the
+// stream be scheduled at once and waits for its predecessor (completion and
+// memory flush) before touching global memory, so launch latency and the
+// prologue (smem zeroing, barrier init, tensor-map prefetch) leave the chain.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -196,6 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kNWC * RMAX);
     uint64_t* empty = full + STAGES;
 
+    pdl_launch_dependents();
+    pdl_wait();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -425,6 +436,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     uint64_t* red_full = reinterpret_cast<uint64_t*>(meta + kMaxStages);  // [2] C0 partial slots
     uint64_t* red_empty = red_full + 2;
 
+    pdl_launch_dependents();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // A lane's NRA rows are NP 16-B pairs at byte offset 16*NP*lane.  NP = 2:
@@ -447,6 +459,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    pdl_wait();
 
     const int seg_begin = p.cta_seg[blockIdx.x];
     const int seg_end = p.cta_seg[blockIdx.x + 1];
@@ -496,7 +509,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             if (p.ndyn > 0) {
                 for (;;) {
                     const int c = atomicAdd(p.dyn_counter, 1);
-                    if (c >= p.ndyn) break;
+                    if (c >= p.ndyn) {
+                        // every CTA ends with exactly one failing fetch: the one
+                        // that draws the last ticket re-arms the counter for
+                        // the next sweep (no memset node per sweep)
+                        if (c == p.ndyn + static_cast<int>(gridDim.x) - 1) *p.dyn_counter = 0;
+                        break;
+                    }
                     run_segment(p.dyn_first + c);
                 }
             }
@@ -930,6 +949,8 @@ __device__ __forceinline__ IDX fdiv(IDX x, int64_t d, uint64_t m, int sh) {
 
 template <typename IDX>
 __global__ void finish_kernel(const FinishArgs f) {
+    pdl_launch_dependents();
+    pdl_wait();
     const IDX nb = static_cast<IDX>(f.n_b01), n0 = static_cast<IDX>(f.n_c0);
     const IDX total = nb + n0 + static_cast<IDX>(f.n_c1);
     const IDX I0 = static_cast<IDX>(f.I0), I1 = static_cast<IDX>(f.I1);
@@ -993,6 +1014,8 @@ __global__ void finish_kernel(const FinishArgs f) {
 // combined in warp order through shared memory — one fixed summation order.
 constexpr int kB01Warps = 16;
 __global__ void __launch_bounds__(kB01Warps * 32) finish_b01_seg_kernel(const FinishArgs f) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ double red[kB01Warps][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t tile_elems = static_cast<int64_t>(f.r0) * f.t1;
@@ -1053,6 +1076,8 @@ struct OuterArgs {
 
 // W[o] = u_2[i_2] * u_3[i_3] * ... (first outer mode fastest).
 __global__ void outer_weights_kernel(const OuterArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.O;
          o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int64_t q = o;
@@ -1452,6 +1477,7 @@ std::shared_ptr<SweepPlan> get_plan(r1_context* ctx, const uint64_t* dims, int o
     P->counters.ensure(std::max<size_t>(1, P->levels.size()) * 64);
     R1_CUDA(cudaMemcpy(P->meta.ptr, P->host_meta.data(), P->host_meta.size() * sizeof(int),
                        cudaMemcpyHostToDevice));
+    R1_CUDA(cudaMemsetAsync(P->counters.ptr, 0, std::max<size_t>(1, P->levels.size()) * 64, ctx->stream));
     ctx->plans[key] = P;
     return P;
 }
@@ -1494,6 +1520,27 @@ CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t 
     return m;
 }
 
+// Launch on ctx->stream as a programmatic dependent of the preceding kernel
+// (the kernels call griddepcontrol.wait before touching global memory).
+template <typename... KArgs, typename... Args>
+void launch_pdl(r1_context* ctx, void (*kern)(KArgs...), int grid, int block, size_t smem,
+                cudaStream_t stream, Args&&... args) {
+    static const char* env = dev_env("R1_SWEEP_PDL");  // development: 0 = plain stream order
+    static const bool pdl = !(env && std::atoi(env) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(block));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    R1_CUDA(cudaLaunchKernelEx(&cfg, kern, KArgs(std::forward<Args>(args))...));
+    (void)ctx;
+}
+
 template <int NRA, int NCB, int STAGES, bool TMA>
 void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const CUtensorMap& m) {
     auto kern = sweep3_kernel<NRA, NCB, STAGES, TMA>;
@@ -1502,7 +1549,7 @@ void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const C
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBudget)));
     });
-    kern<<<L.ncta, kThreads, L.smem, ctx->stream>>>(a, m);
+    launch_pdl(ctx, kern, L.ncta, kThreads, L.smem, ctx->stream, a, m);
     check_launch(ctx, "sweep3_kernel");
 }
 
@@ -1527,7 +1574,7 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
         R1_CUDA(cudaEventCreate(&e1));
         R1_CUDA(cudaEventRecord(e0, ctx->stream));
     }
-    kern<<<L.ncta, (NWC + 1) * 32, L.smem, ctx->stream>>>(a, maps, L.stages, L.stage_dbl);
+    launch_pdl(ctx, kern, L.ncta, (NWC + 1) * 32, L.smem, ctx->stream, a, maps, L.stages, L.stage_dbl);
     check_launch(ctx, "sweep3_box_kernel");
     if (timed) {
         R1_CUDA(cudaEventRecord(e1, ctx->stream));
@@ -1610,7 +1657,8 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         }
     };
 
-    R1_CUDA(cudaMemsetAsync(P->counters.ptr, 0, P->levels.size() * 64, ctx->stream));
+    // (the dynamic-tail counters are zeroed at plan creation and re-armed by the
+    // box kernel itself)
     // Two lanes.  The children of the root need only its C0 / C1, not B01, and
     // its two subtrees are independent: the root's B01 second stage and its C1
     // subtree run on the side stream beside the C0 / C1 second stage and the C0
@@ -1652,7 +1700,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         if (oa.nout == 1) {
             Wsrc = oa.u[0];  // order 3: the outer weights are u_2 itself
         } else {
-            outer_weights_kernel<<<grid_for(L.O, 256, ctx->num_sms), 256, 0, ctx->stream>>>(oa);
+            launch_pdl(ctx, outer_weights_kernel, grid_for(L.O, 256, ctx->num_sms), 256, 0, ctx->stream, oa);
             check_launch(ctx, "outer_weights_kernel");
         }
 
@@ -1743,7 +1791,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
                 bs = ctx->side_stream;
                 side_used = true;
             }
-            finish_b01_seg_kernel<<<grid, kB01Warps * 32, 0, bs>>>(f);
+            launch_pdl(ctx, finish_b01_seg_kernel, grid, kB01Warps * 32, 0, bs, f);
             check_launch(ctx, "finish_b01_seg_kernel");
             f.b01 = nullptr;
             f.n_b01 = 0;
@@ -1759,9 +1807,9 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
             // 32-bit indices only while the grid-stride loop cannot step past
             // 2^31 (e + gridDim.x * 256 must stay representable)
             if (total + static_cast<int64_t>(grid) * 256 < (int64_t(1) << 31))
-                finish_kernel<int><<<grid, 256, 0, ctx->stream>>>(f);
+                launch_pdl(ctx, finish_kernel<int>, grid, 256, 0, ctx->stream, f);
             else
-                finish_kernel<int64_t><<<grid, 256, 0, ctx->stream>>>(f);
+                launch_pdl(ctx, finish_kernel<int64_t>, grid, 256, 0, ctx->stream, f);
         }
         check_launch(ctx, "finish_kernel");
         root_outputs_done();
