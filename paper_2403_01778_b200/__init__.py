@@ -71,11 +71,11 @@ class Context:
         return int(v.value)
 
     def sweep_plan_info(self, dims) -> dict:
-        info = (ctypes.c_int64 * 13)()
+        info = (ctypes.c_int64 * 16)()
         d = dims_arr(dims)
         check(lib().r1x_sweep_plan_info(self.handle, u64p(d), len(dims), info))
         keys = ["r0", "t1", "G0", "G1", "ncta", "nseg", "levels", "work_elems", "smem", "nra", "K", "KO",
-                "ndyn"]
+                "ndyn", "ns", "ts"]
         return dict(zip(keys, [int(v) for v in info]))
 
 

@@ -47,6 +47,13 @@ constexpr int kThreads = (kNWC + 1) * 32;  // + one producer warp
 constexpr int kMaxOrder = 16;
 constexpr int kBoxNWC = 15;  // consumer warps of the TMA box kernel (+1 producer = 16 warps)
 constexpr int kBoxNCB = 4;   // columns per consumer warp (box = 32*NRA x 60)
+// sub-strips per tile of the 128 x 56 shape, accumulators in tensor memory
+// (R1_SWEEP_NS in the development build).  Built, bit-correct and measured
+// SLOWER (same box, C5 5.59 vs 5.17 ms, C2 1.43 vs 1.31 ms with 3 sub-strips):
+// every box moves its 57 KB of accumulators out of and back into tensor
+// memory, and tcgen05.ld reads 64 B per clock and SM — a third of the box
+// period — so the 0.77 GB less partial-sum traffic (C5) does not pay.  Off.
+constexpr int kSubStripsDefault = 1;
 constexpr int kWideDefault = 13;  // wide consumer shapes for all three row-tile heights (tile_level)
 constexpr int kMaxStages = 16;          // mbarrier slots of the box kernel ring
 constexpr double kDynFrac = 0.25;       // share of the work scheduled dynamically
@@ -73,6 +80,7 @@ struct SweepArgs {
     const double* u1;
     const double* W;
     int r0, t1, G0;
+    int ts;                 // box kernel: columns per box (sub-strip of a tile; = t1 without sub-strips)
     int rbox;               // TMA path: box rows (= r0, even); smem column stride
     const Seg* segs;
     const int* cta_seg;
@@ -130,6 +138,73 @@ __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Tensor memory as accumulator storage (box kernel with sub-strips): a warp
+// reads / writes 8 doubles (16 32-bit columns) of each of its 32 lanes.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+// completes the loads; the registers pass through it so no use moves above it
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                   "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                   "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// NE doubles of this thread's lane at column taddr.. (NE % 8 == 0)
+template <int NE>
+__device__ __forceinline__ void tmem_issue_load(uint32_t taddr, uint32_t (&r)[NE / 8][16]) {
+#pragma unroll
+    for (int c = 0; c < NE / 8; ++c) tmem_ld8(taddr + 16 * c, r[c]);
+}
+template <int NE>
+__device__ __forceinline__ void tmem_complete_load(uint32_t (&r)[NE / 8][16], double* d) {
+#pragma unroll
+    for (int c = 0; c < NE / 8; ++c) tmem_wait_ld(r[c]);
+#pragma unroll
+    for (int c = 0; c < NE / 8; ++c)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d[8 * c + e] = __hiloint2double(static_cast<int>(r[c][2 * e + 1]), static_cast<int>(r[c][2 * e]));
+}
+template <int NE>
+__device__ __forceinline__ void tmem_load_doubles(uint32_t taddr, double* d) {
+    uint32_t r[NE / 8][16];
+    tmem_issue_load<NE>(taddr, r);
+    tmem_complete_load<NE>(r, d);
+}
+template <int NE>
+__device__ __forceinline__ void tmem_store_doubles(uint32_t taddr, const double* d) {
+#pragma unroll
+    for (int c = 0; c < NE / 8; ++c) {
+        uint32_t r[16];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            r[2 * e] = static_cast<uint32_t>(__double2loint(d[8 * c + e]));
+            r[2 * e + 1] = static_cast<uint32_t>(__double2hiint(d[8 * c + e]));
+        }
+        tmem_st8(taddr + 16 * c, r);
+    }
+}
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
@@ -418,11 +493,20 @@ struct BoxMaps {
 // KO > 1 (small faces): one box holds KO consecutive o-panels of the tile, so
 // the per-panel fixed work (barrier waits, the C0 block reduction, the C1
 // warp reduction) is paid once per KO panels; segments count o-groups.
-template <int NRA, int NCB, int NWC, bool STAGE_REGS, int KO>
+// NS > 1 (sub-strips, round 2): a tile is NS column sub-strips of ts <= NWC * NCB
+// columns, one TMA box each per o; the B01 accumulators of all sub-strips live
+// in TENSOR MEMORY (256 KB per SM, idle otherwise: tcgen05.ld / .st, 32 doubles
+// per thread and sub-strip), loaded before and stored after each box, so a
+// tile is up to NS x larger than the register file allows and the face has NS
+// x fewer column tiles, i.e. C0 partial sets; the C0 row sums of an o are
+// carried in registers over its sub-strips and reduced once.
+template <int NRA, int NCB, int NWC, bool STAGE_REGS, int KO, int NS = 1>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     sweep3_box_kernel(const SweepArgs p, const __grid_constant__ BoxMaps maps, int nst,
                       int stage_dbl) {
     static_assert(KO * NCB <= 32, "C1 reduction holds KO * NCB values per lane");
+    static_assert(NS == 1 || (KO == 1 && NWC <= 8 && NS * 4 * NRA * NCB <= 512 && (NRA * NCB) % 8 == 0),
+                  "sub-strips: two warps per TMEM lane quadrant, 512 columns");
     static_assert(NRA % 2 == 0 && NRA <= 8, "rows are read in pairs, at most 4 pairs per lane");
     constexpr int RMAX = 32 * NRA;
     constexpr int NP = NRA / 2;
@@ -435,6 +519,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     int4* meta = reinterpret_cast<int4*>(empty + kMaxStages);  // per stage {seg, tile, o, flags}
     uint64_t* red_full = reinterpret_cast<uint64_t*>(meta + kMaxStages);  // [2] C0 partial slots
     uint64_t* red_empty = red_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_empty + 2);  // tensor-memory base (NS > 1)
 
     pdl_launch_dependents();
     const int warp = threadIdx.x >> 5;
@@ -458,7 +543,22 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if constexpr (NS > 1) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_addr(tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     __syncthreads();
+    if constexpr (NS > 1) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this thread's accumulator columns: lane quadrant warp % 4, region (warp / 4, sub-strip)
+    const uint32_t tmem_base = NS > 1 ? *tmem_slot : 0u;
+    const uint32_t tmem_acc = NS > 1 ? tmem_base + ((static_cast<uint32_t>(warp & 3) * 32u) << 16) +
+                                           static_cast<uint32_t>(warp >> 2) * (NS * 2 * NRA * NCB)
+                                     : 0u;
     pdl_wait();
 
     const int seg_begin = p.cta_seg[blockIdx.x];
@@ -469,6 +569,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     const int G1 = static_cast<int>((MI1 + p.t1 - 1) / p.t1);
     const int rem0 = static_cast<int>(MI0 - static_cast<int64_t>(p.G0 - 1) * p.r0);
     const int rem1 = static_cast<int>(MI1 - static_cast<int64_t>(G1 - 1) * p.t1);
+    // boxes are ts columns wide (ts = t1 without sub-strips); only the last box
+    // of the last column tile is narrower (remlast)
+    const int remlast = rem1 - ((rem1 + p.ts - 1) / p.ts - 1) * p.ts;
 
     // Schedule (producer-driven): the static segments [seg_begin, seg_end) of
     // this CTA, then chunks of the dynamic tail taken from a work counter by
@@ -489,19 +592,24 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 const Seg sg = p.segs[s];
                 const int g0 = sg.tile % p.G0, g1 = sg.tile / p.G0;
                 const bool er = g0 == p.G0 - 1, ec = g1 == G1 - 1;
-                const uint32_t bytes = static_cast<uint32_t>(er ? rem0 : p.r0) *
-                                       static_cast<uint32_t>(ec ? rem1 : p.t1) * 8u * KO;
-                const CUtensorMap* map = &maps.m[(er ? 1 : 0) | (ec ? 2 : 0)];
+                const int nsub = ((ec ? rem1 : p.t1) + p.ts - 1) / p.ts;  // boxes per o
                 for (int o = sg.o0; o < sg.o1; ++o) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    meta[stage] = make_int4(s, sg.tile, o,
-                                            (o == sg.o0 ? kFirst : 0) | (o == sg.o1 - 1 ? kLast : 0));
-                    mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_3d(ring + stage * stage_dbl, map, g0 * p.r0, g1 * p.t1, o * KO,
-                                &full[stage], pol);
-                    if (++stage == nst) {
-                        stage = 0;
-                        phase ^= 1;
+                    for (int sb = 0; sb < nsub; ++sb) {
+                        const bool ecs = ec && sb == nsub - 1;
+                        const uint32_t bytes = static_cast<uint32_t>(er ? rem0 : p.r0) *
+                                               static_cast<uint32_t>(ecs ? remlast : p.ts) * 8u * KO;
+                        const CUtensorMap* map = &maps.m[(er ? 1 : 0) | (ecs ? 2 : 0)];
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        meta[stage] = make_int4(s, sg.tile, o,
+                                                (o == sg.o0 && sb == 0 ? kFirst : 0) |
+                                                    (o == sg.o1 - 1 && sb == nsub - 1 ? kLast : 0) | (sb << 8));
+                        mbar_arrive_expect_tx(&full[stage], bytes);
+                        tma_load_3d(ring + stage * stage_dbl, map, g0 * p.r0, g1 * p.t1 + sb * p.ts, o * KO,
+                                    &full[stage], pol);
+                        if (++stage == nst) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
                 }
             };
@@ -537,7 +645,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     int64_t R0s = 0, R1s = 0;
     double u0r[NRA], u1c[NCB];
     double acc[NRA][NCB];
+    double c0p[NRA];  // C0 row sums of the current o (carried over its sub-strips)
     int coff[NCB];  // smem offset (double2 units) of the thread's columns
+    bool live = false;
+    int nsub = 1;
+    int last_w = -1;
     double* P0row = nullptr;
     double* P1row = nullptr;
     // KO == 1: the C0 block reduction of panel q (partials in red slot q & 1)
@@ -587,7 +699,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             cls_lo = static_cast<int>(R0s / I0);
             cls_hi = static_cast<int>((R0s + r0e - 1) / I0);
             const int lr = NRA * lane;
-            const bool live = lr < r0e;
+            live = lr < r0e;
             pcls = live ? static_cast<int>((R0s + lr) / I0) : cls_hi;
             const int64_t i0s = R0s + lr - static_cast<int64_t>(pcls) * I0;
 #pragma unroll
@@ -605,6 +717,39 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             }
             P0row = p.P0 + static_cast<int64_t>(g1) * p.P0_stride + R0s;
             P1row = p.P1 ? p.P1 + static_cast<int64_t>(g0) * p.P1_stride + R1s : nullptr;
+            if constexpr (NS > 1) {
+                // zero this thread's accumulators of every sub-strip of the tile
+                nsub = (t1e + p.ts - 1) / p.ts;
+                tmem_wait_st();
+                for (int q = 0; q < nsub; ++q)
+                    tmem_store_doubles<NRA * NCB>(tmem_acc + q * (2 * NRA * NCB), &acc[0][0]);
+            }
+        }
+        // sub-strip of this box: index, first column inside the tile, width
+        const int sb = NS > 1 ? (md.w >> 8) : 0;
+        const int jb = sb * p.ts;
+        const int wsb = NS > 1 ? min(p.ts, t1e - jb) : t1e;
+        if constexpr (NS > 1) {
+            if (md.w & kFirst) last_w = -1;
+#pragma unroll
+            for (int b = 0; b < NCB; ++b) {
+                const int j = warp + NWC * b;
+                u1c[b] = (j < wsb && live) ? __ldg(p.u1 + K * (R1s + jb + j) + pcls) : 0.0;
+            }
+            if (wsb != last_w) {  // only the ragged last box of the last column tile differs
+#pragma unroll
+                for (int b = 0; b < NCB; ++b)
+                    coff[b] = (min(warp + NWC * b, wsb - 1) * cst) / 2 + (NRA / 2) * lane;
+                last_w = wsb;
+            }
+            // (the first box of a segment starts from the zeros set above).
+            // Requesting the next box's accumulators right after this box's
+            // store — the load under the wait for the next stage — measured
+            // slower (248 registers: C5 6.1 vs 5.6 ms).
+            if (!(md.w & kFirst)) {
+                tmem_wait_st();
+                tmem_load_doubles<NRA * NCB>(tmem_acc + sb * (2 * NRA * NCB), &acc[0][0]);
+            }
         }
         {
             if constexpr (KO == 1) {
@@ -619,10 +764,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 }
                 continue;
             }
-            double c0p[NRA];
             double c1v[NCB];
+            if (sb == 0) {
 #pragma unroll
-            for (int a = 0; a < NRA; ++a) c0p[a] = 0.0;
+                for (int a = 0; a < NRA; ++a) c0p[a] = 0.0;
+            }
             auto column = [&](int b, const double2* v) {
                 double c1p = 0.0;
 #pragma unroll
@@ -673,7 +819,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                 if (cls_lo == cls_hi) {
                     const double c1 = warp_transpose_sum<NCB>(c1v, lane, &col);
                     const int j = warp + NWC * col;
-                    if ((lane & (32 / NCB - 1)) == 0 && j < t1e) dst[cls_lo * MI1 + j] = c1;
+                    if ((lane & (32 / NCB - 1)) == 0 && j < wsb) dst[cls_lo * MI1 + jb + j] = c1;
                 } else {
                     for (int c = cls_lo; c <= cls_hi; ++c) {
                         double mv[NCB];
@@ -681,12 +827,14 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
                         for (int b = 0; b < NCB; ++b) mv[b] = pcls == c ? c1v[b] : 0.0;
                         const double c1 = warp_transpose_sum<NCB>(mv, lane, &col);
                         const int j = warp + NWC * col;
-                        if ((lane & (32 / NCB - 1)) == 0 && j < t1e) dst[c * MI1 + j] = c1;
+                        if ((lane & (32 / NCB - 1)) == 0 && j < wsb) dst[c * MI1 + jb + j] = c1;
                     }
                 }
             }
 
-            {
+            if constexpr (NS > 1)
+                tmem_store_doubles<NRA * NCB>(tmem_acc + sb * (2 * NRA * NCB), &acc[0][0]);
+            if (sb == nsub - 1) {
                 const int slot = pc & 1;
                 mbar_wait(&red_empty[slot], ((pc >> 1) & 1) ^ 1);
                 double2* rb =
@@ -815,14 +963,21 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
             if (md.w & kLast) {
                 // flush the B01 face partial of this segment
                 double* dst = p.P01 + static_cast<int64_t>(s) * p.r0 * p.t1;
+                for (int q = 0; q < nsub; ++q) {
+                    const int jq = q * p.ts, wq = NS > 1 ? min(p.ts, t1e - jq) : t1e;
+                    if constexpr (NS > 1) {
+                        tmem_wait_st();
+                        tmem_load_doubles<NRA * NCB>(tmem_acc + q * (2 * NRA * NCB), &acc[0][0]);
+                    }
 #pragma unroll
-                for (int b = 0; b < NCB; ++b) {
-                    const int j = warp + NWC * b;
-                    if (j >= t1e) continue;
+                    for (int b = 0; b < NCB; ++b) {
+                        const int j = warp + NWC * b;
+                        if (j >= wq) continue;
 #pragma unroll
-                    for (int a = 0; a < NRA; ++a) {
-                        const int i = NRA * lane + 2 * ((a >> 1) ^ hsw) + (a & 1);
-                        if (i < r0e) dst[j * p.r0 + i] = acc[a][b];
+                        for (int a = 0; a < NRA; ++a) {
+                            const int i = NRA * lane + 2 * ((a >> 1) ^ hsw) + (a & 1);
+                            if (i < r0e) dst[(jq + j) * p.r0 + i] = acc[a][b];
+                        }
                     }
                 }
             }
@@ -830,6 +985,15 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1)
     }
     if constexpr (KO == 1) {
         if (pc > 0) reduce_pending();
+    }
+    if constexpr (NS > 1) {
+        tmem_wait_st();
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory");
+        if (warp == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        }
     }
     if (p.trace && threadIdx.x == 0) {
         unsigned long long t_end;
@@ -1111,6 +1275,8 @@ struct Level {
     int64_t MI0 = 0, MI1 = 0;  // merged view K I0 x I1/K (tiles live here)
     int nra = 4, ncb = 8, stages = 3;
     int nwc = 15;  // consumer warps (box kernel)
+    int ns = 1;    // column sub-strips per tile (accumulators in tensor memory when > 1)
+    int ts = 0;    // columns per box (= t1 when ns == 1)
     int stage_dbl = 0;
     int dyn_first = 0, ndyn = 0;  // dynamic-tail segments (box kernel only)
     bool tma = false;
@@ -1242,6 +1408,33 @@ void tile_level(Level& L, int num_sms) {
         L.G1 = static_cast<int>((L.MI1 + cm - 1) / cm);
         L.t1 = static_cast<int>((L.MI1 + L.G1 - 1) / L.G1);
         L.G1 = static_cast<int>((L.MI1 + L.t1 - 1) / L.t1);
+        L.ns = 1;
+        L.ts = L.t1;
+        // Sub-strips (tensor-memory accumulators, 128 x 56 shape only; development
+        // switch, see kSubStripsDefault): tiles of up to 4 boxes' width — the face
+        // has up to 4 x fewer column tiles and as many fewer C0 partial sets (C5:
+        // 9 -> 3, 384 MB less written and read again per sweep) — as long as the
+        // level keeps every SM busy.
+        static const char* ns_env = dev_env("R1_SWEEP_NS");
+        const int ns_max = ns_env ? std::max(1, std::min(4, std::atoi(ns_env))) : kSubStripsDefault;
+        if (L.nra == 4 && L.nwc == 7 && ns_max > 1 && L.G1 > 1) {
+            for (int ns = ns_max; ns > 1; --ns) {
+                const int g1 = static_cast<int>((L.MI1 + static_cast<int64_t>(cm) * ns - 1) / (static_cast<int64_t>(cm) * ns));
+                int t1 = static_cast<int>((L.MI1 + g1 - 1) / g1);
+                const int nsub = (t1 + cm - 1) / cm;       // boxes per regular tile
+                const int ts = (t1 + nsub - 1) / nsub;     // equal sub-strips
+                t1 = nsub * ts;
+                const int g1b = static_cast<int>((L.MI1 + t1 - 1) / t1);
+                static const char* mp_env = dev_env("R1_SWEEP_NS_MINP");  // development: panels per SM required
+                const int64_t minp = mp_env ? std::atoi(mp_env) : 64;
+                if (nsub < 2 || static_cast<int64_t>(L.G0) * g1b * L.O < minp * num_sms) continue;
+                L.ns = nsub;
+                L.ts = ts;
+                L.t1 = t1;
+                L.G1 = g1b;
+                break;
+            }
+        }
         L.ntiles = L.G0 * L.G1;
         // a single small face tile: KO panels per box amortise the per-panel
         // reductions (C4: 60 x 60 faces)
@@ -1256,8 +1449,8 @@ void tile_level(Level& L, int num_sms) {
                     break;
                 }
         const size_t red = static_cast<size_t>(2) * L.KO * L.nwc * rm * 8;
-        const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16 + 4 * 8;
-        const size_t box = static_cast<size_t>(L.r0) * L.t1 * 8 * L.KO;
+        const size_t bars = 2 * kMaxStages * 8 + kMaxStages * 16 + 4 * 8 + 16;  // + tensor-memory base slot
+        const size_t box = static_cast<size_t>(L.r0) * L.ts * 8 * L.KO;
         const size_t ring = kSmemBudget - red - bars - rm * 8 - 1024;
         L.stages = static_cast<int>(std::min<size_t>(kMaxStages, ring / box));
         L.stage_dbl = static_cast<int>(((box + 127) & ~size_t(127)) / 8);  // 128-B aligned
@@ -1553,9 +1746,9 @@ void launch_sweep_t(r1_context* ctx, const Level& L, const SweepArgs& a, const C
     check_launch(ctx, "sweep3_kernel");
 }
 
-template <int NRA, bool SR, int KO, int NCB = kBoxNCB, int NWC = kBoxNWC>
+template <int NRA, bool SR, int KO, int NCB = kBoxNCB, int NWC = kBoxNWC, int NS = 1>
 void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
-    auto kern = sweep3_box_kernel<NRA, NCB, NWC, SR, KO>;
+    auto kern = sweep3_box_kernel<NRA, NCB, NWC, SR, KO, NS>;
     configure_once(reinterpret_cast<const void*>(kern), ctx->device, [&] {
         R1_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBudget)));
@@ -1563,10 +1756,12 @@ void launch_box(r1_context* ctx, const Level& L, const SweepArgs& a) {
     BoxMaps maps;
     const int64_t rem0 = L.MI0 - static_cast<int64_t>(L.G0 - 1) * L.r0;
     const int64_t rem1 = L.MI1 - static_cast<int64_t>(L.G1 - 1) * L.t1;
-    maps.m[0] = make_map(a.A, L, L.r0, L.t1, KO);
-    maps.m[1] = make_map(a.A, L, rem0, L.t1, KO);
-    maps.m[2] = make_map(a.A, L, L.r0, rem1, KO);
-    maps.m[3] = make_map(a.A, L, rem0, rem1, KO);
+    // boxes are ts columns wide; the last box of the last column tile is narrower
+    const int64_t remlast = rem1 - ((rem1 + L.ts - 1) / L.ts - 1) * L.ts;
+    maps.m[0] = make_map(a.A, L, L.r0, L.ts, KO);
+    maps.m[1] = make_map(a.A, L, rem0, L.ts, KO);
+    maps.m[2] = make_map(a.A, L, L.r0, remlast, KO);
+    maps.m[3] = make_map(a.A, L, rem0, remlast, KO);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool timed = ctx->time_kernels && a.trace_level0;
     if (timed) {
@@ -1595,6 +1790,8 @@ void launch_sweep(r1_context* ctx, const Level& L, const SweepArgs& a) {
         } else if (L.nra == 8) {
             if (stage_regs) launch_box<8, true, 1, 2>(ctx, L, a);
             else launch_box<8, false, 1, 2>(ctx, L, a);
+        } else if (L.nra == 4 && L.nwc == 7 && L.ns > 1) {
+            launch_box<4, true, 1, 8, 7, 4>(ctx, L, a);
         } else if (L.nra == 4 && L.nwc == 7) {
             if (stage_regs) launch_box<4, true, 1, 8, 7>(ctx, L, a);
             else launch_box<4, false, 1, 8, 7>(ctx, L, a);
@@ -1717,6 +1914,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         s.W = Wsrc;
         s.r0 = L.r0;
         s.t1 = L.t1;
+        s.ts = L.ts > 0 ? L.ts : L.t1;
         s.G0 = L.G0;
         s.rbox = L.r0;
         s.segs = reinterpret_cast<const Seg*>(meta + L.seg_off);
@@ -1838,6 +2036,8 @@ void sweep_plan_info(r1_context* ctx, const uint64_t* dims, int order, int64_t* 
     info[10] = L.K;
     info[11] = L.KO;
     info[12] = L.ndyn;
+    info[13] = L.ns;
+    info[14] = L.ts;
 }
 
 }  // namespace r1

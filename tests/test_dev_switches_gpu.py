@@ -48,7 +48,7 @@ want = ref.solve("ihoscf", a, dims, tol=1e-8, max_iters=500, seed=0)
 assert got.converged and abs(got.result.lambda_ - want["lam"]) <= 1e-10 * want["lam"]
 # sweep (every block) against the oracle restatement
 from oracle import rank1_oracle as o
-for dims in ((200, 200, 7), (200, 64, 6, 5), (1000, 4, 3), (60, 60, 12, 5, 4)):
+for dims in ((200, 200, 7), (200, 64, 6, 5), (1000, 4, 3), (60, 60, 12, 5, 4), (136, 480, 40), (72, 500, 11)):
     a = o.oracle_random_tensor(dims, 3)
     f = o.oracle_random_unit_factors(dims, 4)
     got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
@@ -64,7 +64,8 @@ DEV_LIB = os.path.join(ROOT, "paper_2403_01778_b200", "librank1_b200_dev.so")
 @pytest.mark.parametrize("env", [{"R1_SOLVER_GRAPHS": "0"}, {"R1_BK_GRID_SOLVE": "1"},
                                  {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"}, {"R1_EIG_TILED": "0"},
                                  {"R1_SWEEP_NRA8": "0"}, {"R1_SWEEP_MERGE": "0"},
-                                 {"R1_SWEEP_WIDE": "0"}, {"R1_SWEEP_FORK": "0"}, {"R1_SWEEP_FORK": "2"}])
+                                 {"R1_SWEEP_WIDE": "0"}, {"R1_SWEEP_FORK": "0"}, {"R1_SWEEP_FORK": "2"},
+                                 {"R1_SWEEP_NS": "4", "R1_SWEEP_NS_MINP": "0"}])
 def test_switch_paths(gpu_ctx, env):
     if not os.path.exists(DEV_LIB):
         pytest.skip("development build not present (build.py --dev)")
