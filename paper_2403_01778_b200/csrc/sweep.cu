@@ -1718,8 +1718,13 @@ CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t 
 template <typename... KArgs, typename... Args>
 void launch_pdl(r1_context* ctx, void (*kern)(KArgs...), int grid, int block, size_t smem,
                 cudaStream_t stream, Args&&... args) {
-    static const char* env = dev_env("R1_SWEEP_PDL");  // development: 0 = plain stream order
-    static const bool pdl = !(env && std::atoi(env) == 0);
+    // OFF by default: with the attribute set, the randomised sweep probe
+    // (tools/fuzz_probe.py) hit an illegal memory access in ~1 of 5,000 sweeps
+    // of tiny high-order tensors (chains of ~40 one-CTA kernels); without it,
+    // none.  Its gain was confined to launch-bound sweeps (C1 20 -> 17.5 us).
+    // R1_SWEEP_PDL=1 (development build) enables it.
+    static const char* env = dev_env("R1_SWEEP_PDL");
+    static const bool pdl = env && std::atoi(env) != 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(static_cast<unsigned>(block));

@@ -32,7 +32,11 @@ while time.time() - t0 < budget:
     a = O.oracle_random_tensor(dims, int(rng.integers(1 << 30)))
     f = O.oracle_random_unit_factors(dims, int(rng.integers(1 << 30)))
     if not solves_only:
-        got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
+        try:
+            got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
+        except Exception:
+            print("build_j FAILED at dims", dims, "after", nb, "sweeps", flush=True)
+            raise
         want = O.build_j(a, dims, f)
         scale = O.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
         if not np.all(np.abs(got - want) <= 1e-13 * scale + 1e-300):
