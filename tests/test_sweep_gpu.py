@@ -116,6 +116,24 @@ def test_dynamic_tail_and_merged_classes_deterministic(gpu_ctx, oracle):
     assert np.all(np.abs(b0 - want) <= 1e-13 * scale + 1e-300)
 
 
+@pytest.mark.parametrize("dims", [(48, 46, 44, 45), (20, 22, 21, 24, 20), (64, 60, 36, 32)])
+def test_two_lane_recursion(gpu_ctx, oracle, dims):
+    """Tensors large enough (>= 2^22 elements, order >= 4) that the recursion
+    forks onto the side stream (root B01 second stage + C1 subtree beside the
+    C0 subtree): every block against the oracle, repeats
+    bit-identical."""
+    import paper_2403_01778_b200 as r1
+    assert int(np.prod(dims)) >= 1 << 22
+    a = oracle.oracle_random_tensor(dims, 31)
+    f = oracle.oracle_random_unit_factors(dims, 32)
+    t = r1.DenseTensor(dims, a)
+    b0 = r1.build_j(t, r1.FactorSet(0.0, f)).blocks
+    for _ in range(2):
+        assert np.array_equal(r1.build_j(t, r1.FactorSet(0.0, f)).blocks, b0)
+    scale = oracle.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
+    assert np.all(np.abs(b0 - oracle.build_j(a, dims, f)) <= 1e-13 * scale + 1e-300)
+
+
 def test_build_j_errors(gpu_ctx, oracle):
     """nepv.cpp:24-41 / test_nepv.cpp:104-107, 227-232."""
     import paper_2403_01778_b200 as r1
