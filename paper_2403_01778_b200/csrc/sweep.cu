@@ -22,10 +22,14 @@
 // Kernels: sweep3_box_kernel — persistent, one CTA per SM, one
 // producer warp streaming (tile, o) panels HBM -> shared memory with 3-D TMA
 // tensor-map loads (cp.async.bulk.tensor, L2 evict_first) into a byte-budgeted
-// mbarrier ring, 15 consumer warps keeping the B01 face tile in registers,
+// mbarrier ring, 7-11 consumer warps (32 elements per thread: 128 x 56,
+// 256 x 44 or 64 x 64 tiles; the 15-warp / 16-element shapes stay selectable
+// in the development build) keeping the B01 face tile in registers,
 // reducing C1 with a transposing warp butterfly and C0 through shared memory;
 // tiles are cut in whole 128-B lines (alignment classes), small faces put KO
-// o-panels in one box, the last 25% of the panels are scheduled dynamically.
+// o-panels in one box, the last 25% of the panels are scheduled dynamically
+// from a work counter the kernel re-arms itself.  The recursion's independent
+// subtrees run on two streams (sweep_blocks).
 // sweep3_kernel — the 1-D cp.async.bulk variant for odd I0 (no 16-B TMA
 // stride).  C0/C1/B01 partials over tiles / segments go to a workspace and are
 // summed in a fixed order by finish_kernel: no atomics anywhere, so results are
@@ -45,8 +49,8 @@ namespace {
 constexpr int kNWC = 8;                    // consumer warps
 constexpr int kThreads = (kNWC + 1) * 32;  // + one producer warp
 constexpr int kMaxOrder = 16;
-constexpr int kBoxNWC = 15;  // consumer warps of the TMA box kernel (+1 producer = 16 warps)
-constexpr int kBoxNCB = 4;   // columns per consumer warp (box = 32*NRA x 60)
+constexpr int kBoxNWC = 15;  // consumer warps of the 16-element box shapes (+1 producer = 16 warps)
+constexpr int kBoxNCB = 4;   // their columns per consumer warp (box = 32*NRA x 60)
 // sub-strips per tile of the 128 x 56 shape, accumulators in tensor memory
 // (R1_SWEEP_NS in the development build).  Built, bit-correct and measured
 // SLOWER (same box, C5 5.59 vs 5.17 ms, C2 1.43 vs 1.31 ms with 3 sub-strips):
@@ -1713,8 +1717,9 @@ CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t 
     return m;
 }
 
-// Launch on ctx->stream as a programmatic dependent of the preceding kernel
-// (the kernels call griddepcontrol.wait before touching global memory).
+// Launch a sweep kernel; with R1_SWEEP_PDL=1 (development build) as a
+// programmatic dependent of the preceding kernel (the kernels call
+// griddepcontrol.wait before touching global memory; a no-op otherwise).
 template <typename... KArgs, typename... Args>
 void launch_pdl(r1_context* ctx, void (*kern)(KArgs...), int grid, int block, size_t smem,
                 cudaStream_t stream, Args&&... args) {

@@ -1,7 +1,9 @@
 #!/bin/bash
+# dynamic-tail share / chunk with the wide shapes (development build)
 export R1_LIB_PATH=$PWD/paper_2403_01778_b200/librank1_b200_dev.so
-for i in 1 2 3; do echo "== PDL=1 fresh plans run $i =="; R1_SWEEP_PDL=1 timeout 120 python tools/pdl_hunt.py 6000 1 2>&1 | tail -1; done
-for i in 1 2; do echo "== PDL=1 cached plans run $i =="; R1_SWEEP_PDL=1 timeout 120 python tools/pdl_hunt.py 6000 0 2>&1 | tail -1; done
-echo "== PDL=1 WIDE=0 fresh =="; R1_SWEEP_PDL=1 R1_SWEEP_WIDE=0 timeout 120 python tools/pdl_hunt.py 6000 1 2>&1 | tail -1
-echo "== PDL=1 WIDE=0 fresh =="; R1_SWEEP_PDL=1 R1_SWEEP_WIDE=0 timeout 120 python tools/pdl_hunt.py 6000 1 2>&1 | tail -1
-echo "== PDL=0 fresh =="; R1_SWEEP_PDL=0 timeout 120 python tools/pdl_hunt.py 6000 1 2>&1 | tail -1
+for F in 0.25 0.15 0.35 0.25; do
+ for C in 8 4 16; do
+  echo "== FRAC=$F CHUNK=$C =="
+  R1_SWEEP_DYN_FRAC=$F R1_SWEEP_DYN_CHUNK=$C timeout 300 python tools/sweep_probe.py C5 C2 C3 --reps 20 2>&1 | grep "median" | sed 's/plan={.*nseg.: \([0-9]*\).*} median/nseg \1 median/'
+ done
+done
