@@ -253,6 +253,20 @@ struct r1_context {
 
 namespace r1 {
 
+// Host -> device upload of plan metadata / tables from pageable memory, complete
+// on return.  (A synchronous cudaMemcpy from pageable memory returns once the
+// data is STAGED; its DMA is ordered with the legacy default stream only, not
+// with the context's non-blocking stream — a kernel launched right behind it
+// could read the destination before the data landed.  Found with the
+// randomised sweep probe: new plans' segment tables read early.)
+inline void upload_now(r1_context* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    R1_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    R1_CUDA(cudaStreamIsCapturing(ctx->stream, &st));
+    if (st == cudaStreamCaptureStatusNone) R1_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 inline void count_launch(r1_context* ctx, uint64_t n = 1) { ctx->launches += n; }
 
 inline void check_launch(r1_context* ctx, const char* what) {

@@ -216,7 +216,7 @@ int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
                 all.insert(all.end(), u.begin(), u.end());
             }
             facbuf.ensure(tot * sizeof(double));
-            R1_CUDA(cudaMemcpy(facbuf.ptr, all.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
+            upload_now(ctx, facbuf.ptr, all.data(), tot * sizeof(double));
             uint64_t off = 0;
             for (int k = 0; k < order; ++k) {
                 a.fac[k] = facbuf.as<double>() + off;
@@ -256,7 +256,7 @@ int r1_generate_config(r1_context* ctx, r1_tensor* t, int cfg, uint64_t seed,
                     ek[(r - 1) * Ik + k] = std::exp(-static_cast<double>(r) * k / Ik);
             }
             tab.ensure(h.size() * sizeof(double));
-            R1_CUDA(cudaMemcpy(tab.ptr, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+            upload_now(ctx, tab.ptr, h.data(), h.size() * sizeof(double));
             a.tab = tab.as<double>();
         }
         const int g = 8 * ctx->num_sms;
@@ -304,7 +304,7 @@ int r1_generate(r1_context* ctx, r1_tensor* t, const char* name, uint64_t seed) 
         }
         if (!h.empty()) {
             tab.ensure(h.size() * sizeof(double));
-            R1_CUDA(cudaMemcpy(tab.ptr, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+            upload_now(ctx, tab.ptr, h.data(), h.size() * sizeof(double));
             a.tab = tab.as<double>();
         }
         named_gen_kernel<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(a);

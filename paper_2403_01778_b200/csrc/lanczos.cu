@@ -1530,7 +1530,7 @@ struct EigPlan {
 // Split the (pair, row chunk, column) units of the blocks into G contiguous
 // ranges of equal cost (rows of the chunk + a per-column overhead) and cut
 // them into segments (one row chunk each).
-void build_tiles(EigPlan& P, int G) {
+void build_tiles(r1_context* ctx, EigPlan& P, int G) {
     const BlockOp& op = P.op;
     LzTiles& tl = P.tl;
     tl = LzTiles{};
@@ -1599,9 +1599,9 @@ void build_tiles(EigPlan& P, int G) {
     const size_t off_rcf = off_cta + ((cta_bytes + 15) & ~size_t(15));
     P.tl_meta.ensure(off_rcf + rcf_bytes + 16);
     char* base = P.tl_meta.as<char>();
-    R1_CUDA(cudaMemcpy(base, segs.data(), seg_bytes, cudaMemcpyHostToDevice));
-    R1_CUDA(cudaMemcpy(base + off_cta, cta_seg.data(), cta_bytes, cudaMemcpyHostToDevice));
-    R1_CUDA(cudaMemcpy(base + off_rcf, rc_first.data(), rcf_bytes, cudaMemcpyHostToDevice));
+    upload_now(ctx, base, segs.data(), seg_bytes);
+    upload_now(ctx, base + off_cta, cta_seg.data(), cta_bytes);
+    upload_now(ctx, base + off_rcf, rc_first.data(), rcf_bytes);
     tl.segs = reinterpret_cast<const LzSeg*>(base);
     tl.cta_seg = reinterpret_cast<const int*>(base + off_cta);
     tl.meta = reinterpret_cast<const int*>(base + off_rcf);
@@ -1670,7 +1670,7 @@ void run_lanczos(r1_context* ctx, EigPlan& P, const double* x0, double* value_de
     // small operators take the single-cluster kernel below (unless overridden)
     const bool small_pref = n <= kSmallN && !gs && !gc && !(gsm && std::atoi(gsm) == 0);
     const bool tiled = !P.op.dense && !small_pref && !(cl_size > 1 && !gs) && !(tz && std::atoi(tz) == 0);
-    if (tiled && P.tl_G != grid_ctas) build_tiles(P, grid_ctas);
+    if (tiled && P.tl_G != grid_ctas) build_tiles(ctx, P, grid_ctas);
     const int64_t tl_n = tiled ? P.tl_coldot_n + P.tl_rowpart_n + 16 : 0;
     const int64_t need = n * (maxm + 1) + n + 2 * (maxm + 1) + 2 * maxm + 8 * ctx->num_sms +
                          2 * static_cast<int64_t>(ctx->num_sms) * (kMaxKrylov + 8) +

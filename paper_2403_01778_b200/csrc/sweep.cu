@@ -1672,8 +1672,7 @@ std::shared_ptr<SweepPlan> get_plan(r1_context* ctx, const uint64_t* dims, int o
     plan_rec(*P, dims, order, order, d, m, Ref{Where::Tensor, 0}, true, ctx->num_sms);
     P->meta.ensure(std::max<size_t>(16, P->host_meta.size() * sizeof(int)));
     P->counters.ensure(std::max<size_t>(1, P->levels.size()) * 64);
-    R1_CUDA(cudaMemcpy(P->meta.ptr, P->host_meta.data(), P->host_meta.size() * sizeof(int),
-                       cudaMemcpyHostToDevice));
+    upload_now(ctx, P->meta.ptr, P->host_meta.data(), P->host_meta.size() * sizeof(int));
     R1_CUDA(cudaMemsetAsync(P->counters.ptr, 0, std::max<size_t>(1, P->levels.size()) * 64, ctx->stream));
     ctx->plans[key] = P;
     return P;
@@ -1717,19 +1716,13 @@ CUtensorMap make_map(const double* A, const Level& L, int64_t box_rows, int64_t 
     return m;
 }
 
-// Launch a sweep kernel; with R1_SWEEP_PDL=1 (development build) as a
-// programmatic dependent of the preceding kernel (the kernels call
-// griddepcontrol.wait before touching global memory; a no-op otherwise).
+// Launch a sweep kernel as a programmatic dependent of the preceding kernel
+// (the kernels call griddepcontrol.wait before touching global memory).
 template <typename... KArgs, typename... Args>
 void launch_pdl(r1_context* ctx, void (*kern)(KArgs...), int grid, int block, size_t smem,
                 cudaStream_t stream, Args&&... args) {
-    // OFF by default: with the attribute set, the randomised sweep probe
-    // (tools/fuzz_probe.py) hit an illegal memory access in ~1 of 5,000 sweeps
-    // of tiny high-order tensors (chains of ~40 one-CTA kernels); without it,
-    // none.  Its gain was confined to launch-bound sweeps (C1 20 -> 17.5 us).
-    // R1_SWEEP_PDL=1 (development build) enables it.
-    static const char* env = dev_env("R1_SWEEP_PDL");
-    static const bool pdl = env && std::atoi(env) != 0;
+    static const char* env = dev_env("R1_SWEEP_PDL");  // development: 0 = plain stream order
+    static const bool pdl = !(env && std::atoi(env) == 0);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(static_cast<unsigned>(block));

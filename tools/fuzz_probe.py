@@ -16,7 +16,7 @@ from oracle import ref  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
-mode = sys.argv[3] if len(sys.argv) > 3 else ""  # "solves" / "hoscf": skip the sweep checks, solve every case
+mode = sys.argv[3] if len(sys.argv) > 3 else ""  # "solves" / "hoscf": skip the sweep checks, solve every case; "sweeps": no solves
 solves_only = mode in ("solves", "hoscf")
 O.build()
 t0 = time.time()
@@ -42,7 +42,10 @@ while time.time() - t0 < budget:
         if not np.all(np.abs(got - want) <= 1e-13 * scale + 1e-300):
             bad.append(("build_j", dims))
         nb += 1
-    if d >= 3 and np.prod(dims) <= 2e5 and min(dims) >= 2 and (solves_only or rng.random() < 0.25):
+    do_solve = solves_only or rng.random() < 0.25  # (drawn in every mode: same shape sequence)
+    if mode == "sweeps":
+        continue
+    if d >= 3 and np.prod(dims) <= 2e5 and min(dims) >= 2 and do_solve:
         alg = "hoscf" if mode == "hoscf" else ("ihoscf" if solves_only or rng.random() < 0.5 else "hoscf")
         seed = int(rng.integers(100))
         rep = r1.solve(alg, r1.DenseTensor(dims, a), r1.SolveOptions(tol=1e-10, max_iters=300, seed=seed))
