@@ -1,6 +1,5 @@
 #!/bin/bash
-export R1_LIB_PATH=$PWD/paper_2403_01778_b200/librank1_b200_dev.so
-for S in 51 52 53 54 55 56 57 58 59 60 61 62 63 64 65 66; do
-  echo "== PDL=1 sweeps only seed=$S =="
-  R1_SWEEP_PDL=1 timeout 200 python tools/fuzz_probe.py 30 $S sweeps 2>&1 | grep "FAILED\|fuzz:\|error" | cut -c1-160
-done
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/r02_bench_final.log 2>&1; tail -c 200 gpurun_out/r02_bench_final.log
+timeout 1200 python bench.py --impl reference > gpurun_out/r02_bench_ref_final.log 2>&1; tail -c 300 gpurun_out/r02_bench_ref_final.log
