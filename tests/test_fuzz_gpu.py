@@ -31,6 +31,25 @@ def test_random_sweeps(gpu_ctx, oracle):
         assert np.all(np.abs(got - want) <= 1e-13 * scale + 1e-300), dims
 
 
+def test_fresh_plans_high_order(gpu_ctx, oracle):
+    """A NEW sweep plan per shape on small order 4-6 tensors, each swept right
+    after its plan metadata went up (the window of the round-2 upload race:
+    a fresh plan's segment tables must be on the device before its first box
+    kernel, launched as a programmatic dependent, reads them)."""
+    import paper_2403_01778_b200 as r1
+    rng = np.random.default_rng(4242)
+    for _ in range(400):
+        d = int(rng.integers(4, 7))
+        cap = {4: 40, 5: 12, 6: 8}[d]
+        dims = tuple(int(rng.integers(1, cap + 1)) for _ in range(d))
+        a = oracle.oracle_random_tensor(dims, int(rng.integers(1 << 30)))
+        f = oracle.oracle_random_unit_factors(dims, int(rng.integers(1 << 30)))
+        got = r1.build_j(r1.DenseTensor(dims, a), r1.FactorSet(0.0, f)).blocks
+        want = oracle.build_j(a, dims, f)
+        scale = oracle.build_j_numpy(np.abs(a), dims, [np.abs(u) for u in f])
+        assert np.all(np.abs(got - want) <= 1e-13 * scale + 1e-300), dims
+
+
 def test_random_hoscf_solves(gpu_ctx, oracle, ref):
     import paper_2403_01778_b200 as r1
     rng = np.random.default_rng(77)
