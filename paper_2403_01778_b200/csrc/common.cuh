@@ -112,12 +112,18 @@ struct DescCache {
     bool used[N] = {};
     int next = 0;
     void* dev[N] = {};
+    // the upload of a pinned slot must have run before the host rewrites the
+    // slot (the host can be hundreds of launches ahead of the stream)
+    cudaEvent_t sent[N] = {};
+    bool sent_valid[N] = {};
     DescCache() = default;
     DescCache(const DescCache&) = delete;
     DescCache& operator=(const DescCache&) = delete;
     ~DescCache() {
         for (auto p : dev)
             if (p) cudaFree(p);
+        for (auto e : sent)
+            if (e) cudaEventDestroy(e);
         if (host) cudaFreeHost(host);
     }
     // All slots are allocated on the first (never captured) use, so a miss
@@ -126,14 +132,22 @@ struct DescCache {
         if (!host) {
             R1_CUDA(cudaMallocHost(&host, N * sizeof(T)));
             for (int i = 0; i < N; ++i) R1_CUDA(cudaMalloc(&dev[i], sizeof(T)));
+            for (int i = 0; i < N; ++i) R1_CUDA(cudaEventCreateWithFlags(&sent[i], cudaEventDisableTiming));
         }
         for (int i = 0; i < N; ++i)
             if (used[i] && std::memcmp(&host[i], &d, sizeof(T)) == 0) return static_cast<T*>(dev[i]);
         const int i = next;
         next = (next + 1) % N;
         used[i] = false;
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        R1_CUDA(cudaStreamIsCapturing(s, &cap));
+        if (sent_valid[i] && cap == cudaStreamCaptureStatusNone) R1_CUDA(cudaEventSynchronize(sent[i]));
         std::memcpy(&host[i], &d, sizeof(T));
         R1_CUDA(cudaMemcpyAsync(dev[i], &host[i], sizeof(T), cudaMemcpyHostToDevice, s));
+        if (cap == cudaStreamCaptureStatusNone) {
+            R1_CUDA(cudaEventRecord(sent[i], s));
+            sent_valid[i] = true;
+        }
         used[i] = true;
         return static_cast<T*>(dev[i]);
     }
