@@ -64,7 +64,7 @@ DEV_LIB = os.path.join(ROOT, "paper_2403_01778_b200", "librank1_b200_dev.so")
 @pytest.mark.parametrize("env", [{"R1_SOLVER_GRAPHS": "0"}, {"R1_BK_GRID_SOLVE": "1"},
                                  {"R1_EIG_SMALL": "0"}, {"R1_EIG_CLUSTER": "8"}, {"R1_EIG_TILED": "0"},
                                  {"R1_SWEEP_NRA8": "0"}, {"R1_SWEEP_MERGE": "0"},
-                                 {"R1_SWEEP_WIDE": "0"}, {"R1_SWEEP_FORK": "0"}, {"R1_SWEEP_FORK": "2"},
+                                 {"R1_SWEEP_WIDE": "0"}, {"R1_SWEEP_FORK": "0"}, {"R1_SWEEP_FORK": "1"},
                                  {"R1_SWEEP_NS": "4", "R1_SWEEP_NS_MINP": "0"}])
 def test_switch_paths(gpu_ctx, env):
     if not os.path.exists(DEV_LIB):
