@@ -1,5 +1,5 @@
 #!/bin/bash
-timeout 2400 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-for S in 11 21 31 41; do timeout 200 python tools/fuzz_probe.py 30 $S 2>&1 | grep "FAILED\|fuzz:\|error" | cut -c1-200; done
-timeout 300 python tools/fuzz_probe.py 90 14 hoscf 2>&1 | tail -2 | cut -c1-200
-timeout 200 python tools/decide_probe.py 2>&1 | tail -6 | cut -c1-200
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/r02_bench_final.log 2>&1; tail -c 200 gpurun_out/r02_bench_final.log
+timeout 1200 python bench.py --impl reference > gpurun_out/r02_bench_ref_final.log 2>&1; tail -c 300 gpurun_out/r02_bench_ref_final.log
