@@ -128,9 +128,9 @@ int r1_context_create(int device, r1_context** out);
 int r1_context_destroy(r1_context* ctx);
 /* Use a caller-owned cudaStream_t (e.g. torch's current stream) for every
  * subsequent launch on this context; NULL restores the context's own stream.
- * A sweep of an order >= 4 tensor also uses an internal side stream for the
- * independent half of its recursion; it is forked from and joined back into
- * this stream with events inside the call, so stream order (and a stream
+ * A sweep of an order >= 4 tensor also uses internal side streams for the
+ * independent chains of its recursion; they are forked from and joined back
+ * into this stream with events inside the call, so stream order (and a stream
  * capture) on the caller's stream covers all of the call's work. */
 int r1_context_set_stream(r1_context* ctx, void* cuda_stream);
 int r1_context_synchronize(r1_context* ctx);

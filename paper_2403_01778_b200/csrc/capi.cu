@@ -152,8 +152,11 @@ int r1_context_create(int device, r1_context** out) {
         ctx->smem_optin = prop.sharedMemPerBlockOptin;
         R1_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
-        R1_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+        for (auto& st : ctx->side_streams) R1_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        ctx->side_stream = ctx->side_streams[0];
         for (auto& e : ctx->ev_sweep) R1_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ctx->ev_done) R1_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ctx->ev_join) R1_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *out = ctx;
     });
 }
@@ -170,11 +173,16 @@ int r1_context_destroy(r1_context* ctx) {
         ctx->plans.clear();
         if (ctx->comm) ctx->comm->ctx = nullptr;  // the communicator outlives its context
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
-        if (ctx->side_stream) {
-            cudaStreamSynchronize(ctx->side_stream);
-            cudaStreamDestroy(ctx->side_stream);
-        }
+        for (auto st : ctx->side_streams)
+            if (st) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+            }
         for (auto e : ctx->ev_sweep)
+            if (e) cudaEventDestroy(e);
+        for (auto e : ctx->ev_done)
+            if (e) cudaEventDestroy(e);
+        for (auto e : ctx->ev_join)
             if (e) cudaEventDestroy(e);
         delete ctx;
     });

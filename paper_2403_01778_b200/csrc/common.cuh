@@ -236,8 +236,11 @@ struct r1_context {
     cudaStream_t stream = nullptr;
     // second lane of a sweep (sweep.cu): independent subtrees of the recursion
     // and the B01 second stage run beside the main stream, joined by events
-    cudaStream_t side_stream = nullptr;
-    cudaEvent_t ev_sweep[3] = {nullptr, nullptr, nullptr};  // root box done, root C1 done, side joined
+    cudaStream_t side_stream = nullptr;                    // lane 1 (= side_streams[0])
+    cudaStream_t side_streams[3] = {nullptr, nullptr, nullptr};  // lanes 1..3
+    cudaEvent_t ev_sweep[3] = {nullptr, nullptr, nullptr};  // [0] root box kernel done
+    cudaEvent_t ev_done[16] = {};   // outputs of the spine level at depth k done
+    cudaEvent_t ev_join[3] = {};    // lane 1..3 finished
     uint64_t launches = 0;
     unsigned long long* dbg_sweep_trace = nullptr;  // diagnostics: per-CTA timing of level 0
     // diagnostics: CUDA events around every top-level sweep kernel launch

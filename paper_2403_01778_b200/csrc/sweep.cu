@@ -1291,7 +1291,13 @@ struct Level {
     // outputs
     Ref out_b01, out_c0, out_c1;
     Ref w, p01, p0, p1;
-    int lane = 0;  // 1: in the root's C1 subtree (runs on the side stream)
+    // Lanes: the levels whose blocks are all needed form a spine (root, its C0
+    // child, that one's C0 child, ...) on lane 0; the C1 child of the spine
+    // level at depth k starts a chain (each of its levels has one child) on lane
+    // 1 + k % 3, which depends only on that spine level's C0 / C1.
+    int lane = 0;
+    int depth = 0;          // spine depth of this level (lane 0) or of the chain's parent
+    bool chain_head = false;  // first level of a chain: waits for the spine level at `depth`
 };
 
 }  // namespace
@@ -1590,9 +1596,11 @@ void partition_level(Level& L, int num_sms, std::vector<int>& meta) {
 // need_all: also produce the blocks among modes >= 2 of this sub-problem.
 void plan_rec(SweepPlan& P, const uint64_t* full_dims, int full_order, int order,
               const int64_t* dims, const int* modes, Ref input, bool need_all, int num_sms,
-              int lane = 0) {
+              int lane = 0, int depth = 0, bool chain_head = false) {
     Level L;
     L.lane = lane;
+    L.depth = depth;
+    L.chain_head = chain_head;
     L.order = order;
     for (int k = 0; k < order; ++k) {
         L.dims[k] = dims[k];
@@ -1644,14 +1652,16 @@ void plan_rec(SweepPlan& P, const uint64_t* full_dims, int full_order, int order
             m0[k - 1] = modes[k];
         }
         const Ref c0 = L.out_c0, c1 = L.out_c1;
-        plan_rec(P, full_dims, full_order, order - 1, d0, m0, c0, need_all, num_sms, lane);
+        // the C0 child continues its parent's lane (the spine: depth + 1; a chain: same depth)
+        plan_rec(P, full_dims, full_order, order - 1, d0, m0, c0, need_all, num_sms, lane,
+                 need_all ? depth + 1 : depth, false);
         if (need_c1) {
             d0[0] = dims[1];
             m0[0] = modes[1];
-            // the root's C1 subtree shares nothing with its C0 subtree (disjoint
-            // work regions, disjoint final blocks): second lane
-            plan_rec(P, full_dims, full_order, order - 1, d0, m0, c1, false, num_sms,
-                     order == full_order ? 1 : lane);
+            // a spine level's C1 subtree shares nothing with its C0 subtree
+            // (disjoint work regions, disjoint final blocks): its own lane
+            plan_rec(P, full_dims, full_order, order - 1, d0, m0, c1, false, num_sms, 1 + depth % 3, depth,
+                     true);
         }
     }
 }
@@ -1859,35 +1869,37 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
 
     // (the dynamic-tail counters are zeroed at plan creation and re-armed by the
     // box kernel itself)
-    // Two lanes.  The children of the root need only its C0 / C1, not B01, and
-    // its two subtrees are independent: the root's B01 second stage and its C1
-    // subtree run on the side stream beside the C0 / C1 second stage and the C0
-    // subtree (C4: 18 small kernels of ~190 us in a chain become two chains of
-    // ~70 us).  Forked after the root's box kernel, joined at the end — inside
-    // a stream capture the side stream joins the capture the same way.
+    // Lanes.  The children of a level need only its C0 / C1, not B01, and its two
+    // subtrees are independent: the root's B01 second stage and every spine
+    // level's C1 chain (Level::lane) run on side streams beside the spine (C4:
+    // 18 small kernels of ~190 us in a chain become chains of <= ~60 us).
+    // Forked with events after the producing level's second stage, joined at
+    // the end — inside a stream capture the side streams join the capture the
+    // same way.
     static const char* fork_env = dev_env("R1_SWEEP_FORK");
-    // 0 never, 1 tensors of >= 2^22 elements only, 2 (default) whenever the plan has two lanes:
+    // 0 never, 1 tensors of >= 2^22 elements only, 2 (default) whenever the plan has chains:
     // small high-order tensors gain the most (16^5 76 -> 55 us, 40^4 38 -> 31 us, 10^6 143 -> 111 us)
     const int fork_mode = fork_env ? std::atoi(fork_env) : 2;
     const Level& root = P->levels.front();
     const bool root_seg = root.nseg >= 64 * root.ntiles;
     const bool fork = ctx->side_stream && fork_mode != 0 && (fork_mode == 2 || n >= (uint64_t(1) << 22)) &&
-                      (P->levels.size() > 1 && (root_seg || P->levels.back().lane == 1));
+                      P->levels.size() > 1;
     cudaStream_t const main_stream = ctx->stream;
     struct StreamGuard {
         r1_context* c;
         cudaStream_t s;
         ~StreamGuard() { c->stream = s; }
     } guard{ctx, main_stream};
-    bool side_used = false, side_has_c1 = false;
+    bool lane_used[4] = {true, false, false, false};
     int level_idx = 0;
     for (const Level& L : P->levels) {
-        const bool on_side = fork && L.lane == 1;
-        if (on_side && !side_has_c1) {
-            R1_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sweep[1], 0));
-            side_has_c1 = side_used = true;
+        const int lane = fork ? L.lane : 0;
+        cudaStream_t const lane_stream = lane == 0 ? main_stream : ctx->side_streams[lane - 1];
+        if (lane != 0 && L.chain_head) {
+            R1_CUDA(cudaStreamWaitEvent(lane_stream, ctx->ev_done[L.depth], 0));
+            lane_used[lane] = true;
         }
-        ctx->stream = on_side ? ctx->side_stream : main_stream;
+        ctx->stream = lane_stream;
         const bool is_root = &L == &root;
         // outer weights
         OuterArgs oa{};
@@ -1979,9 +1991,9 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         fastdiv_init(L.I1, f.m_I1, f.s_I1);
         fastdiv_init(L.r0, f.m_r0, f.s_r0);
         fastdiv_init(L.t1, f.m_t1, f.s_t1);
-        // the root's children wait for its C0 / C1 only (event 1, recorded below)
+        // a spine level's C1 chain waits for its C0 / C1 only (recorded below)
         auto root_outputs_done = [&]() {
-            if (is_root && fork) R1_CUDA(cudaEventRecord(ctx->ev_sweep[1], main_stream));
+            if (fork && L.lane == 0 && L.order >= 4) R1_CUDA(cudaEventRecord(ctx->ev_done[L.depth], main_stream));
         };
         if (L.nseg >= 64 * L.ntiles) {
             // many segments per tile: B01 by segment slices, C0/C1 (if any) below
@@ -1992,7 +2004,7 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
                 R1_CUDA(cudaEventRecord(ctx->ev_sweep[0], main_stream));
                 R1_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sweep[0], 0));
                 bs = ctx->side_stream;
-                side_used = true;
+                lane_used[1] = true;
             }
             launch_pdl(ctx, finish_b01_seg_kernel, grid, kB01Warps * 32, 0, bs, f);
             check_launch(ctx, "finish_b01_seg_kernel");
@@ -2018,10 +2030,11 @@ void sweep_blocks(r1_context* ctx, const double* a, const uint64_t* dims, int or
         root_outputs_done();
     }
     ctx->stream = main_stream;
-    if (side_used) {
-        R1_CUDA(cudaEventRecord(ctx->ev_sweep[2], ctx->side_stream));
-        R1_CUDA(cudaStreamWaitEvent(main_stream, ctx->ev_sweep[2], 0));
-    }
+    for (int l = 1; l < 4; ++l)
+        if (lane_used[l]) {
+            R1_CUDA(cudaEventRecord(ctx->ev_join[l - 1], ctx->side_streams[l - 1]));
+            R1_CUDA(cudaStreamWaitEvent(main_stream, ctx->ev_join[l - 1], 0));
+        }
 }
 
 // Introspection for tests / DESIGN.md: the plan of the top level.
