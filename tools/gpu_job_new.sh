@@ -1,5 +1,6 @@
 #!/bin/bash
-mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/r02_bench_final.log 2>&1; tail -c 200 gpurun_out/r02_bench_final.log
-timeout 1200 python bench.py --impl reference > gpurun_out/r02_bench_ref_final.log 2>&1; tail -c 300 gpurun_out/r02_bench_ref_final.log
+# soak at HEAD (release library): mixed sweeps + solves, short processes
+for S in 101 102 103 104 105 106 107 108; do
+    timeout 200 python tools/fuzz_probe.py 30 $S 2>&1 | grep "FAILED\|fuzz:\|error" | cut -c1-200
+done
+timeout 200 python tools/bk_fuzz_probe.py 40 9 2>&1 | tail -1 | cut -c1-200
